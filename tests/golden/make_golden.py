@@ -1,0 +1,156 @@
+"""Generate the golden parity fixtures by running the REAL reference.
+
+Run in the build container only (needs /root/reference, read-only):
+
+    python tests/golden/make_golden.py
+
+Every case stores the inputs it was fed (or the seed recipe plus a sha256 of
+the bytes when the input is large and regenerable with plain numpy) and the
+reference outputs. The fixtures travel with the repo; nothing at test time
+reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+import scipy.sparse as sp
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def uniform_x(m, n, seed):
+    """cfg1-style input: fp32-representable uniform values."""
+    return np.random.default_rng(seed).random((m, n, n), dtype=np.float32)
+
+
+def main():
+    sys.path.insert(0, REF)
+    import rescalkit as rk
+    from rescalkit.dist_rescal import perturbation_field
+
+    out = {}
+
+    # 1. config 1: dense m=8, n=256, k=4, 200 tracked iterations, fp64 oracle on
+    #    fp32-representable X with random_init(256, 4, 8, 0) as the start.
+    x32 = uniform_x(8, 256, 0)
+    x = rk.RelTensor(x32.astype(np.float64))
+    f0 = rk.random_init(256, 4, 8, 0)
+    f, tr = rk.rescal_solve(x, 4, rk.SolverConfig(max_iters=200), initial=f0)
+    out["cfg1_uniform"] = dict(x_recipe=np.array([8, 256, 0]), x_sha=_sha(x32), A0=f0.A, R0=f0.R,
+                               A=f.A, R=f.R, trace=tr)
+    fu, tru = rk.rescal_solve(x, 4, rk.SolverConfig(max_iters=200, track_error=False), initial=f0)
+    out["cfg1_untracked"] = dict(A=fu.A, R=fu.R, trace_len=np.array(len(tru)))
+
+    # 2. planted, lightly noised (synth.generate), small enough to store X
+    xp, ap, rp = rk.generate(rk.SynthSpec(n=64, m=4, k_true=4, noise=0.01, seed=1))
+    f0p = rk.random_init(64, 4, 4, 3)
+    fp, trp = rk.rescal_solve(xp, 4, rk.SolverConfig(max_iters=300), initial=f0p)
+    out["planted64"] = dict(X=xp.slices, A0=f0p.A, R0=f0p.R, A=fp.A, R=fp.R, trace=trp)
+
+    # 3. exact recovery with a tolerance stop (test_rescal.py:119-122 shape)
+    xe, _, _ = rk.generate(rk.SynthSpec(n=16, m=4, k_true=3, noise=0.0, seed=1, pedestal=0.15))
+    fe, tre = rk.rescal_solve(xe, 3, rk.SolverConfig(max_iters=2000, tolerance=1e-4, seed=11))
+    fe0 = rk.random_init(16, 3, 4, 11)
+    out["exact16_tol"] = dict(X=xe.slices, A0=fe0.A, R0=fe0.R, A=fe.A, R=fe.R, trace=tre)
+
+    # 4. all-ones rank one (test_rescal.py:110-117)
+    xo = rk.RelTensor(np.ones((1, 2, 2)))
+    fo, tro = rk.rescal_solve(xo, 1, rk.SolverConfig(max_iters=2000, tolerance=1e-8, seed=3))
+    no = rk.finalize_normalize(fo)
+    out["all_ones"] = dict(X=xo.slices, A=fo.A, R=fo.R, trace=tro, An=no.A, Rn=no.R)
+
+    # 5. split API single steps and rel_error on a small random tensor
+    rng = np.random.default_rng(27)
+    xs = rng.random((3, 7, 7))
+    f0s = rk.random_init(7, 2, 3, 28)
+    fr = rk.update_r(rk.RelTensor(xs), f0s)
+    fa = rk.update_a(rk.RelTensor(xs), f0s)
+    fsplit = rk.update_a(rk.RelTensor(xs), fr)
+    out["split7"] = dict(X=xs, A0=f0s.A, R0=f0s.R, R_upd=fr.R, A_upd=fa.A, A_split=fsplit.A,
+                         R_split=fsplit.R, rel_err=np.array(rk.rel_error(rk.RelTensor(xs), f0s)))
+
+    # 6. fp32 end-to-end (test_rescal.py:150-154)
+    x32s = np.random.default_rng(12).random((2, 8, 8)).astype(np.float32)
+    f32, tr32 = rk.rescal_solve(rk.RelTensor(x32s), 2, rk.SolverConfig(max_iters=20, seed=1))
+    out["fp32_small"] = dict(X=x32s, A=f32.A, R=f32.R, trace=tr32)
+
+    # 7. regress_r / rel_error with frozen A (test_rescal.py:249-254 shape)
+    xr, ar, rr = rk.generate(rk.SynthSpec(n=16, m=3, k_true=3, noise=0.0, seed=21))
+    rfit = rk.regress_r(xr, ar)
+    out["regress16"] = dict(X=xr.slices, A=ar, R_true=rr, R_fit=rfit,
+                            err=np.array(rk.rel_error(xr, rk.RescalFactors(ar, rfit))))
+
+    # 8. finalize_normalize
+    fn0 = rk.random_init(9, 3, 2, 17)
+    fn = rk.finalize_normalize(fn0)
+    out["normalize"] = dict(A0=fn0.A, R0=fn0.R, A=fn.A, R=fn.R)
+
+    # 9. perturbation field / perturb (dense and sparse)
+    pc = rk.PerturbConfig(delta=0.02, base_seed=5)
+    fld = perturbation_field(9, 2, pc, (3, 4))
+    xd = np.random.default_rng(11).random((2, 9, 9))
+    pdense = rk.perturb(rk.RelTensor(xd), pc, (3, 4))
+    xsp = rk.sparsify(rk.RelTensor(xd), 0.3)
+    psp = rk.perturb(xsp, pc, (3, 4))
+    out["perturb9"] = dict(field=fld, X=xd, Xp=pdense.slices,
+                           sp_indptr=np.stack([s.indptr for s in xsp.slices]),
+                           sp_indices=np.concatenate([s.indices for s in xsp.slices]),
+                           sp_data=np.concatenate([s.data for s in xsp.slices]),
+                           sp_nnz=np.array([s.nnz for s in xsp.slices]),
+                           psp_data=np.concatenate([s.data for s in psp.slices]),
+                           psp_indices=np.concatenate([s.indices for s in psp.slices]))
+
+    # 10. CSR canonicalisation: duplicates, explicit zeros, unsorted columns
+    r_ = np.array([0, 0, 1, 2, 2, 2, 3, 3, 0])
+    c_ = np.array([2, 1, 0, 3, 3, 1, 0, 0, 2])
+    v_ = np.array([1.0, 2.0, 0.0, 0.5, 0.25, 3.0, 1.0, -1.0, 4.0])
+    coo = sp.coo_matrix((v_, (r_, c_)), shape=(4, 4))
+    canon = rk.SparseRelTensor([coo]).slices[0]
+    out["csr_canon"] = dict(rows=r_, cols=c_, vals=v_, indptr=canon.indptr, indices=canon.indices,
+                            data=canon.data)
+
+    # 11. sparse solve equals dense solve (test_dist_rescal.py:190-198 shape)
+    xsd = rk.sparsify(rk.RelTensor(np.random.default_rng(14).random((2, 12, 12))), 0.15)
+    fs_, ts_ = rk.rescal_solve(xsd, 2, rk.SolverConfig(max_iters=40, seed=3))
+    fs0 = rk.random_init(12, 2, 2, 3)
+    out["sparse12"] = dict(X=xsd.to_dense().slices, A0=fs0.A, R0=fs0.R, A=fs_.A, R=fs_.R, trace=ts_)
+
+    # 12. grid solve p=4 with padding (test_dist_rescal.py:55-63 shape)
+    xg = rk.RelTensor(np.random.default_rng(3).random((2, 7, 7)))
+    fg, tg, _ = rk.solve_on_grid(xg, 2, rk.SolverConfig(max_iters=40, seed=4), 4)
+    out["grid7_p4"] = dict(X=xg.slices, A=fg.A, R=fg.R, trace=tg)
+
+    # 13. RESCALk on a planted tensor (test_model_select.py:270-282 shape)
+    xk, _, _ = rk.generate(rk.SynthSpec(n=16, m=3, k_true=3, noise=0.01, seed=5))
+    rep = rk.rescalk(xk, 2, 4, r=4, cfg=rk.SolverConfig(max_iters=120, seed=6),
+                     pcfg=rk.PerturbConfig(delta=0.02, base_seed=6))
+    out["rescalk16"] = dict(
+        X=xk.slices, k_opt=np.array(rep.k_opt), low_conf=np.array(rep.low_confidence),
+        ks=np.array([e.k for e in rep.entries]),
+        s_min=np.array([e.s_min for e in rep.entries]),
+        s_avg=np.array([e.s_avg for e in rep.entries]),
+        rel_error=np.array([e.rel_error for e in rep.entries]),
+        **{f"medians_k{e.k}": e.medians for e in rep.entries},
+        **{f"core_k{e.k}": e.core for e in rep.entries},
+    )
+
+    import numpy, scipy
+    meta = dict(numpy=numpy.__version__, scipy=scipy.__version__, reference=REF)
+    for name, d in out.items():
+        d = dict(d)
+        d["meta"] = np.array(repr(meta))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+        print("wrote", name)
+
+
+if __name__ == "__main__":
+    main()
