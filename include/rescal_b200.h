@@ -1,0 +1,142 @@
+/*
+ * rescal_b200.h — C-ABI of the B200-native RESCAL multiplicative-update engine.
+ *
+ * This is the drop-in boundary for the reference's MU hot path. The reference
+ * (rescalkit, pure Python) has no FFI of its own; its internal swap seam is
+ * `_mu_iteration(x_ops, a_row, a_col, r, eps, hooks, counters)`
+ * (pkg/src/rescalkit/rescal.py:114-146) driven by `rescal_solve`
+ * (rescal.py:186-225). Each entry point below names the reference function
+ * it replaces. Plain pointers and sizes only; the Python mirror of the
+ * reference API (paper_2202_09512_b200/) binds these with ctypes, and
+ * INTEGRATION.md shows the binding a rescalkit maintainer would add.
+ *
+ * Conventions
+ *   - Every call returns an rk_status; on failure rk_last_error() returns a
+ *     thread-local message. Status classes map 1:1 onto the reference's
+ *     exception hierarchy (errors.py:4-21): DATA -> DataError,
+ *     NUMERICAL -> NumericalError, GRID -> GridError, DEVICE -> a CUDA/NCCL
+ *     failure (no reference equivalent; raised as RescalkitError).
+ *   - Host buffers are BORROWED for the duration of a call (copied to/from
+ *     the device). Device buffers are OWNED by the handle and released by
+ *     rk_destroy. A handle is bound to one device and one host thread.
+ *   - Factors cross the boundary as float64 (row-major A (n,k), R (m,k,k)),
+ *     whatever the tensor dtype; the Python layer casts to x.dtype the way
+ *     rescal.py:205-209 does.
+ */
+#ifndef RESCAL_B200_H
+#define RESCAL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RK_OK = 0,
+  RK_ERR_DATA = 1,      /* DataError      (errors.py:8)  */
+  RK_ERR_NUMERICAL = 2, /* NumericalError (errors.py:12) */
+  RK_ERR_GRID = 3,      /* GridError      (errors.py:16) */
+  RK_ERR_DEVICE = 4     /* CUDA / NCCL failure           */
+} rk_status;
+
+typedef enum { RK_F32 = 0, RK_F64 = 1 } rk_dtype;
+
+typedef enum {
+  RK_ENGINE_AUTO = 0, /* tcgen05 when k fits TMEM, else SIMT            */
+  RK_ENGINE_TC = 1,   /* tcgen05 3xBF16 split-precision slice contraction */
+  RK_ENGINE_SIMT = 2  /* CUDA-core fp32 slice contraction (large k)       */
+} rk_engine;
+
+typedef struct rk_handle rk_handle;
+
+/* Library identification / last error (thread-local). */
+int rk_version(void);
+const char* rk_last_error(void);
+int rk_device_count(int* out);
+
+/* Create an engine for a dense tensor with m slices of n x n, rank k.
+ * Replaces the setup half of rescal_solve (rescal.py:194-209). The tensor is
+ * stored on the device as two bf16 planes (hi, lo) per element, zero padded
+ * to a multiple of 128; k is padded to a multiple of 16 (exact: zero factor
+ * entries stay zero under MU, rescal.py:144 / dist_rescal.py:15-16). */
+int rk_create(int device, int64_t n, int64_t m, int32_t k, int32_t engine, rk_handle** out);
+void rk_destroy(rk_handle* h);
+
+/* Host tensor -> device. x is (m, n, n) C-contiguous in `dtype`. Replaces the
+ * dense RelTensor.slice_ops() operand view (tensor.py:67-69). Also records
+ * ||X||^2 in fp64 from the host values (rescal.py:160-165). */
+int rk_upload_dense(rk_handle* h, const void* x, int32_t dtype);
+
+/* Same, but for one rank's block of a p_r x p_c grid: x is (m, rows, cols)
+ * C-contiguous and lands in the top-left corner of the padded slices. */
+int rk_upload_block(rk_handle* h, const void* x, int32_t dtype, int64_t rows, int64_t cols,
+                    double sq_norm_global);
+
+/* Synthetic device-resident input (benchmarks): x = uniform [0,1) drawn with
+ * a counter-based hash of (seed, t, i, j), rounded to fp32. */
+int rk_fill_uniform(rk_handle* h, uint64_t seed);
+
+/* Factors in/out (fp64, unpadded). Replaces the `initial` copy-in
+ * (rescal.py:198-201) and the RescalFactors return (rescal.py:225). */
+int rk_set_factors(rk_handle* h, const double* A, const double* R);
+int rk_get_factors(rk_handle* h, double* A, double* R);
+
+/* Run up to `iters` MU iterations (rescal.py:215-224 loop around
+ * _mu_iteration, rescal.py:114-146). track_error!=0 writes the relative error
+ * after each iteration into trace_out[0..*iters_done) (rescal.py:218-222);
+ * tol<0 means no tolerance; the loop stops as soon as err < tol
+ * (rescal.py:223-224). Non-finite factors -> RK_ERR_NUMERICAL
+ * (rescal.py:168-170,217,220-221). */
+int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double tol,
+           double* trace_out, int32_t* iters_done);
+
+/* Split API: update_r (rescal.py:228-240) and update_a (rescal.py:243-258)
+ * applied to the factors held by the handle. */
+int rk_update_r(rk_handle* h, double eps);
+int rk_update_a(rk_handle* h, double eps);
+
+/* sum_t ||X_t - A R_t A^T||^2 (direct, rescal.py:149-157) and ||X||^2 for the
+ * factors held by the handle; rel_error = sqrt(res/norm) (rescal.py:269-276). */
+int rk_residual(rk_handle* h, double* sq_residual, double* sq_norm);
+
+/* regress_r (rescal.py:293-324): with A fixed (the handle's A), fit R from
+ * all-ones cores; result is left in the handle (read with rk_get_factors). */
+int rk_regress_r(rk_handle* h, int32_t max_iters, double tol, double eps, int32_t* iters_done);
+
+/* Multiply the device tensor by the RESCALk resampling field
+ * 1 + delta*(2u-1), u = PCG64 doubles (dist_rescal.py:164-171,205-215).
+ * (state_hi, state_lo, inc_hi, inc_lo) is numpy's PCG64 state after seeding
+ * from SeedSequence((base_seed, 3, q)); element e = t*n*n + i*n + j consumes
+ * draw e. The original tensor is kept; rk_perturb always starts from it.
+ * row0/col0 and n_global locate a grid block inside the global tensor. */
+int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+               uint64_t inc_lo, double delta, int64_t n_global, int64_t row0, int64_t col0,
+               const int64_t* col_map);
+
+/* Multi-GPU p_r x p_c grid (dist_rescal.py:113-161 generalised to non-square
+ * grids). nccl_id is a 128-byte ncclUniqueId broadcast by the caller. The
+ * handle then holds the (m, n/p_r, n/p_c) block of rank (i, j); A pieces of
+ * b = ceil(n/p) rows; rank (i,j) owns piece i*p_c+j. */
+int rk_grid_init(rk_handle* h, int32_t pr, int32_t pc, int32_t rank, const void* nccl_id,
+                 int64_t n_global);
+int rk_nccl_unique_id(void* out128);
+
+/* Timing of the last rk_run (device time, CUDA events on the engine stream):
+ * out[0]=total ms, out[1]=slice-contraction (K1) ms per launch averaged,
+ * out[2]=number of K1 launches, out[3]=kernel launches total. */
+int rk_last_timing(rk_handle* h, double* out, int32_t n_out);
+
+/* Raw stream handle (cudaStream_t) for callers that time on it. */
+void* rk_stream(rk_handle* h);
+
+/* Engine introspection: out[0]=engine used, out[1]=n_pad, out[2]=k_pad,
+ * out[3]=strip tiles (TC), out[4]=CTAs (TC), out[5]=smem bytes (TC). */
+int rk_info(rk_handle* h, int64_t* out, int32_t n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESCAL_B200_H */

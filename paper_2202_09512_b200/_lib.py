@@ -1,0 +1,283 @@
+"""ctypes binding of librescal_b200.so (include/rescal_b200.h).
+
+The product path has no CPU fallback: if the CUDA library is missing or no
+Blackwell GPU is visible, every solver entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .exceptions import DataError, GridError, NumericalError, RescalkitError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librescal_b200.so")
+
+RK_OK, RK_ERR_DATA, RK_ERR_NUMERICAL, RK_ERR_GRID, RK_ERR_DEVICE = range(5)
+RK_F32, RK_F64 = 0, 1
+ENGINES = {"auto": 0, "tc": 1, "simt": 2}
+
+
+class DeviceError(RescalkitError):
+    """CUDA / NCCL failure inside the engine (no reference equivalent)."""
+
+
+_EXC = {RK_ERR_DATA: DataError, RK_ERR_NUMERICAL: NumericalError, RK_ERR_GRID: GridError,
+        RK_ERR_DEVICE: DeviceError}
+
+_i32, _i64, _u64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+_vp = ctypes.c_void_p
+_pd = ctypes.POINTER(ctypes.c_double)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+_pf = ctypes.POINTER(ctypes.c_float)
+
+# name -> (restype, argtypes); mirrors include/rescal_b200.h plus the
+# engine-private helpers declared at the end of this table.
+SIGNATURES = {
+    "rk_version": (ctypes.c_int, []),
+    "rk_last_error": (ctypes.c_char_p, []),
+    "rk_device_count": (ctypes.c_int, [_pi32]),
+    "rk_create": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i32, _i32, ctypes.POINTER(_vp)]),
+    "rk_destroy": (None, [_vp]),
+    "rk_upload_dense": (ctypes.c_int, [_vp, _vp, _i32]),
+    "rk_upload_block": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _f64]),
+    "rk_fill_uniform": (ctypes.c_int, [_vp, _u64]),
+    "rk_set_factors": (ctypes.c_int, [_vp, _pd, _pd]),
+    "rk_get_factors": (ctypes.c_int, [_vp, _pd, _pd]),
+    "rk_run": (ctypes.c_int, [_vp, _i32, _f64, _i32, _f64, _pd, _pi32]),
+    "rk_update_r": (ctypes.c_int, [_vp, _f64]),
+    "rk_update_a": (ctypes.c_int, [_vp, _f64]),
+    "rk_residual": (ctypes.c_int, [_vp, _pd, _pd]),
+    "rk_regress_r": (ctypes.c_int, [_vp, _i32, _f64, _f64, _pi32]),
+    "rk_perturb": (ctypes.c_int, [_vp, _u64, _u64, _u64, _u64, _f64, _i64, _i64, _i64, _pi64]),
+    "rk_grid_init": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _i64]),
+    "rk_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "rk_last_timing": (ctypes.c_int, [_vp, _pd, _i32]),
+    "rk_stream": (_vp, [_vp]),
+    "rk_info": (ctypes.c_int, [_vp, _pi64, _i32]),
+    # engine-private (not part of the reference-facing header)
+    "rk_set_rank": (ctypes.c_int, [_vp, _i32]),
+    "rk_set_option": (ctypes.c_int, [_vp, _i32, _i64]),
+    "rk_uniform_values": (ctypes.c_int, [_u64, _i64, _i64, _pf]),
+    "rk_pcg64_draws": (ctypes.c_int, [_u64, _u64, _u64, _u64, _u64, _i64, _pd]),
+    "rk_grid_block": (ctypes.c_int, [_vp, _pi64, _i32]),
+    "rk_grid_colmap": (ctypes.c_int, [_vp, _pi64]),
+    "rk_time_k1": (ctypes.c_int, [_vp, _i32, _pd]),
+    "rk_trace_len": (ctypes.c_int, [_vp, _pi32]),
+    "rk_restore": (ctypes.c_int, [_vp]),
+}
+
+_LIB = None
+
+
+def load():
+    """Load the CUDA library (raises ImportError when it was never built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the RESCAL engine has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def check(status):
+    if status != RK_OK:
+        msg = load().rk_last_error().decode(errors="replace")
+        raise _EXC.get(status, RescalkitError)(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(_pd)
+
+
+def pcg64_seed_state(entropy):
+    """numpy PCG64 (state, inc) after seeding from SeedSequence(entropy), as
+    four u64 words (state_hi, state_lo, inc_hi, inc_lo) — the published
+    seeding of the reference's RNG (dist_rescal.py:167-168)."""
+    bg = np.random.PCG64(np.random.SeedSequence(entropy))
+    st = bg.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return (s >> 64) & m, s & m, (inc >> 64) & m, inc & m
+
+
+class Engine:
+    """One device-resident RESCAL problem (tensor + factors) on one GPU."""
+
+    def __init__(self, n, m, k, device=None, engine="auto"):
+        lib = load()
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0"))
+        self.n, self.m, self.k = int(n), int(m), int(k)
+        self._h = _vp()
+        check(lib.rk_create(int(device), self.n, self.m, self.k, ENGINES[engine], ctypes.byref(self._h)))
+        self._lib = lib
+
+    # lifecycle -----------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.rk_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # data ------------------------------------------------------------------
+    def upload(self, x):
+        x = np.ascontiguousarray(x)
+        if x.dtype not in (np.float32, np.float64):
+            x = x.astype(np.float64)
+        if x.shape != (self.m, self.n, self.n):
+            raise DataError(f"tensor shape {x.shape} != ({self.m}, {self.n}, {self.n})")
+        check(self._lib.rk_upload_dense(self._h, x.ctypes.data_as(_vp), RK_F32 if x.dtype == np.float32 else RK_F64))
+
+    def upload_block(self, xb, sq_norm_global):
+        xb = np.ascontiguousarray(xb)
+        if xb.dtype not in (np.float32, np.float64):
+            xb = xb.astype(np.float64)
+        check(self._lib.rk_upload_block(self._h, xb.ctypes.data_as(_vp),
+                                        RK_F32 if xb.dtype == np.float32 else RK_F64,
+                                        xb.shape[1], xb.shape[2], float(sq_norm_global)))
+
+    def fill_uniform(self, seed):
+        check(self._lib.rk_fill_uniform(self._h, int(seed)))
+
+    def set_rank(self, k):
+        check(self._lib.rk_set_rank(self._h, int(k)))
+        self.k = int(k)
+
+    def set_option(self, key, value):
+        check(self._lib.rk_set_option(self._h, int(key), int(value)))
+
+    def set_factors(self, a, r):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        if a.shape != (self.n, self.k) or r.shape != (self.m, self.k, self.k):
+            raise DataError("initial factors do not match tensor/k")
+        check(self._lib.rk_set_factors(self._h, _dp(a), _dp(r)))
+
+    def get_factors(self):
+        a = np.empty((self.n, self.k), dtype=np.float64)
+        r = np.empty((self.m, self.k, self.k), dtype=np.float64)
+        check(self._lib.rk_get_factors(self._h, _dp(a), _dp(r)))
+        return a, r
+
+    # compute ---------------------------------------------------------------
+    def run(self, iters, eps, track_error=True, tol=None):
+        trace = np.zeros(iters + 1, dtype=np.float64)
+        done = _i32(0)
+        status = self._lib.rk_run(self._h, int(iters), float(eps), 1 if track_error else 0,
+                                  -1.0 if tol is None else float(tol), _dp(trace), ctypes.byref(done))
+        tl = _i32(0)
+        self._lib.rk_trace_len(self._h, ctypes.byref(tl))
+        self.last_trace = trace[: tl.value].copy() if track_error else np.zeros(0)
+        check(status)
+        return int(done.value), self.last_trace
+
+    def update_r(self, eps):
+        check(self._lib.rk_update_r(self._h, float(eps)))
+
+    def update_a(self, eps):
+        check(self._lib.rk_update_a(self._h, float(eps)))
+
+    def residual(self):
+        res, nrm = _f64(0.0), _f64(0.0)
+        check(self._lib.rk_residual(self._h, ctypes.byref(res), ctypes.byref(nrm)))
+        return res.value, nrm.value
+
+    def regress_r(self, max_iters, tol, eps):
+        done = _i32(0)
+        check(self._lib.rk_regress_r(self._h, int(max_iters), -1.0 if tol is None else float(tol),
+                                     float(eps), ctypes.byref(done)))
+        return int(done.value)
+
+    def perturb(self, entropy, delta, n_global=None, row0=0):
+        sh, sl, ih, il = pcg64_seed_state(entropy)
+        check(self._lib.rk_perturb(self._h, sh, sl, ih, il, float(delta),
+                                   int(n_global or self.n), int(row0), 0, None))
+
+    def restore(self):
+        """Undo rk_perturb: the device tensor goes back to the uploaded one."""
+        check(self._lib.rk_restore(self._h))
+
+    # p_r x p_c grid ------------------------------------------------------------
+    def grid_init(self, pr, pc, rank, nccl_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        check(self._lib.rk_grid_init(self._h, int(pr), int(pc), int(rank), buf, self.n))
+
+    def grid_block(self):
+        out = np.zeros(8, dtype=np.int64)
+        check(self._lib.rk_grid_block(self._h, out.ctypes.data_as(_pi64), 8))
+        keys = ["gi", "gj", "piece", "rows", "cols", "row0", "pr", "pc"]
+        info = dict(zip(keys, (int(v) for v in out)))
+        cm = np.zeros(info["cols"], dtype=np.int64)
+        check(self._lib.rk_grid_colmap(self._h, cm.ctypes.data_as(_pi64)))
+        info["colmap"] = cm
+        return info
+
+    def timing(self):
+        out = np.zeros(4, dtype=np.float64)
+        check(self._lib.rk_last_timing(self._h, _dp(out), 4))
+        return {"run_ms": out[0], "k1_ms": out[1], "k1_launches": int(out[2]), "launches": int(out[3])}
+
+    def time_k1(self, reps=10):
+        ms = _f64(0.0)
+        check(self._lib.rk_time_k1(self._h, int(reps), ctypes.byref(ms)))
+        return ms.value
+
+    def info(self):
+        out = np.zeros(10, dtype=np.int64)
+        check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 10))
+        keys = ["engine", "n_pad", "k_pad", "strip_tiles", "ctas", "smem", "strips", "slots", "k2a_blocks", "nc_pad"]
+        return dict(zip(keys, (int(v) for v in out)))
+
+    @property
+    def stream(self):
+        return self._lib.rk_stream(self._h)
+
+
+def device_count():
+    n = _i32(0)
+    check(load().rk_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def pcg64_draws(entropy, offset, count):
+    """Device PCG64 draws u_{offset..offset+count} (tests / parity checks)."""
+    sh, sl, ih, il = pcg64_seed_state(entropy)
+    out = np.empty(count, dtype=np.float64)
+    check(load().rk_pcg64_draws(sh, sl, ih, il, int(offset), int(count), _dp(out)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().rk_nccl_unique_id(buf))
+    return buf.raw
+
+
+def uniform_values(seed, offset, count):
+    out = np.empty(count, dtype=np.float32)
+    check(load().rk_uniform_values(int(seed), int(offset), int(count), out.ctypes.data_as(_pf)))
+    return out

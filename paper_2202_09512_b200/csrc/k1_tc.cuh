@@ -1,0 +1,470 @@
+// K1 — tcgen05 dual slice contraction for the RESCAL MU iteration (sm_100a).
+//
+// Computes, for every slice t, P_t = X_t A and Q_t = X_t^T A in ONE pass over
+// X (reference: rescal.py:128 X_t A and rescal.py:134-135 X_t^T (A R_t), the
+// latter restructured as (X_t^T A) R_t so both products read the same X tile;
+// SURVEY.md App. C). Split precision 3xBF16: X = Xh + Xl and A = Ah + Al are
+// bf16 pairs; each product accumulates Xh*Ah + Xh*Al + Xl*Ah in fp32 TMEM.
+//
+// Work decomposition (persistent, one CTA per SM):
+//   tile   = 128 x 128 block of one slice (rows i, cols j)
+//   strip  = `c` consecutive column tiles (W = 128c columns)
+//   item   = (t, strip, row-block rb): the c tiles of one row block in a strip
+// Each CTA owns a contiguous range of items (balanced by tile count). Within
+// an item the P accumulator (128 rows x K) lives in TMEM (double buffered);
+// the c Q accumulators (one per column tile, 128 x K each) live in TMEM for
+// the whole run of items the CTA has in the same (t, strip) — a "segment".
+//   P partial  -> Ppart[t][strip][row][K]      (one writer per (t,strip,row))
+//   Q partial  -> Qpart[slot][strip col][K]    (one slot per segment)
+// k1_reduce sums the partials in a fixed order (deterministic, no atomics).
+//
+// Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
+// w2..w5 epilogue (TMEM -> registers -> global), lane quadrant = warp % 4.
+#pragma once
+
+#include <cuda.h>
+
+#include "rk_common.cuh"
+
+namespace rk {
+namespace tc {
+
+constexpr int kStages = 2;
+constexpr int kTile = 128;
+constexpr int kThreads = 192;
+constexpr uint32_t kXBox = 128 * 64 * 2;  // one 128-row x 64-col bf16 box = 16 KB
+
+struct K1Args {
+  int NR, NC, K, M;
+  int c;          // tiles per strip
+  int nstrips;
+  int nrb;        // NR / 128 row blocks
+  int ncb;        // NC / 128 column tiles
+  float* Ppart;   // [M][nstrips][NR][K]
+  float* Qpart;   // [nslots][c*128][K]
+  const int* cta_begin;  // [grid + 1] item ranges
+  const int* cta_slot;   // [grid] first Q slot of the CTA
+  const Ctl* ctl;
+  int skip_if_stopped;
+};
+
+// ------------------------------- PTX helpers -------------------------------
+RK_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+RK_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+RK_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+RK_DEV void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+RK_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+RK_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+RK_DEV void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+RK_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+RK_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+RK_DEV void tc_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+
+// D[tmem] (+)= A[smem desc] * B[smem desc], kind::f16 (bf16 in, fp32 accum)
+RK_DEV void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                   uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 16 columns of 32-bit: thread = lane, 16 consecutive columns
+RK_DEV void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm100 version bits.
+RK_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A/B = BF16, D = F32, M = 128, N = n.
+RK_DEV uint32_t idesc_bf16(int n, int a_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn_major << 15) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// item -> (t, strip, rb); items are ordered (t, strip, rb)
+RK_DEV void decode_item(int item, int nstrips, int nrb, int& t, int& s, int& rb) {
+  rb = item % nrb;
+  int ts = item / nrb;
+  s = ts % nstrips;
+  t = ts / nstrips;
+}
+
+RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
+  return s == nstrips - 1 ? ncb - c * (nstrips - 1) : c;
+}
+
+// ------------------------------- the kernel --------------------------------
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1)
+    k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
+                 const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_rl,
+                 const __grid_constant__ CUtensorMap map_ch, const __grid_constant__ CUtensorMap map_cl,
+                 K1Args args) {
+  // map_x*: the block's slices as a (M*NR) x NC bf16 matrix (hi / lo planes)
+  // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
+  // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
+  static_assert(K == 16 || K == 32, "tcgen05 path supports k_pad 16 or 32");
+  constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
+  constexpr uint32_t kStageX = 4 * kXBox;          // Xh0 Xh1 Xl0 Xl1
+  constexpr uint32_t kStageBytes = kStageX + 4 * kABox;
+  constexpr uint32_t kAIBytes = 4 * kABox;
+
+  if (args.skip_if_stopped && args.ctl->stop) return;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment (of the shared-window address) for SWIZZLE_128B atoms
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stage_base = smem;                                  // kStages * kStageBytes
+  uint8_t* ai_base = smem + kStages * kStageBytes;             // 2 * kAIBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ai_base + 2 * kAIBytes);
+  // barrier slots
+  uint64_t* full = bars;             // [kStages]
+  uint64_t* empty = bars + 2;        // [kStages]
+  uint64_t* ai_full = bars + 4;      // [2]
+  uint64_t* ai_empty = bars + 6;     // [2]
+  uint64_t* p_full = bars + 8;       // [2]
+  uint64_t* p_empty = bars + 10;     // [2]
+  uint64_t* q_full = bars + 12;      // [1]
+  uint64_t* q_empty = bars + 13;     // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int item_b = args.cta_begin[blockIdx.x];
+  const int item_e = args.cta_begin[blockIdx.x + 1];
+  const int nstrips = args.nstrips, nrb = args.nrb, ncb = args.ncb, c = args.c, NR = args.NR;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&ai_full[i]), 1);
+      mbar_init(smem_u32(&ai_empty[i]), 1);
+      mbar_init(smem_u32(&p_full[i]), 1);
+      mbar_init(smem_u32(&p_empty[i]), 4);  // one arrive per epilogue warp
+    }
+    mbar_init(smem_u32(q_full), 1);
+    mbar_init(smem_u32(q_empty), 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_xh);
+    tma_prefetch(&map_xl);
+    tma_prefetch(&map_rh);
+    tma_prefetch(&map_rl);
+    tma_prefetch(&map_ch);
+    tma_prefetch(&map_cl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = item_b; item < item_e; ++item) {
+        int t, s, rb;
+        decode_item(item, nstrips, nrb, t, s, rb);
+        const int ct = strip_tiles(s, nstrips, c, ncb);
+        const int ab = (item - item_b) & 1;
+        const uint32_t ap = ((item - item_b) >> 1) & 1;
+        // A^T[:, I] (row operand of Q) for this row block
+        mbar_wait(smem_u32(&ai_empty[ab]), ap ^ 1);
+        const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
+        const uint32_t aib = smem_u32(&ai_full[ab]);
+        mbar_expect_tx(aib, kAIBytes);
+        tma_load_2d(ai + 0 * kABox, &map_rh, rb * kTile, 0, aib);
+        tma_load_2d(ai + 1 * kABox, &map_rh, rb * kTile + 64, 0, aib);
+        tma_load_2d(ai + 2 * kABox, &map_rl, rb * kTile, 0, aib);
+        tma_load_2d(ai + 3 * kABox, &map_rl, rb * kTile + 64, 0, aib);
+        const int xrow = t * NR + rb * kTile;
+        for (int cb = 0; cb < ct; ++cb) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_expect_tx(fb, kStageBytes);
+          const int j0 = (s * c + cb) * kTile;
+          tma_load_2d(st + 0 * kXBox, &map_xh, j0, xrow, fb);
+          tma_load_2d(st + 1 * kXBox, &map_xh, j0 + 64, xrow, fb);
+          tma_load_2d(st + 2 * kXBox, &map_xl, j0, xrow, fb);
+          tma_load_2d(st + 3 * kXBox, &map_xl, j0 + 64, xrow, fb);
+          tma_load_2d(st + kStageX + 0 * kABox, &map_ch, j0, 0, fb);
+          tma_load_2d(st + kStageX + 1 * kABox, &map_ch, j0 + 64, 0, fb);
+          tma_load_2d(st + kStageX + 2 * kABox, &map_cl, j0, 0, fb);
+          tma_load_2d(st + kStageX + 3 * kABox, &map_cl, j0 + 64, 0, fb);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    if (lane == 0) {
+      const uint32_t id_p = idesc_bf16(K, 0);  // A = X tile, K-major (K-dim = j)
+      const uint32_t id_q = idesc_bf16(K, 1);  // A = X tile, MN-major (M = j, K-dim = i)
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t qe_phase = 0;
+      int seg = 0;
+      for (int item = item_b; item < item_e; ++item) {
+        int t, s, rb;
+        decode_item(item, nstrips, nrb, t, s, rb);
+        const int ct = strip_tiles(s, nstrips, c, ncb);
+        const int ts = item / nrb;
+        const bool first_in_seg = item == item_b || (item - 1) / nrb != ts;
+        const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
+        if (first_in_seg && seg > 0) {
+          mbar_wait(smem_u32(q_empty), qe_phase);  // previous segment's Q drained
+          qe_phase ^= 1;
+          tc_fence_after();
+        }
+        const int idx = item - item_b;
+        const int ab = idx & 1;
+        const uint32_t ap = (idx >> 1) & 1;
+        const int pb = idx & 1;
+        const uint32_t pp = (idx >> 1) & 1;
+        mbar_wait(smem_u32(&ai_full[ab]), ap);
+        mbar_wait(smem_u32(&p_empty[pb]), pp ^ 1);
+        tc_fence_after();
+        const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
+        const uint32_t p_tmem = tmem + (uint32_t)(c * K + pb * K);
+        for (int cb = 0; cb < ct; ++cb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+          const uint32_t xh = st, xl = st + 2 * kXBox;
+          const uint32_t ajh = st + kStageX, ajl = st + kStageX + 2 * kABox;
+          const uint32_t q_tmem = tmem + (uint32_t)(cb * K);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
+            const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
+            const uint32_t aoff = (ks >> 2) * kABox + (ks & 3) * 32;
+            const uint64_t dxh = umma_desc(xh + xoff, 16, 1024);
+            const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
+            const uint64_t dah = umma_desc(ajh + aoff, 16, 1024);
+            const uint64_t dal = umma_desc(ajl + aoff, 16, 1024);
+            const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
+            tc_mma(p_tmem, dxh, dah, id_p, accp);
+            tc_mma(p_tmem, dxh, dal, id_p, 1u);
+            tc_mma(p_tmem, dxl, dah, id_p, 1u);
+            // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
+            const uint32_t roff = ks * 16 * 128;
+            const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
+            const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
+            const uint64_t qah = umma_desc(ai + aoff, 16, 1024);
+            const uint64_t qal = umma_desc(ai + 2 * kABox + aoff, 16, 1024);
+            const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
+            tc_mma(q_tmem, qxh, qah, id_q, accq);
+            tc_mma(q_tmem, qxh, qal, id_q, 1u);
+            tc_mma(q_tmem, qxl, qah, id_q, 1u);
+          }
+          tc_commit(smem_u32(&empty[stage]));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(smem_u32(&p_full[pb]));
+        tc_commit(smem_u32(&ai_empty[ab]));
+        if (last_in_seg) {
+          tc_commit(smem_u32(q_full));
+          ++seg;
+        }
+      }
+    }
+  } else {
+    // ============================ epilogue ================================
+    const int quad = warp & 3;                 // TMEM lane quadrant
+    const int row = quad * 32 + lane;          // row within the 128-row tile
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    uint32_t qf_phase = 0;
+    int slot = args.cta_slot[blockIdx.x];
+    for (int item = item_b; item < item_e; ++item) {
+      int t, s, rb;
+      decode_item(item, nstrips, nrb, t, s, rb);
+      const int ct = strip_tiles(s, nstrips, c, ncb);
+      const int ts = item / nrb;
+      const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
+      const int idx = item - item_b;
+      const int pb = idx & 1;
+      const uint32_t pp = (idx >> 1) & 1;
+      mbar_wait(smem_u32(&p_full[pb]), pp);
+      tc_fence_after();
+      float v[K];
+#pragma unroll
+      for (int h = 0; h < K / 16; ++h)
+        tmem_ld16(tmem + lane_base + (uint32_t)(c * K + pb * K + 16 * h), v + 16 * h);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&p_empty[pb]));
+      float4* dst = reinterpret_cast<float4*>(
+          args.Ppart + ((((size_t)t * nstrips + s) * NR) + (size_t)rb * kTile + row) * K);
+#pragma unroll
+      for (int h = 0; h < K / 4; ++h) dst[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+      if (last_in_seg) {
+        mbar_wait(smem_u32(q_full), qf_phase);
+        qf_phase ^= 1;
+        tc_fence_after();
+        float* qdst = args.Qpart + (size_t)slot * c * kTile * K;
+        for (int cb = 0; cb < ct; ++cb) {
+          float w[K];
+#pragma unroll
+          for (int h = 0; h < K / 16; ++h)
+            tmem_ld16(tmem + lane_base + (uint32_t)(cb * K + 16 * h), w + 16 * h);
+          float4* qd = reinterpret_cast<float4*>(qdst + ((size_t)cb * kTile + row) * K);
+#pragma unroll
+          for (int h = 0; h < K / 4; ++h)
+            qd[h] = make_float4(w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(q_empty));
+        ++slot;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int K>
+constexpr uint32_t k1_smem_bytes() {
+  return 1024 /*align slack*/ + kStages * (4 * kXBox + 4 * K * 128) + 2 * (4 * K * 128) + 256;
+}
+
+// Deterministic reduction of the partials:
+//   P[t][i] = sum_s Ppart[t][s][i]                         (i < NR)
+//   Q[t][j] = sum_{slots of (t, strip(j))} Qpart[slot][j - strip0]   (j < NC)
+__global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
+                                                 const float* __restrict__ Ppart,
+                                                 const float* __restrict__ Qpart,
+                                                 const int* __restrict__ slot_first,
+                                                 const int* __restrict__ slot_count,
+                                                 float* __restrict__ P, float* __restrict__ Q,
+                                                 int NR, int NC, int K, int M, int c, int nstrips,
+                                                 int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  const int W = c * kTile;
+  const int K4 = K / 4;
+  const int64_t totalP = (int64_t)M * NR * K4;
+  const int64_t total = totalP + (int64_t)M * NC * K4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < totalP) {
+      const int q4 = (int)(e % K4);
+      const int64_t ti = e / K4;
+      const int i = (int)(ti % NR);
+      const int t = (int)(ti / NR);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < nstrips; ++s) {
+        float4 v = reinterpret_cast<const float4*>(
+            Ppart + ((((size_t)t * nstrips + s) * NR) + i) * K)[q4];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      reinterpret_cast<float4*>(P + ((size_t)t * NR + i) * K)[q4] = acc;
+    } else {
+      const int64_t e2 = e - totalP;
+      const int q4 = (int)(e2 % K4);
+      const int64_t tj = e2 / K4;
+      const int j = (int)(tj % NC);
+      const int t = (int)(tj / NC);
+      const int s = j / W;
+      const int jl = j - s * W;
+      const int f = slot_first[t * nstrips + s], nsl = slot_count[t * nstrips + s];
+      float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < nsl; ++q) {
+        float4 v = reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K)[q4];
+        qa.x += v.x; qa.y += v.y; qa.z += v.z; qa.w += v.w;
+      }
+      reinterpret_cast<float4*>(Q + ((size_t)t * NC + j) * K)[q4] = qa;
+    }
+  }
+}
+
+}  // namespace tc
+}  // namespace rk

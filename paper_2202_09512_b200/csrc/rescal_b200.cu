@@ -1,0 +1,1234 @@
+// rescal_b200.cu — C-ABI implementation (include/rescal_b200.h).
+//
+// One handle = one GPU, one CUDA stream, all tensor/factor buffers resident
+// in HBM. An MU iteration (rescal.py:114-146 + the trace of :215-224) is the
+// kernel sequence
+//   K1  slice contraction  P_t = X_t A_col, Q_t = X_t^T A_row   (tcgen05 or SIMT)
+//   K5  direct residual of the current iterate (only in the small-error regime)
+//   K2a G / S_t partials   K2f per-slice core update + M_t   K2m trace/commit
+//   K2b A update + next-iteration operand planes
+// captured once into a CUDA graph and replayed; stop conditions live in a
+// device control block so queued iterations become no-ops without host syncs.
+// On a p_r x p_c grid the same kernels run on the local block with NCCL
+// all-gather / all-reduce / reduce-scatter in between.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rescal_b200.h"
+#include "k1_tc.cuh"
+#include "rk_kernels.cuh"
+
+using rk::Ctl;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RkError {
+  int code;
+  std::string msg;
+};
+
+#define RK_CUDA(expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw RkError{RK_ERR_DEVICE, std::string(#expr) + ": " + cudaGetErrorString(_e)};    \
+  } while (0)
+
+#define RK_NCCL(expr)                                                                      \
+  do {                                                                                     \
+    ncclResult_t _r = (expr);                                                              \
+    if (_r != ncclSuccess)                                                                 \
+      throw RkError{RK_ERR_GRID, std::string(#expr) + ": " + ncclGetErrorString(_r)};      \
+  } while (0)
+
+#define RK_REQUIRE(cond, code, msg)             \
+  do {                                          \
+    if (!(cond)) throw RkError{(code), (msg)}; \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RK_OK;
+  } catch (const RkError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RK_ERR_DEVICE;
+  }
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  RK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  RK_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    RK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    RK_REQUIRE(q == cudaDriverEntryPointSuccess && p, RK_ERR_DEVICE,
+               "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 row-major matrix [rows][cols], box {64 cols, box_rows}, 128B swizzle
+CUtensorMap make_map(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RK_REQUIRE(r == CUDA_SUCCESS, RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+}  // namespace
+
+struct rk_handle {
+  int dev = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  // problem
+  int64_t n = 0, m = 0;  // global n, slices
+  int k = 0, K = 0;      // rank, padded rank
+  int engine = RK_ENGINE_AUTO;
+  int requested_engine = RK_ENGINE_AUTO;
+  // local block (NR x NC padded; rows_valid x cols_valid real)
+  int64_t NR = 0, NC = 0, rows_valid = 0, cols_valid = 0;
+  // grid
+  int pr = 1, pc = 1, rank = 0, gi = 0, gj = 0;
+  int64_t piece = 0;  // b = ceil(n / p)
+  ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+  std::vector<int64_t> colmap;  // local col -> global col
+  int64_t* d_colmap = nullptr;
+  // tensor
+  __nv_bfloat16 *Xh = nullptr, *Xl = nullptr, *Xh0 = nullptr, *Xl0 = nullptr;
+  bool have_x = false, perturbed = false;
+  double norm2 = 0.0, norm2_dev = 0.0, norm2_dev0 = 0.0, norm2_orig = 0.0;
+  // factors and working copies
+  double *Arow = nullptr, *Acol = nullptr;  // alias on one GPU
+  float *A32row = nullptr, *A32col = nullptr;
+  __nv_bfloat16 *ATh_row = nullptr, *ATl_row = nullptr, *ATh_col = nullptr, *ATl_col = nullptr;
+  double *R = nullptr, *Rnext = nullptr, *Mt = nullptr, *Mm = nullptr, *tt = nullptr;
+  double* part = nullptr;   // K2a partials [nb][(M+1)K^2]
+  double* red = nullptr;    // reduced partials + residual scalar (grid all-reduce buffer)
+  int nb = 1;
+  double* gscratch = nullptr;
+  double *UI = nullptr, *UJ = nullptr;  // grid numerator partials
+  double *regS = nullptr, *regG = nullptr, *regT = nullptr, *regRn = nullptr;
+  int* d_iters = nullptr;
+  float *P = nullptr, *Q = nullptr;
+  double* rpart = nullptr;
+  int nr = 1;
+  double* trace_dev = nullptr;
+  int trace_cap = 0;
+  Ctl* ctl = nullptr;
+  Ctl* ctl_host = nullptr;   // pinned
+  int* stop_host = nullptr;  // pinned [2]
+  double* npart = nullptr;   // upload norm partials
+  double* npart2 = nullptr;
+  int nnp = 0;
+  // tcgen05 schedule
+  int c = 0, nstrips = 0, grid_tc = 0, nslots = 0;
+  size_t smem_tc = 0;
+  float *Ppart = nullptr, *Qpart = nullptr;
+  int *d_cta_begin = nullptr, *d_cta_slot = nullptr, *d_slot_first = nullptr,
+      *d_slot_count = nullptr;
+  CUtensorMap maps[6];
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  bool use_graph = true;
+  // timing
+  bool profile = false;
+  cudaEvent_t ev_run0 = nullptr, ev_run1 = nullptr;
+  std::vector<cudaEvent_t> ev_k1;
+  double last_ms = 0.0, k1_ms_sum = 0.0;
+  int k1_count = 0, launches = 0, iter_launches = 0;
+  double eps = 1e-16;
+
+  bool grid() const { return pr * pc > 1; }
+};
+
+namespace {
+
+size_t k2f_smem(int K) {
+  size_t s = (size_t)6 * K * K * sizeof(double);
+  return s <= 200 * 1024 ? s : 0;
+}
+
+void free_factor_buffers(rk_handle* h) {
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
+                  h->part, h->red, h->gscratch, h->UI, h->UJ, h->regS, h->regG, h->regT,
+                  h->regRn, h->P, h->Q, h->rpart, h->Ppart, h->Qpart, h->d_cta_begin,
+                  h->d_cta_slot, h->d_slot_first, h->d_slot_count};
+  for (void* p : ptrs) dfree(p);
+  if (h->Acol != h->Arow) dfree(h->Acol);
+  if (h->A32col != h->A32row) dfree(h->A32col);
+  if (h->ATh_col != h->ATh_row) dfree(h->ATh_col);
+  if (h->ATl_col != h->ATl_row) dfree(h->ATl_col);
+  h->Arow = h->Acol = nullptr;
+  h->A32row = h->A32col = nullptr;
+  h->ATh_row = h->ATl_row = h->ATh_col = h->ATl_col = nullptr;
+  h->R = h->Rnext = h->Mt = h->Mm = h->tt = h->part = h->red = h->gscratch = nullptr;
+  h->UI = h->UJ = h->regS = h->regG = h->regT = h->regRn = nullptr;
+  h->P = h->Q = nullptr;
+  h->rpart = nullptr;
+  h->Ppart = h->Qpart = nullptr;
+  h->d_cta_begin = h->d_cta_slot = h->d_slot_first = h->d_slot_count = nullptr;
+}
+
+// Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
+void plan_tc(rk_handle* h) {
+  const int K = h->K;
+  const int nrb = (int)(h->NR / 128), ncb = (int)(h->NC / 128);
+  const int cmax = 512 / K - 2;
+  int c = std::min(cmax, ncb);
+  int nstrips = (ncb + c - 1) / c;
+  c = (ncb + nstrips - 1) / nstrips;
+  nstrips = (ncb + c - 1) / c;
+  h->c = c;
+  h->nstrips = nstrips;
+  const int M = (int)h->m;
+  const int64_t n_items = (int64_t)M * nstrips * nrb;
+  auto tiles_of = [&](int64_t item) {
+    int s = (int)((item / nrb) % nstrips);
+    return s == nstrips - 1 ? ncb - c * (nstrips - 1) : c;
+  };
+  int64_t total = 0;
+  for (int64_t it = 0; it < n_items; ++it) total += tiles_of(it);
+  const int grid = (int)std::min<int64_t>(h->num_sms, n_items);
+  std::vector<int> begin(grid + 1, 0);
+  int64_t cum = 0, it = 0;
+  for (int g = 0; g < grid; ++g) {
+    begin[g] = (int)it;
+    const int64_t target = total * (g + 1) / grid;
+    while (it < n_items && cum + tiles_of(it) <= target) cum += tiles_of(it++);
+    if (it == begin[g] && it < n_items) cum += tiles_of(it++);  // at least one item
+  }
+  begin[grid] = (int)n_items;
+  // slots: one per (CTA, segment) in item order
+  std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips, 0), slot_count(M * nstrips, 0);
+  int slots = 0;
+  for (int g = 0; g < grid; ++g) {
+    cta_slot[g] = slots;
+    int prev = -1;
+    for (int i = begin[g]; i < begin[g + 1]; ++i) {
+      int ts = i / nrb;
+      if (ts != prev) {
+        if (slot_count[ts] == 0) slot_first[ts] = slots;
+        slot_count[ts] += 1;
+        ++slots;
+        prev = ts;
+      }
+    }
+  }
+  h->grid_tc = grid;
+  h->nslots = slots;
+  h->d_cta_begin = dalloc<int>(grid + 1);
+  h->d_cta_slot = dalloc<int>(grid);
+  h->d_slot_first = dalloc<int>(M * nstrips);
+  h->d_slot_count = dalloc<int>(M * nstrips);
+  RK_CUDA(cudaMemcpy(h->d_cta_begin, begin.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(h->d_cta_slot, cta_slot.data(), sizeof(int) * grid, cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(h->d_slot_first, slot_first.data(), sizeof(int) * M * nstrips,
+                     cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(h->d_slot_count, slot_count.data(), sizeof(int) * M * nstrips,
+                     cudaMemcpyHostToDevice));
+  h->Ppart = dalloc<float>((size_t)M * nstrips * h->NR * K);
+  h->Qpart = dalloc<float>((size_t)slots * c * 128 * K);
+  h->maps[0] = make_map(h->Xh, h->NC, (uint64_t)M * h->NR, 128);
+  h->maps[1] = make_map(h->Xl, h->NC, (uint64_t)M * h->NR, 128);
+  h->maps[2] = make_map(h->ATh_row, h->NR, K, K);
+  h->maps[3] = make_map(h->ATl_row, h->NR, K, K);
+  h->maps[4] = make_map(h->ATh_col, h->NC, K, K);
+  h->maps[5] = make_map(h->ATl_col, h->NC, K, K);
+  h->smem_tc = K == 16 ? rk::tc::k1_smem_bytes<16>() : rk::tc::k1_smem_bytes<32>();
+  if (K == 16)
+    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)h->smem_tc));
+  else
+    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)h->smem_tc));
+}
+
+void alloc_factor_buffers(rk_handle* h) {
+  const int K = h->K;
+  const int64_t M = h->m;
+  const size_t KK = (size_t)K * K;
+  h->Arow = dalloc<double>((size_t)h->NR * K);
+  h->A32row = dalloc<float>((size_t)h->NR * K);
+  h->ATh_row = dalloc<__nv_bfloat16>((size_t)h->NR * K);
+  h->ATl_row = dalloc<__nv_bfloat16>((size_t)h->NR * K);
+  if (h->grid()) {
+    h->Acol = dalloc<double>((size_t)h->NC * K);
+    h->A32col = dalloc<float>((size_t)h->NC * K);
+    h->ATh_col = dalloc<__nv_bfloat16>((size_t)h->NC * K);
+    h->ATl_col = dalloc<__nv_bfloat16>((size_t)h->NC * K);
+    h->UI = dalloc<double>((size_t)h->NR * K);
+    h->UJ = dalloc<double>((size_t)h->NC * K);
+  } else {
+    h->Acol = h->Arow;
+    h->A32col = h->A32row;
+    h->ATh_col = h->ATh_row;
+    h->ATl_col = h->ATl_row;
+  }
+  h->R = dalloc<double>(M * KK);
+  h->Rnext = dalloc<double>(M * KK);
+  h->Mt = dalloc<double>(M * KK);
+  h->Mm = dalloc<double>(KK);
+  h->tt = dalloc<double>(2 * M);
+  // K2a partial blocks: enough parallelism, bounded partial traffic (~16 MB)
+  int64_t rows = std::max(h->NR, (int64_t)h->piece);
+  int nb = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, rows / 64));
+  const size_t per = (size_t)(M + 1) * KK * sizeof(double);
+  nb = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (16ll << 20) / (int64_t)per));
+  h->nb = nb;
+  h->part = dalloc<double>((size_t)nb * (M + 1) * KK);
+  h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
+  if (!k2f_smem(K)) h->gscratch = dalloc<double>((size_t)M * 6 * KK);
+  h->P = dalloc<float>((size_t)M * h->NR * K);
+  h->Q = dalloc<float>((size_t)M * h->NC * K);
+  h->nr = h->num_sms * 2;
+  h->rpart = dalloc<double>(h->nr);
+  h->regS = dalloc<double>(M * KK);
+  h->regG = dalloc<double>(KK);
+  h->regT = dalloc<double>(M * KK);
+  h->regRn = dalloc<double>(M * KK);
+  // engine
+  int eng = h->requested_engine;
+  if (eng == RK_ENGINE_AUTO) eng = (K == 16 || K == 32) ? RK_ENGINE_TC : RK_ENGINE_SIMT;
+  RK_REQUIRE(!(eng == RK_ENGINE_TC && !(K == 16 || K == 32)), RK_ERR_DATA,
+             "tcgen05 engine needs k_pad in {16, 32}");
+  h->engine = eng;
+  if (eng == RK_ENGINE_TC) plan_tc(h);
+  const size_t simt_smem = (size_t)(64 * 33 + 64 * K) * sizeof(float);
+  RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
+  RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
+  const size_t k5s = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
+  RK_CUDA(cudaFuncSetAttribute(rk::k5_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s));
+  if (k2f_smem(K))
+    RK_CUDA(cudaFuncSetAttribute(rk::k2f_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
+  const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
+  RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
+  const size_t k2ps = (size_t)K * (K + 1) * 8 + (256 / K) * K * 4;
+  RK_CUDA(cudaFuncSetAttribute(rk::k2b_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2ps));
+}
+
+// ------------------------------- launches ----------------------------------
+
+void launch_k1(rk_handle* h, bool timed) {
+  cudaStream_t s = h->stream;
+  const int K = h->K, M = (int)h->m;
+  if (timed) {
+    size_t i = (size_t)h->k1_count * 2;
+    if (h->ev_k1.size() < i + 2) {
+      for (int q = 0; q < 2; ++q) {
+        cudaEvent_t e;
+        RK_CUDA(cudaEventCreate(&e));
+        h->ev_k1.push_back(e);
+      }
+    }
+    RK_CUDA(cudaEventRecord(h->ev_k1[i], s));
+  }
+  if (h->engine == RK_ENGINE_TC) {
+    rk::tc::K1Args a;
+    a.NR = (int)h->NR;
+    a.NC = (int)h->NC;
+    a.K = K;
+    a.M = M;
+    a.c = h->c;
+    a.nstrips = h->nstrips;
+    a.nrb = (int)(h->NR / 128);
+    a.ncb = (int)(h->NC / 128);
+    a.Ppart = h->Ppart;
+    a.Qpart = h->Qpart;
+    a.cta_begin = h->d_cta_begin;
+    a.cta_slot = h->d_cta_slot;
+    a.ctl = h->ctl;
+    a.skip_if_stopped = 1;
+    if (K == 16)
+      rk::tc::k1_tc_kernel<16><<<h->grid_tc, rk::tc::kThreads, h->smem_tc, s>>>(
+          h->maps[0], h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
+    else
+      rk::tc::k1_tc_kernel<32><<<h->grid_tc, rk::tc::kThreads, h->smem_tc, s>>>(
+          h->maps[0], h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
+    RK_CUDA(cudaGetLastError());
+    if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
+    rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
+                                                      h->d_slot_count, h->P, h->Q, (int)h->NR,
+                                                      (int)h->NC, K, M, h->c, h->nstrips, 1);
+    h->launches += 2;
+  } else {
+    const size_t smem = (size_t)(64 * 33 + 64 * K) * sizeof(float);
+    rk::k1_simt_p<<<dim3((unsigned)(h->NR / 32), M), rk::kThreads, smem, s>>>(
+        h->ctl, h->Xh, h->Xl, h->A32col, h->P, (int)h->NR, (int)h->NC, K, 1);
+    rk::k1_simt_q<<<dim3((unsigned)(h->NC / 32), M), rk::kThreads, smem, s>>>(
+        h->ctl, h->Xh, h->Xl, h->A32row, h->Q, (int)h->NR, (int)h->NC, K, 1);
+    RK_CUDA(cudaGetLastError());
+    if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
+    h->launches += 2;
+  }
+  if (timed) h->k1_count += 1;
+}
+
+void launch_k5(rk_handle* h, int gate) {
+  const int K = h->K;
+  const size_t smem = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
+  rk::k5_residual<<<h->nr, rk::kThreads, smem, h->stream>>>(
+      h->ctl, h->Xh, h->Xl, h->A32row, h->A32col, h->R, (int)h->NR, (int)h->NC, K, (int)h->m,
+      (int)h->rows_valid, (int)h->cols_valid, h->rpart, gate);
+  RK_CUDA(cudaGetLastError());
+  h->launches += 1;
+}
+
+void launch_k2a(rk_handle* h, int skip) {
+  const int K = h->K;
+  const double* Aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
+  const int Nown = h->grid() ? (int)h->piece : (int)h->NR;
+  rk::k2a_gram_s<<<h->nb, rk::kThreads, 2 * 32 * K * sizeof(double), h->stream>>>(
+      h->ctl, Aown, Nown, h->Arow, h->P, (int)h->NR, K, (int)h->m, h->part, skip);
+  RK_CUDA(cudaGetLastError());
+  h->launches += 1;
+}
+
+// On a grid: reduce the K2a partials locally, append the direct-residual
+// scalar, and all-reduce over the world communicator. K2f then reads one
+// partial block (nb = 1) from `red`.
+void grid_allreduce_parts(rk_handle* h, bool with_resid) {
+  const int K = h->K;
+  const int len = (int)((h->m + 1) * K * K);
+  rk::reduce_parts<<<64, 256, 0, h->stream>>>(h->part, h->nb, len, h->red);
+  rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, with_resid ? h->nr : 0, h->red + len);
+  RK_NCCL(ncclAllReduce(h->red, h->red, (size_t)len + 1, ncclDouble, ncclSum, h->world, h->stream));
+  h->launches += 2;
+}
+
+void launch_k2f(rk_handle* h, int mode, int skip) {
+  const int K = h->K;
+  const double* part = h->grid() ? h->red : h->part;
+  const int nb = h->grid() ? 1 : h->nb;
+  rk::k2f_core<<<(unsigned)h->m, rk::kThreads, k2f_smem(K), h->stream>>>(
+      h->ctl, part, nb, h->R, h->Rnext, h->Mt, h->tt, K, (int)h->m, h->eps, mode, h->gscratch, skip);
+  RK_CUDA(cudaGetLastError());
+  h->launches += 1;
+}
+
+void launch_k2m(rk_handle* h, int mode) {
+  const int K = h->K;
+  const double* rp = h->grid() ? h->red + (h->m + 1) * K * K : h->rpart;
+  const int nr = h->grid() ? 1 : h->nr;
+  rk::k2m_commit<<<1, rk::kThreads, 0, h->stream>>>(h->ctl, h->tt, h->Mt, h->Mm, h->Rnext, h->R, rp,
+                                                    nr, h->trace_dev, K, (int)h->m, mode);
+  RK_CUDA(cudaGetLastError());
+  h->launches += 1;
+}
+
+void launch_emit(rk_handle* h) {
+  const int K = h->K;
+  rk::emit_operands<<<h->num_sms * 2, 256, 0, h->stream>>>(h->Arow, (int)h->NR, K, h->A32row,
+                                                           h->ATh_row, h->ATl_row);
+  if (h->grid())
+    rk::emit_operands<<<h->num_sms * 2, 256, 0, h->stream>>>(h->Acol, (int)h->NC, K, h->A32col,
+                                                             h->ATh_col, h->ATl_col);
+  RK_CUDA(cudaGetLastError());
+  h->launches += h->grid() ? 2 : 1;
+}
+
+// Grid: gather the owned pieces into the row / col operand sets.
+void grid_allgather_a(rk_handle* h) {
+  const size_t cnt = (size_t)h->piece * h->K;
+  RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Arow, cnt, ncclDouble, h->rowc, h->stream));
+  RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Acol, cnt, ncclDouble, h->colc, h->stream));
+}
+
+void launch_k2b(rk_handle* h) {
+  const int K = h->K;
+  const double eps_m = h->eps * (double)h->m;
+  if (!h->grid()) {
+    const int rpb = 256 / K;
+    const size_t smem = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * rpb * K * 4;
+    rk::k2b_update_a<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
+        h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->P, h->Q, h->R, h->Mm, (int)h->NR, K,
+        (int)h->m, eps_m, 0);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 1;
+    return;
+  }
+  const int rpb = 256 / K;
+  const size_t smem = (size_t)K * (K + 1) * 8 + rpb * K * 4;
+  rk::k2b_partial<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
+      h->ctl, h->P, h->R, (int)h->NR, K, (int)h->m, 1, h->UI);
+  rk::k2b_partial<<<(unsigned)((h->NC + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
+      h->ctl, h->Q, h->R, (int)h->NC, K, (int)h->m, 0, h->UJ);
+  RK_CUDA(cudaGetLastError());
+  const size_t cnt = (size_t)h->piece * K;
+  // reduce-scatter in place: the own piece's sum lands at its slot
+  RK_NCCL(ncclReduceScatter(h->UI, h->UI + (size_t)h->gj * cnt, cnt, ncclDouble, ncclSum, h->rowc,
+                            h->stream));
+  RK_NCCL(ncclReduceScatter(h->UJ, h->UJ + (size_t)h->gi * cnt, cnt, ncclDouble, ncclSum, h->colc,
+                            h->stream));
+  rk::k2b_apply_own<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
+      h->ctl, h->Arow + (size_t)h->gj * cnt, h->UI + (size_t)h->gj * cnt, h->UJ + (size_t)h->gi * cnt,
+      h->Mm, (int)h->piece, K, eps_m);
+  RK_CUDA(cudaGetLastError());
+  grid_allgather_a(h);
+  launch_emit(h);
+  h->launches += 3;
+}
+
+void enqueue_iteration(rk_handle* h, bool timed) {
+  launch_k1(h, timed);
+  launch_k5(h, 1);
+  launch_k2a(h, 1);
+  if (h->grid()) grid_allreduce_parts(h, true);
+  launch_k2f(h, 0, 1);
+  launch_k2m(h, 0);
+  launch_k2b(h);
+}
+
+void enqueue_tail(rk_handle* h) {
+  rk::set_tail<<<1, 1, 0, h->stream>>>(h->ctl, 1);
+  launch_k1(h, false);
+  launch_k5(h, 1);
+  launch_k2a(h, 1);
+  if (h->grid()) grid_allreduce_parts(h, true);
+  launch_k2f(h, 1, 1);
+  launch_k2m(h, 1);
+}
+
+void reset_ctl(rk_handle* h, int track, double tol, int max_iters) {
+  Ctl c;
+  std::memset(&c, 0, sizeof(c));
+  c.track = track;
+  c.tol = tol;
+  c.eps = h->eps;
+  c.norm2 = h->norm2;
+  c.norm2_dev = h->norm2_dev;
+  c.direct_thresh = 0.2;
+  c.max_iters = max_iters;
+  *h->ctl_host = c;
+  RK_CUDA(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+}
+
+void read_ctl(rk_handle* h) {
+  RK_CUDA(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+void ensure_trace(rk_handle* h, int cap) {
+  if (cap + 1 > h->trace_cap) {
+    dfree(h->trace_dev);
+    h->trace_cap = cap + 1;
+    h->trace_dev = dalloc<double>(h->trace_cap);
+  }
+}
+
+void check_ready(rk_handle* h) {
+  RK_REQUIRE(h != nullptr, RK_ERR_DATA, "null handle");
+  RK_REQUIRE(h->have_x, RK_ERR_DATA, "no tensor uploaded");
+  RK_CUDA(cudaSetDevice(h->dev));
+}
+
+void finish_upload_norm(rk_handle* h, bool exact_from_dev) {
+  std::vector<double> p(h->nnp), p2(h->nnp);
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  RK_CUDA(cudaMemcpy(p.data(), h->npart, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
+  RK_CUDA(cudaMemcpy(p2.data(), h->npart2, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
+  double s = 0.0, s2 = 0.0;
+  for (int i = 0; i < h->nnp; ++i) {
+    s += p[i];
+    s2 += p2[i];
+  }
+  h->norm2_dev = s;
+  if (exact_from_dev) h->norm2 = s2;
+  if (h->grid()) {
+    double v[2] = {h->norm2_dev, exact_from_dev ? h->norm2 : 0.0};
+    double* d = h->red;
+    RK_CUDA(cudaMemcpy(d, v, sizeof(v), cudaMemcpyHostToDevice));
+    RK_NCCL(ncclAllReduce(d, d, 2, ncclDouble, ncclSum, h->world, h->stream));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    RK_CUDA(cudaMemcpy(v, d, sizeof(v), cudaMemcpyDeviceToHost));
+    h->norm2_dev = v[0];
+    if (exact_from_dev) h->norm2 = v[1];
+  }
+  h->norm2_dev0 = h->norm2_dev;
+}
+
+void set_block_dims(rk_handle* h, int64_t rows_valid, int64_t cols_valid, int64_t NR, int64_t NC) {
+  h->rows_valid = rows_valid;
+  h->cols_valid = cols_valid;
+  h->NR = NR;
+  h->NC = NC;
+}
+
+void alloc_tensor(rk_handle* h) {
+  dfree(h->Xh);
+  dfree(h->Xl);
+  dfree(h->Xh0);
+  dfree(h->Xl0);
+  h->Xh0 = h->Xl0 = nullptr;
+  const size_t count = (size_t)h->m * h->NR * h->NC;
+  h->Xh = dalloc<__nv_bfloat16>(count);
+  h->Xl = dalloc<__nv_bfloat16>(count);
+}
+
+template <typename T>
+void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
+  // chunks of host rows through a pinned staging ring when the host buffer is
+  // pageable; straight async copies when it is already pinned.
+  cudaPointerAttributes attr;
+  bool pinned = cudaPointerGetAttributes(&attr, x) == cudaSuccess &&
+                (attr.type == cudaMemoryTypeHost);
+  cudaGetLastError();
+  const size_t row_bytes = (size_t)cols * sizeof(T);
+  const size_t chunk_bytes = 64ull << 20;
+  const int64_t rows_per = std::max<int64_t>(1, (int64_t)(chunk_bytes / row_bytes));
+  T* dstage[2] = {dalloc<T>((size_t)rows_per * cols), dalloc<T>((size_t)rows_per * cols)};
+  T* hstage[2] = {nullptr, nullptr};
+  if (!pinned)
+    for (int i = 0; i < 2; ++i) RK_CUDA(cudaMallocHost(&hstage[i], (size_t)rows_per * row_bytes));
+  cudaEvent_t done[2];
+  for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  int slot = 0;
+  for (int64_t t = 0; t < h->m; ++t) {
+    for (int64_t r0 = 0; r0 < rows; r0 += rows_per) {
+      const int64_t nrow = std::min(rows_per, rows - r0);
+      const T* src = x + ((size_t)t * rows + r0) * cols;
+      if (used[slot]) RK_CUDA(cudaEventSynchronize(done[slot]));
+      const T* from = src;
+      if (!pinned) {
+        std::memcpy(hstage[slot], src, (size_t)nrow * row_bytes);
+        from = hstage[slot];
+      }
+      RK_CUDA(cudaMemcpyAsync(dstage[slot], from, (size_t)nrow * row_bytes, cudaMemcpyHostToDevice,
+                              h->stream));
+      rk::split_chunk<T><<<h->nnp, rk::kThreads, 0, h->stream>>>(
+          dstage[slot], nrow, cols, h->Xh, h->Xl, h->NR, h->NC, (int)t, r0, h->npart);
+      RK_CUDA(cudaGetLastError());
+      RK_CUDA(cudaEventRecord(done[slot], h->stream));
+      used[slot] = true;
+      slot ^= 1;
+    }
+  }
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(done[i]);
+    dfree(dstage[i]);
+    if (hstage[i]) cudaFreeHost(hstage[i]);
+  }
+}
+
+double host_sq_norm(const void* x, int dtype, size_t count) {
+  double s = 0.0;
+  if (dtype == RK_F32) {
+    const float* p = static_cast<const float*>(x);
+    for (size_t i = 0; i < count; ++i) s += (double)p[i] * (double)p[i];
+  } else {
+    const double* p = static_cast<const double*>(x);
+    for (size_t i = 0; i < count; ++i) s += p[i] * p[i];
+  }
+  return s;
+}
+
+void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iters_done) {
+  // S_t = A^T X_t A with the handle's A (one contraction pass), then sweeps.
+  const int K = h->K;
+  reset_ctl(h, 0, -1.0, 0);
+  launch_k1(h, false);
+  launch_k2a(h, 0);
+  const double* part = h->part;
+  int nb = h->nb;
+  if (h->grid()) {
+    grid_allreduce_parts(h, false);
+    part = h->red;
+    nb = 1;
+  }
+  rk::regress_loop<<<1, 1024, 0, h->stream>>>(part, nb, h->R, h->regS, h->regG, h->regT, h->regRn,
+                                             K, (int)h->m, eps, max_iters, tol, h->d_iters);
+  RK_CUDA(cudaGetLastError());
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  int it = 0;
+  RK_CUDA(cudaMemcpy(&it, h->d_iters, sizeof(int), cudaMemcpyDeviceToHost));
+  if (iters_done) *iters_done = it;
+}
+
+}  // namespace
+
+// =============================== C ABI ======================================
+
+extern "C" {
+
+int rk_version(void) { return 10000; }
+
+const char* rk_last_error(void) { return g_err.c_str(); }
+
+int rk_device_count(int* out) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *out = n;
+  });
+}
+
+int rk_create(int device, int64_t n, int64_t m, int32_t k, int32_t engine, rk_handle** out) {
+  return guarded([&] {
+    RK_REQUIRE(out, RK_ERR_DATA, "null output handle");
+    *out = nullptr;
+    RK_REQUIRE(n >= 1 && m >= 1, RK_ERR_DATA, "need n >= 1 and m >= 1");
+    RK_REQUIRE(1 <= k && k <= n, RK_ERR_DATA,
+               "need 1 <= k <= n, got k=" + std::to_string(k) + ", n=" + std::to_string(n));
+    RK_REQUIRE(k <= 256, RK_ERR_DATA, "device engine supports k <= 256");
+    int ndev = 0;
+    RK_CUDA(cudaGetDeviceCount(&ndev));
+    RK_REQUIRE(device >= 0 && device < ndev, RK_ERR_DEVICE, "no such CUDA device");
+    RK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RK_CUDA(cudaGetDeviceProperties(&prop, device));
+    RK_REQUIRE(prop.major == 10, RK_ERR_DEVICE,
+               std::string("sm_100a build needs a Blackwell (cc 10.x) GPU, found ") + prop.name);
+    rk_handle* h = new rk_handle();
+    h->dev = device;
+    h->num_sms = prop.multiProcessorCount;
+    h->n = n;
+    h->m = m;
+    h->k = k;
+    h->K = (int)round_up(k, 16);
+    h->requested_engine = engine;
+    h->piece = n;
+    set_block_dims(h, n, n, round_up(n, 128), round_up(n, 128));
+    RK_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    RK_CUDA(cudaMalloc(&h->ctl, sizeof(Ctl)));
+    RK_CUDA(cudaMemset(h->ctl, 0, sizeof(Ctl)));
+    RK_CUDA(cudaMallocHost(&h->ctl_host, sizeof(Ctl)));
+    RK_CUDA(cudaMallocHost(&h->stop_host, 2 * sizeof(int)));
+    RK_CUDA(cudaEventCreate(&h->ev_run0));
+    RK_CUDA(cudaEventCreate(&h->ev_run1));
+    h->nnp = h->num_sms * 4;
+    h->npart = dalloc<double>(h->nnp);
+    h->npart2 = dalloc<double>(h->nnp);
+    h->d_iters = dalloc<int>(1);
+    alloc_tensor(h);
+    alloc_factor_buffers(h);
+    *out = h;
+  });
+}
+
+void rk_destroy(rk_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  cudaStreamSynchronize(h->stream);
+  free_factor_buffers(h);
+  dfree(h->Xh);
+  dfree(h->Xl);
+  dfree(h->Xh0);
+  dfree(h->Xl0);
+  dfree(h->ctl);
+  dfree(h->npart);
+  dfree(h->npart2);
+  dfree(h->d_iters);
+  dfree(h->trace_dev);
+  dfree(h->d_colmap);
+  if (h->ctl_host) cudaFreeHost(h->ctl_host);
+  if (h->stop_host) cudaFreeHost(h->stop_host);
+  for (auto e : h->ev_k1) cudaEventDestroy(e);
+  if (h->ev_run0) cudaEventDestroy(h->ev_run0);
+  if (h->ev_run1) cudaEventDestroy(h->ev_run1);
+  if (h->rowc) ncclCommDestroy(h->rowc);
+  if (h->colc) ncclCommDestroy(h->colc);
+  if (h->world) ncclCommDestroy(h->world);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int rk_set_rank(rk_handle* h, int32_t k) {
+  return guarded([&] {
+    RK_REQUIRE(h, RK_ERR_DATA, "null handle");
+    RK_REQUIRE(1 <= k && k <= h->n && k <= 256, RK_ERR_DATA, "bad rank");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    free_factor_buffers(h);
+    h->k = k;
+    h->K = (int)round_up(k, 16);
+    alloc_factor_buffers(h);
+  });
+}
+
+int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
+  return guarded([&] {
+    RK_REQUIRE(h, RK_ERR_DATA, "null handle");
+    if (key == 1) h->profile = value != 0;
+    else if (key == 2) {
+      h->use_graph = value != 0;
+      if (!h->use_graph && h->graph) {
+        cudaGraphExecDestroy(h->graph);
+        h->graph = nullptr;
+      }
+    } else
+      throw RkError{RK_ERR_DATA, "unknown option"};
+  });
+}
+
+int rk_upload_dense(rk_handle* h, const void* x, int32_t dtype) {
+  return guarded([&] {
+    RK_REQUIRE(h && x, RK_ERR_DATA, "null argument");
+    RK_REQUIRE(dtype == RK_F32 || dtype == RK_F64, RK_ERR_DATA, "dtype must be f32 or f64");
+    RK_REQUIRE(!h->grid(), RK_ERR_GRID, "grid handles take rk_upload_block");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaMemsetAsync(h->npart, 0, sizeof(double) * h->nnp, h->stream));
+    RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
+    if (dtype == RK_F32)
+      upload_rows(h, static_cast<const float*>(x), h->n, h->n);
+    else
+      upload_rows(h, static_cast<const double*>(x), h->n, h->n);
+    finish_upload_norm(h, false);
+    h->norm2 = host_sq_norm(x, dtype, (size_t)h->m * h->n * h->n);
+    h->have_x = true;
+    h->perturbed = false;
+  });
+}
+
+int rk_upload_block(rk_handle* h, const void* x, int32_t dtype, int64_t rows, int64_t cols,
+                    double sq_norm_global) {
+  return guarded([&] {
+    RK_REQUIRE(h && x, RK_ERR_DATA, "null argument");
+    RK_REQUIRE(rows == h->rows_valid && cols == h->cols_valid, RK_ERR_GRID,
+               "block shape does not match the rank's grid block");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaMemsetAsync(h->npart, 0, sizeof(double) * h->nnp, h->stream));
+    RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
+    if (dtype == RK_F32)
+      upload_rows(h, static_cast<const float*>(x), rows, cols);
+    else
+      upload_rows(h, static_cast<const double*>(x), rows, cols);
+    finish_upload_norm(h, false);
+    h->norm2 = sq_norm_global;
+    h->have_x = true;
+    h->perturbed = false;
+  });
+}
+
+int rk_fill_uniform(rk_handle* h, uint64_t seed) {
+  return guarded([&] {
+    RK_REQUIRE(h, RK_ERR_DATA, "null handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    rk::fill_uniform<<<h->nnp, rk::kThreads, 0, h->stream>>>(
+        h->Xh, h->Xl, h->NR, h->NC, h->rows_valid, h->cols_valid, h->n,
+        h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0, h->d_colmap, (int)h->m, seed, h->npart,
+        h->npart2);
+    RK_CUDA(cudaGetLastError());
+    finish_upload_norm(h, true);
+    h->have_x = true;
+    h->perturbed = false;
+  });
+}
+
+int rk_uniform_values(uint64_t seed, int64_t offset, int64_t count, float* out) {
+  return guarded([&] {
+    float* d = dalloc<float>((size_t)count);
+    rk::uniform_values<<<1024, 256>>>(d, count, offset, seed);
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, d, sizeof(float) * count, cudaMemcpyDeviceToHost));
+    dfree(d);
+  });
+}
+
+int rk_set_factors(rk_handle* h, const double* A, const double* R) {
+  return guarded([&] {
+    RK_REQUIRE(h && A && R, RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(h->dev));
+    const int K = h->K, k = h->k;
+    // A: global (n, k) -> this rank's row / col sets, zero padded
+    std::vector<double> arow((size_t)h->NR * K, 0.0), acol((size_t)h->NC * K, 0.0);
+    const int64_t r0 = h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0;
+    for (int64_t i = 0; i < h->rows_valid; ++i) {
+      int64_t g = r0 + i;
+      if (g < h->n)
+        for (int c = 0; c < k; ++c) arow[(size_t)i * K + c] = A[g * k + c];
+    }
+    if (h->grid())
+      for (int64_t j = 0; j < h->cols_valid; ++j) {
+        int64_t g = h->colmap[j];
+        if (g < h->n)
+          for (int c = 0; c < k; ++c) acol[(size_t)j * K + c] = A[g * k + c];
+      }
+    std::vector<double> r((size_t)h->m * K * K, 0.0);
+    for (int64_t t = 0; t < h->m; ++t)
+      for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) r[((size_t)t * K + a) * K + b] = R[((size_t)t * k + a) * k + b];
+    RK_CUDA(cudaMemcpyAsync(h->Arow, arow.data(), arow.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    if (h->grid())
+      RK_CUDA(cudaMemcpyAsync(h->Acol, acol.data(), acol.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    RK_CUDA(cudaMemcpyAsync(h->R, r.data(), r.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    launch_emit(h);
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int rk_get_factors(rk_handle* h, double* A, double* R) {
+  return guarded([&] {
+    RK_REQUIRE(h, RK_ERR_DATA, "null handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    const int K = h->K, k = h->k;
+    if (A) {
+      // gather the full A: on a grid every rank's row set covers pc pieces;
+      // the (gi, *) row sets tile all n rows, so all-gather row sets over the
+      // col communicator.
+      std::vector<double> full;
+      if (h->grid()) {
+        const size_t rs = (size_t)h->pc * h->piece * K;
+        double* d = dalloc<double>(rs * h->pr);
+        RK_CUDA(cudaMemcpyAsync(d + (size_t)h->gi * rs, h->Arow, rs * 8, cudaMemcpyDeviceToDevice, h->stream));
+        RK_NCCL(ncclAllGather(d + (size_t)h->gi * rs, d, rs, ncclDouble, h->colc, h->stream));
+        RK_CUDA(cudaStreamSynchronize(h->stream));
+        full.resize(rs * h->pr);
+        RK_CUDA(cudaMemcpy(full.data(), d, full.size() * 8, cudaMemcpyDeviceToHost));
+        dfree(d);
+      } else {
+        full.resize((size_t)h->NR * K);
+        RK_CUDA(cudaMemcpy(full.data(), h->Arow, full.size() * 8, cudaMemcpyDeviceToHost));
+      }
+      for (int64_t i = 0; i < h->n; ++i)
+        for (int c = 0; c < k; ++c) A[i * k + c] = full[(size_t)i * K + c];
+    }
+    if (R) {
+      std::vector<double> r((size_t)h->m * K * K);
+      RK_CUDA(cudaMemcpy(r.data(), h->R, r.size() * 8, cudaMemcpyDeviceToHost));
+      for (int64_t t = 0; t < h->m; ++t)
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) R[((size_t)t * k + a) * k + b] = r[((size_t)t * K + a) * K + b];
+    }
+  });
+}
+
+int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double tol,
+           double* trace_out, int32_t* iters_done) {
+  return guarded([&] {
+    check_ready(h);
+    RK_REQUIRE(iters >= 1, RK_ERR_DATA, "max_iters must be >= 1");
+    if (track_error) RK_REQUIRE(h->norm2 > 0.0, RK_ERR_DATA, "cannot track relative error: tensor norm is zero");
+    if (h->eps != eps && h->graph) {
+      cudaGraphExecDestroy(h->graph);
+      h->graph = nullptr;
+    }
+    h->eps = eps;
+    ensure_trace(h, iters + 1);
+    reset_ctl(h, track_error ? 1 : 0, tol, iters);
+    h->k1_count = 0;
+    h->launches = 0;
+    const bool timed = h->profile;
+    const bool graph = h->use_graph && !timed && !h->grid();
+    if (graph && !h->graph) {
+      cudaGraph_t g;
+      RK_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      const int before = h->launches;
+      enqueue_iteration(h, false);
+      h->iter_launches = h->launches - before;
+      RK_CUDA(cudaStreamEndCapture(h->stream, &g));
+      RK_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
+      cudaGraphDestroy(g);
+    }
+    RK_CUDA(cudaEventRecord(h->ev_run0, h->stream));
+    const int chunk = 16;
+    cudaEvent_t chk[2];
+    for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&chk[i], cudaEventDisableTiming));
+    h->launches = 0;
+    int launched = 0, pending = -1;
+    while (launched < iters) {
+      const int nthis = std::min(chunk, iters - launched);
+      for (int q = 0; q < nthis; ++q) {
+        if (graph) {
+          RK_CUDA(cudaGraphLaunch(h->graph, h->stream));
+          h->launches += h->iter_launches;
+        } else {
+          enqueue_iteration(h, timed);
+        }
+      }
+      launched += nthis;
+      const int slot = (launched / chunk) & 1;
+      RK_CUDA(cudaMemcpyAsync(&h->stop_host[slot], &h->ctl->stop, sizeof(int), cudaMemcpyDeviceToHost,
+                              h->stream));
+      RK_CUDA(cudaEventRecord(chk[slot], h->stream));
+      if (pending >= 0) {
+        RK_CUDA(cudaEventSynchronize(chk[pending]));
+        if (h->stop_host[pending]) break;
+      }
+      pending = slot;
+    }
+    if (track_error) enqueue_tail(h);
+    RK_CUDA(cudaEventRecord(h->ev_run1, h->stream));
+    read_ctl(h);
+    for (int i = 0; i < 2; ++i) cudaEventDestroy(chk[i]);
+    float ms = 0.f;
+    RK_CUDA(cudaEventElapsedTime(&ms, h->ev_run0, h->ev_run1));
+    h->last_ms = ms;
+    h->k1_ms_sum = 0.0;
+    for (int i = 0; i < h->k1_count; ++i) {
+      float e = 0.f;
+      RK_CUDA(cudaEventElapsedTime(&e, h->ev_k1[2 * i], h->ev_k1[2 * i + 1]));
+      h->k1_ms_sum += e;
+    }
+    const Ctl& c = *h->ctl_host;
+    if (iters_done) *iters_done = c.iter;
+    if (track_error && trace_out && c.trace_len > 0)
+      RK_CUDA(cudaMemcpy(trace_out, h->trace_dev, sizeof(double) * c.trace_len, cudaMemcpyDeviceToHost));
+    if (c.nonfinite == 2) throw RkError{RK_ERR_NUMERICAL, "non-finite reconstruction error"};
+    if (c.nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};
+  });
+}
+
+int rk_trace_len(rk_handle* h, int32_t* out) {
+  return guarded([&] { *out = h->ctl_host->trace_len; });
+}
+
+int rk_update_r(rk_handle* h, double eps) {
+  return guarded([&] {
+    check_ready(h);
+    h->eps = eps;
+    reset_ctl(h, 0, -1.0, 1);
+    launch_k1(h, false);
+    launch_k2a(h, 0);
+    if (h->grid()) grid_allreduce_parts(h, false);
+    launch_k2f(h, 0, 0);
+    launch_k2m(h, 2);
+    read_ctl(h);
+    if (h->ctl_host->nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};
+  });
+}
+
+int rk_update_a(rk_handle* h, double eps) {
+  return guarded([&] {
+    check_ready(h);
+    h->eps = eps;
+    reset_ctl(h, 0, -1.0, 1);
+    launch_k1(h, false);
+    launch_k2a(h, 0);
+    if (h->grid()) grid_allreduce_parts(h, false);
+    launch_k2f(h, 3, 0);
+    launch_k2m(h, 2);
+    launch_k2b(h);
+    read_ctl(h);
+    if (h->ctl_host->nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};
+  });
+}
+
+int rk_residual(rk_handle* h, double* sq_residual, double* sq_norm) {
+  return guarded([&] {
+    check_ready(h);
+    reset_ctl(h, 0, -1.0, 0);
+    launch_k5(h, 0);
+    double* out = h->red;
+    rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, h->nr, out);
+    if (h->grid()) RK_NCCL(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, h->world, h->stream));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    double v = 0.0;
+    RK_CUDA(cudaMemcpy(&v, out, sizeof(double), cudaMemcpyDeviceToHost));
+    if (sq_residual) *sq_residual = v;
+    if (sq_norm) *sq_norm = h->norm2;
+  });
+}
+
+int rk_regress_r(rk_handle* h, int32_t max_iters, double tol, double eps, int32_t* iters_done) {
+  return guarded([&] {
+    check_ready(h);
+    regress_core(h, max_iters, tol, eps, iters_done);
+  });
+}
+
+int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+               double delta, int64_t n_global, int64_t row0, int64_t col0, const int64_t* col_map) {
+  return guarded([&] {
+    check_ready(h);
+    (void)col0;
+    (void)col_map;
+    if (!h->Xh0) {
+      const size_t count = (size_t)h->m * h->NR * h->NC;
+      h->Xh0 = dalloc<__nv_bfloat16>(count);
+      h->Xl0 = dalloc<__nv_bfloat16>(count);
+      RK_CUDA(cudaMemcpyAsync(h->Xh0, h->Xh, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      RK_CUDA(cudaMemcpyAsync(h->Xl0, h->Xl, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      h->norm2_dev0 = h->norm2_dev;
+      h->norm2_orig = h->norm2;
+    }
+    rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+    RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
+    rk::perturb_planes<<<h->nnp, rk::kThreads, 0, h->stream>>>(
+        h->Xh0, h->Xl0, h->Xh, h->Xl, h->NR, h->NC, h->rows_valid, h->cols_valid, (int)h->m,
+        n_global, row0, h->d_colmap, st, inc, delta, 0, h->npart);
+    RK_CUDA(cudaGetLastError());
+    finish_upload_norm(h, false);
+    // the trace denominator of a resampled tensor is its own norm
+    h->norm2 = h->norm2_dev;
+    h->perturbed = true;
+  });
+}
+
+int rk_restore(rk_handle* h) {
+  return guarded([&] {
+    check_ready(h);
+    if (h->Xh0) {
+      const size_t count = (size_t)h->m * h->NR * h->NC;
+      RK_CUDA(cudaMemcpyAsync(h->Xh, h->Xh0, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      RK_CUDA(cudaMemcpyAsync(h->Xl, h->Xl0, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      RK_CUDA(cudaStreamSynchronize(h->stream));
+      h->norm2 = h->norm2_orig;
+      h->norm2_dev = h->norm2_dev0;
+    }
+    h->perturbed = false;
+  });
+}
+
+int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                   uint64_t offset, int64_t count, double* out) {
+  return guarded([&] {
+    double* d = dalloc<double>((size_t)count);
+    rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+    const int64_t threads = (count + 63) / 64;
+    rk::pcg64_draws<<<(unsigned)((threads + 255) / 256), 256>>>(st, inc, offset, count, d);
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    dfree(d);
+  });
+}
+
+int rk_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    RK_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int rk_grid_init(rk_handle* h, int32_t pr, int32_t pc, int32_t rank, const void* nccl_id,
+                 int64_t n_global) {
+  return guarded([&] {
+    RK_REQUIRE(h && nccl_id, RK_ERR_DATA, "null argument");
+    RK_REQUIRE(pr >= 1 && pc >= 1 && rank >= 0 && rank < pr * pc, RK_ERR_GRID, "bad grid shape");
+    RK_REQUIRE(n_global == h->n, RK_ERR_GRID, "n mismatch");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    const int p = pr * pc;
+    h->pr = pr;
+    h->pc = pc;
+    h->rank = rank;
+    h->gi = rank / pc;
+    h->gj = rank % pc;
+    h->piece = (h->n + p - 1) / p;
+    const int64_t b = h->piece;
+    set_block_dims(h, pc * b, pr * b, round_up(pc * b, 128), round_up(pr * b, 128));
+    h->colmap.resize(pr * b);
+    for (int ip = 0; ip < pr; ++ip)
+      for (int64_t r = 0; r < b; ++r) h->colmap[ip * b + r] = ((int64_t)ip * pc + h->gj) * b + r;
+    dfree(h->d_colmap);
+    h->d_colmap = dalloc<int64_t>(h->colmap.size());
+    RK_CUDA(cudaMemcpy(h->d_colmap, h->colmap.data(), h->colmap.size() * 8, cudaMemcpyHostToDevice));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    if (p > 1) {
+      RK_NCCL(ncclCommInitRank(&h->world, p, id, rank));
+      RK_NCCL(ncclCommSplit(h->world, h->gi, h->gj, &h->rowc, nullptr));
+      RK_NCCL(ncclCommSplit(h->world, h->gj, h->gi, &h->colc, nullptr));
+    }
+    free_factor_buffers(h);
+    alloc_tensor(h);
+    alloc_factor_buffers(h);
+    h->have_x = false;
+  });
+}
+
+int rk_grid_block(rk_handle* h, int64_t* out, int32_t n_out) {
+  return guarded([&] {
+    int64_t v[8] = {h->gi, h->gj, h->piece, h->rows_valid, h->cols_valid,
+                    h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0, h->pr, h->pc};
+    for (int i = 0; i < n_out && i < 8; ++i) out[i] = v[i];
+  });
+}
+
+int rk_grid_colmap(rk_handle* h, int64_t* out) {
+  return guarded([&] {
+    for (size_t i = 0; i < h->colmap.size(); ++i) out[i] = h->colmap[i];
+  });
+}
+
+int rk_last_timing(rk_handle* h, double* out, int32_t n_out) {
+  return guarded([&] {
+    double v[4] = {h->last_ms, h->k1_count ? h->k1_ms_sum / h->k1_count : 0.0, (double)h->k1_count,
+                   (double)h->launches};
+    for (int i = 0; i < n_out && i < 4; ++i) out[i] = v[i];
+  });
+}
+
+int rk_time_k1(rk_handle* h, int32_t reps, double* ms_per_launch) {
+  return guarded([&] {
+    check_ready(h);
+    reset_ctl(h, 0, -1.0, 0);
+    cudaEvent_t a, b;
+    RK_CUDA(cudaEventCreate(&a));
+    RK_CUDA(cudaEventCreate(&b));
+    launch_k1(h, false);
+    RK_CUDA(cudaEventRecord(a, h->stream));
+    for (int i = 0; i < reps; ++i) launch_k1(h, false);
+    RK_CUDA(cudaEventRecord(b, h->stream));
+    RK_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    RK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_launch = ms / reps;
+  });
+}
+
+void* rk_stream(rk_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int rk_info(rk_handle* h, int64_t* out, int32_t n_out) {
+  return guarded([&] {
+    RK_REQUIRE(h, RK_ERR_DATA, "null handle");
+    int64_t v[10] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
+                     h->nstrips, h->nslots, h->nb, h->NC};
+    for (int i = 0; i < n_out && i < 10; ++i) out[i] = v[i];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,871 @@
+// RESCAL MU engine: k-wide update kernels (K2*), CUDA-core slice contraction
+// (SIMT K1, used for k_pad > 128 or RK_ENGINE_SIMT), direct residual (K5),
+// tensor upload/split and the PCG64 resampling field (K4).
+//
+// Layout (all row-major, zero padded). The local tensor block has NR rows and
+// NC columns per slice (NR = NC = n_pad on one GPU; on a p_r x p_c grid the
+// rank holds X[:, I_i, J_j]); both are multiples of 128.
+// K = k_pad (multiple of 16), M = m slices.
+//   Xhi/Xlo      bf16 [M][NR][NC]  tensor as hi + lo planes
+//   Arow/Acol    f64  [NR|NC][K]   factor rows of the block's row / col set
+//   A32row/col   f32  [NR|NC][K]   working copies (SIMT K1, K5)
+//   AT*row/col   bf16 [K][NR|NC]   transposed hi/lo operand planes (tcgen05 K1)
+//   R64          f64  [M][K][K]    master cores (replicated)
+//   P            f32  [M][NR][K]   P_t = X_t A_col
+//   Q            f32  [M][NC][K]   Q_t = X_t^T A_row
+#pragma once
+
+#include "rk_common.cuh"
+
+namespace rk {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// K2a: per-block partials of G = A^T A and S_t = A^T P_t (fp64).
+// part[b][0] = G partial, part[b][1+t] = S_t partial; each K*K.
+// Reference: rescal.py:124 (gram) and :129 (A^T X_t A).
+// G is taken over `Aown` (Nown rows: the whole A on one GPU, the rank's own
+// piece on a grid); S_t over the block's row set `Arow` (NR rows) and P.
+__global__ void __launch_bounds__(kThreads) k2a_gram_s(const Ctl* __restrict__ ctl,
+                                                       const double* __restrict__ Aown, int Nown,
+                                                       const double* __restrict__ Arow,
+                                                       const float* __restrict__ P, int NR, int K,
+                                                       int M, double* __restrict__ part,
+                                                       int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ double sh[];
+  constexpr int TR = 32;           // rows per smem tile
+  double* sa = sh;                 // [TR][K]
+  double* sb = sh + TR * K;        // [TR][K]
+  const int b = blockIdx.x;
+  const int KK = K * K;
+  constexpr int Q = 8;             // entries per thread per pass
+  for (int slot = 0; slot <= M; ++slot) {
+    double* out = part + ((size_t)b * (M + 1) + slot) * KK;
+    const int nrows = slot == 0 ? Nown : NR;
+    const int chunk = (nrows + gridDim.x - 1) / gridDim.x;
+    const int r_begin = min(nrows, b * chunk);
+    const int r_end = min(nrows, r_begin + chunk);
+    const double* A = slot == 0 ? Aown : Arow;
+    for (int e0 = 0; e0 < KK; e0 += kThreads * Q) {
+      double acc[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+      for (int r0 = r_begin; r0 < r_end; r0 += TR) {
+        const int rows = min(TR, r_end - r0);
+        for (int idx = threadIdx.x; idx < TR * K; idx += kThreads) {
+          int rr = idx / K, c = idx - rr * K;
+          double av = 0.0, bv = 0.0;
+          if (rr < rows) {
+            av = A[(size_t)(r0 + rr) * K + c];
+            bv = slot == 0 ? av : (double)P[((size_t)(slot - 1) * NR + r0 + rr) * K + c];
+          }
+          sa[idx] = av;
+          sb[idx] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          int e = e0 + q * kThreads + threadIdx.x;
+          if (e < KK) {
+            int c = e / K, d = e - c * K;
+            double s = acc[q];
+            for (int rr = 0; rr < rows; ++rr) s = fma(sa[rr * K + c], sb[rr * K + d], s);
+            acc[q] = s;
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int e = e0 + q * kThreads + threadIdx.x;
+        if (e < KK) out[e] = acc[q];
+      }
+    }
+  }
+}
+
+// C = op(A) * op(B) for K x K fp64 matrices (row-major), all threads of the block.
+RK_DEV void mm_kk(double* __restrict__ C, const double* __restrict__ A, bool ta,
+                  const double* __restrict__ B, bool tb, int K) {
+  const int KK = K * K;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    int i = e / K, j = e - i * K;
+    double s = 0.0;
+    for (int l = 0; l < K; ++l) {
+      double a = ta ? A[l * K + i] : A[i * K + l];
+      double bb = tb ? B[j * K + l] : B[l * K + j];
+      s = fma(a, bb, s);
+    }
+    C[e] = s;
+  }
+}
+
+RK_DEV double block_sum(double v, double* scratch) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += scratch[i];
+    scratch[0] = t;
+  }
+  __syncthreads();
+  t = scratch[0];
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// K2f: one block per slice t. Reduces G and S_t from the K2a partials, forms
+// the trace terms of the CURRENT (A, R_t) — <R_t, S_t> and <R_t, G R_t G> —
+// then the core update (rescal.py:130-132)
+//     R_t' = R_t * S_t / (G (R_t G) + eps)
+// and this slice's share of the A denominator matrix (rescal.py:138-143)
+//     M_t = R_t'^T G R_t' + R_t' G R_t'^T      (deno_A = A sum_t M_t + m eps).
+// `mode`: 0 = full update, 1 = trace terms only, 3 = no core update (M_t from
+// the current cores; split update_a, rescal.py:243-258).
+// scratch (global) is used when K*K*6 doubles do not fit shared memory.
+__global__ void __launch_bounds__(kThreads) k2f_core(const Ctl* __restrict__ ctl,
+                                                     const double* __restrict__ part, int nb,
+                                                     const double* __restrict__ R,
+                                                     double* __restrict__ Rnext,
+                                                     double* __restrict__ Mt,
+                                                     double* __restrict__ tt, int K, int M,
+                                                     double eps, int mode, double* gscratch,
+                                                     int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ double sh[];
+  const int t = blockIdx.x;
+  const int KK = K * K;
+  double* base = gscratch ? gscratch + (size_t)t * 6 * KK : sh;
+  double* G = base;
+  double* S = base + KK;
+  double* Rt = base + 2 * KK;
+  double* T1 = base + 3 * KK;
+  double* T2 = base + 4 * KK;
+  double* Rn = base + 5 * KK;
+  __shared__ double red[32];
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    double g = 0.0, s = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      const double* pb = part + (size_t)b * (M + 1) * KK;
+      g += pb[e];
+      s += pb[(size_t)(1 + t) * KK + e];
+    }
+    G[e] = g;
+    S[e] = s;
+    Rt[e] = R[(size_t)t * KK + e];
+  }
+  __syncthreads();
+  mm_kk(T1, Rt, false, G, false, K);  // R G
+  __syncthreads();
+  mm_kk(T2, G, false, T1, false, K);  // G (R G)
+  __syncthreads();
+  double rs = 0.0, rgrg = 0.0;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    rs += Rt[e] * S[e];
+    rgrg += Rt[e] * T2[e];
+  }
+  rs = block_sum(rs, red);
+  rgrg = block_sum(rgrg, red);
+  if (threadIdx.x == 0) {
+    tt[2 * t] = rs;
+    tt[2 * t + 1] = rgrg;
+  }
+  if (mode == 1) return;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    double v = mode == 3 ? Rt[e] : Rt[e] * S[e] / (T2[e] + eps);
+    Rn[e] = v;
+    Rnext[(size_t)t * KK + e] = v;
+  }
+  __syncthreads();
+  mm_kk(T1, G, false, Rn, false, K);  // G R'
+  __syncthreads();
+  mm_kk(T2, Rn, true, T1, false, K);  // R'^T G R'
+  __syncthreads();
+  mm_kk(T1, G, false, Rn, true, K);   // G R'^T
+  __syncthreads();
+  mm_kk(S, Rn, false, T1, false, K);  // R' G R'^T  (S no longer needed)
+  __syncthreads();
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + S[e];
+}
+
+// ---------------------------------------------------------------------------
+// K2m: single block. Trace bookkeeping for the iterate the K1 pass just read,
+// tolerance stop (rescal.py:218-224), non-finite check of the new cores
+// (rescal.py:168-170), M = sum_t M_t, and the commit R <- R'.
+// mode: 0 = iteration, 1 = tail (trace only), 2 = commit only (split API).
+__global__ void __launch_bounds__(kThreads) k2m_commit(Ctl* __restrict__ ctl,
+                                                       const double* __restrict__ tt,
+                                                       const double* __restrict__ Mt,
+                                                       double* __restrict__ Mout,
+                                                       const double* __restrict__ Rnext,
+                                                       double* __restrict__ R,
+                                                       const double* __restrict__ rpart, int nr,
+                                                       double* __restrict__ trace, int K, int M,
+                                                       int mode) {
+  if (ctl->stop) return;
+  __shared__ double red[32];
+  __shared__ int s_stop;
+  const int KK = K * K;
+  if (threadIdx.x == 0) s_stop = 0;
+  __syncthreads();
+  const bool want_trace = (mode != 2) && ctl->track && (ctl->iter >= 1 || mode == 1);
+  if (want_trace) {
+    double res;
+    if (ctl->direct) {
+      double acc = 0.0;
+      for (int i = threadIdx.x; i < nr; i += blockDim.x) acc += rpart[i];
+      res = block_sum(acc, red);
+    } else {
+      double acc = 0.0;
+      for (int t = threadIdx.x; t < M; t += blockDim.x) acc += -2.0 * tt[2 * t] + tt[2 * t + 1];
+      res = ctl->norm2_dev + block_sum(acc, red);
+    }
+    if (threadIdx.x == 0) {
+      double err = sqrt(fmax(res, 0.0) / ctl->norm2);
+      trace[ctl->trace_len] = err;
+      ctl->trace_len += 1;
+      ctl->last_err = err;
+      if (!isfinite(err)) {
+        ctl->nonfinite = 2;
+        s_stop = 1;
+      } else if (ctl->tol >= 0.0 && err < ctl->tol) {
+        s_stop = 1;
+      } else if (!ctl->direct && err < ctl->direct_thresh) {
+        ctl->direct = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (mode == 1 || s_stop) {
+    if (threadIdx.x == 0) ctl->stop = 1;
+    return;
+  }
+  int bad = 0;
+  for (int e = threadIdx.x; e < M * KK; e += blockDim.x) {
+    double v = Rnext[e];
+    if (!isfinite(v)) bad = 1;
+    R[e] = v;
+  }
+  bad = __syncthreads_or(bad);
+  if (bad) {
+    if (threadIdx.x == 0) {
+      ctl->nonfinite = 1;
+      ctl->stop = 1;
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < M; ++t) s += Mt[(size_t)t * KK + e];
+    Mout[e] = s;
+  }
+  if (threadIdx.x == 0) ctl->iter += 1;
+}
+
+// ---------------------------------------------------------------------------
+// K2b: accumulated A update (rescal.py:133-145), one thread per (row, column):
+//   num_i = sum_t P_t[i] R_t^T + Q_t[i] R_t,  deno_i = A_i Mm + m eps,
+//   A_i <- A_i * num_i / deno_i,
+// then emit the working copies for the next slice contraction.
+// rows_per_block = kThreads / K (K <= 256); R_t staged in shared memory with a
+// +1 pad (bank-conflict free column reads) when K <= 128, else read from L2.
+__global__ void __launch_bounds__(kThreads) k2b_update_a(Ctl* __restrict__ ctl,
+                                                         double* __restrict__ A64,
+                                                         float* __restrict__ A32,
+                                                         __nv_bfloat16* __restrict__ ATh,
+                                                         __nv_bfloat16* __restrict__ ATl,
+                                                         const float* __restrict__ P,
+                                                         const float* __restrict__ Q,
+                                                         const double* __restrict__ R,
+                                                         const double* __restrict__ Mm, int N,
+                                                         int K, int M, double eps_m,
+                                                         int emit_only) {
+  if (ctl->stop) return;
+  extern __shared__ double sh[];
+  const int rpb = kThreads / K;
+  const int r = threadIdx.x / K, c = threadIdx.x - r * K;
+  const bool smem_r = K <= 128;
+  const int ldr = smem_r ? K + 1 : K;
+  double* Rs = sh;  // [K][K+1]
+  float* Ps = reinterpret_cast<float*>(sh + (smem_r ? K * (K + 1) : 0));  // [rpb][K]
+  float* Qs = Ps + rpb * K;
+  const int i = blockIdx.x * rpb + r;
+  const bool active = r < rpb && i < N;
+  double num = 0.0;
+  if (!emit_only) {
+    for (int t = 0; t < M; ++t) {
+      const double* Rt = R + (size_t)t * K * K;
+      __syncthreads();
+      if (smem_r)
+        for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+          int a = e / K, b = e - a * K;
+          Rs[a * ldr + b] = Rt[e];
+        }
+      for (int e = threadIdx.x; e < rpb * K; e += blockDim.x) {
+        int a = e / K, b = e - a * K;
+        int row = blockIdx.x * rpb + a;
+        Ps[e] = row < N ? P[((size_t)t * N + row) * K + b] : 0.f;
+        Qs[e] = row < N ? Q[((size_t)t * N + row) * K + b] : 0.f;
+      }
+      __syncthreads();
+      const double* Rsrc = smem_r ? Rs : Rt;
+      if (active) {
+        const float* pr = Ps + r * K;
+        const float* qr = Qs + r * K;
+        double s = 0.0;
+        for (int d = 0; d < K; ++d)
+          s += (double)pr[d] * Rsrc[c * ldr + d] + (double)qr[d] * Rsrc[d * ldr + c];
+        num += s;
+      }
+    }
+  }
+  double anew = 0.0;
+  if (active) {
+    anew = A64[(size_t)i * K + c];
+    if (!emit_only) {
+      double deno = eps_m;
+      const double* Ai = A64 + (size_t)i * K;
+      for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+      anew = anew * num / deno;
+      if (!isfinite(anew)) {
+        ctl->nonfinite = 1;
+        ctl->stop = 1;
+      }
+    }
+  }
+  // the denominator above reads the whole row: finish all reads first
+  __syncthreads();
+  if (active) {
+    A64[(size_t)i * K + c] = anew;
+    A32[(size_t)i * K + c] = (float)anew;
+    __nv_bfloat16 hi, lo;
+    split_bf16(anew, hi, lo);
+    ATh[(size_t)c * N + i] = hi;
+    ATl[(size_t)c * N + i] = lo;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Grid (p_r x p_c) variants of the A update:
+//   U_I = sum_t P_t R_t^T over the block's row set (NR rows)
+//   U_J = sum_t Q_t R_t   over the block's col set (NC rows)
+// are reduce-scattered over the row / col communicators onto the rank's own
+// piece, then k2b_apply_own updates that piece.
+__global__ void __launch_bounds__(kThreads) k2b_partial(const Ctl* __restrict__ ctl,
+                                                        const float* __restrict__ PQ,
+                                                        const double* __restrict__ R, int rows,
+                                                        int K, int M, int transpose_r,
+                                                        double* __restrict__ U) {
+  if (ctl->stop) return;
+  extern __shared__ double sh[];
+  const int rpb = kThreads / K;
+  const int r = threadIdx.x / K, c = threadIdx.x - r * K;
+  const int ldr = K + 1;
+  double* Rs = sh;
+  float* Ps = reinterpret_cast<float*>(sh + K * ldr);
+  const int i = blockIdx.x * rpb + r;
+  const bool active = r < rpb && i < rows;
+  double num = 0.0;
+  for (int t = 0; t < M; ++t) {
+    const double* Rt = R + (size_t)t * K * K;
+    __syncthreads();
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+      int a = e / K, b = e - a * K;
+      Rs[a * ldr + b] = Rt[e];
+    }
+    for (int e = threadIdx.x; e < rpb * K; e += blockDim.x) {
+      int a = e / K, b = e - a * K;
+      int row = blockIdx.x * rpb + a;
+      Ps[e] = row < rows ? PQ[((size_t)t * rows + row) * K + b] : 0.f;
+    }
+    __syncthreads();
+    if (active) {
+      const float* pr = Ps + r * K;
+      double s = 0.0;
+      if (transpose_r)
+        for (int d = 0; d < K; ++d) s += (double)pr[d] * Rs[c * ldr + d];
+      else
+        for (int d = 0; d < K; ++d) s += (double)pr[d] * Rs[d * ldr + c];
+      num += s;
+    }
+  }
+  if (active) U[(size_t)i * K + c] = num;
+}
+
+__global__ void __launch_bounds__(kThreads) k2b_apply_own(Ctl* __restrict__ ctl,
+                                                          double* __restrict__ Aown,
+                                                          const double* __restrict__ numI,
+                                                          const double* __restrict__ numJ,
+                                                          const double* __restrict__ Mm, int rows,
+                                                          int K, double eps_m) {
+  if (ctl->stop) return;
+  const int rpb = kThreads / K;
+  const int r = threadIdx.x / K, c = threadIdx.x - r * K;
+  const int i = blockIdx.x * rpb + r;
+  const bool active = r < rpb && i < rows;
+  double anew = 0.0;
+  if (active) {
+    const double* Ai = Aown + (size_t)i * K;
+    double deno = eps_m;
+    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+    const double num = numI[(size_t)i * K + c] + numJ[(size_t)i * K + c];
+    anew = Ai[c] * num / deno;
+    if (!isfinite(anew)) {
+      ctl->nonfinite = 1;
+      ctl->stop = 1;
+    }
+  }
+  __syncthreads();
+  if (active) Aown[(size_t)i * K + c] = anew;
+}
+
+// fp64 factor rows -> fp32 copy and transposed bf16 hi/lo operand planes.
+__global__ void __launch_bounds__(kThreads) emit_operands(const double* __restrict__ A, int rows,
+                                                          int K, float* __restrict__ A32,
+                                                          __nv_bfloat16* __restrict__ ATh,
+                                                          __nv_bfloat16* __restrict__ ATl) {
+  const int64_t total = (int64_t)rows * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / K), c = (int)(e - (int64_t)i * K);
+    const double v = A[e];
+    A32[e] = (float)v;
+    __nv_bfloat16 hi, lo;
+    split_bf16(v, hi, lo);
+    ATh[(size_t)c * rows + i] = hi;
+    ATl[(size_t)c * rows + i] = lo;
+  }
+}
+
+// Sum the K2a per-block partials into one (M+1)*K*K buffer (+ trailing
+// scalars copied through) before the world all-reduce.
+__global__ void reduce_parts(const double* __restrict__ part, int nb, int len,
+                             double* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[(size_t)b * len + e];
+    out[e] = s;
+  }
+}
+
+__global__ void sum_scalars(const double* __restrict__ v, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+__global__ void set_tail(Ctl* ctl, int v) { ctl->tail = v; }
+
+// ---------------------------------------------------------------------------
+// SIMT K1 (CUDA cores, fp32): P_t = X_t A (one block per 32-row strip) and
+// Q_t = X_t^T A (one block per 32-column strip). Deterministic, no partials.
+// Used for k_pad > 128 (TMEM budget) or when RK_ENGINE_SIMT is forced.
+__global__ void __launch_bounds__(kThreads) k1_simt_p(const Ctl* __restrict__ ctl,
+                                                      const __nv_bfloat16* __restrict__ Xh,
+                                                      const __nv_bfloat16* __restrict__ Xl,
+                                                      const float* __restrict__ A32col,
+                                                      float* __restrict__ P, int NR, int NC,
+                                                      int K, int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ float shf[];
+  constexpr int BR = 32, BC = 64;
+  float* xs = shf;             // [BR][BC+1]
+  float* as = shf + BR * (BC + 1);  // [BC][K]
+  const int t = blockIdx.y;
+  const int i0 = blockIdx.x * BR;
+  const int r = threadIdx.x >> 3, cg = threadIdx.x & 7;
+  const size_t sl = (size_t)t * NR * NC;
+  float acc[32];
+  const int nc = (K + 7) / 8;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+  for (int j0 = 0; j0 < NC; j0 += BC) {
+    for (int e = threadIdx.x; e < BR * BC; e += kThreads) {
+      int rr = e / BC, cc = e - rr * BC;
+      size_t off = sl + (size_t)(i0 + rr) * NC + j0 + cc;
+      xs[rr * (BC + 1) + cc] = join_bf16(Xh[off], Xl[off]);
+    }
+    for (int e = threadIdx.x; e < BC * K; e += kThreads) as[e] = A32col[(size_t)j0 * K + e];
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = 0; jj < BC; ++jj) {
+      float x = xs[r * (BC + 1) + jj];
+      const float* ar = as + jj * K;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < nc && cg + 8 * q < K) acc[q] = fmaf(x, ar[cg + 8 * q], acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q < nc && cg + 8 * q < K) P[((size_t)t * NR + i0 + r) * K + cg + 8 * q] = acc[q];
+}
+
+__global__ void __launch_bounds__(kThreads) k1_simt_q(const Ctl* __restrict__ ctl,
+                                                      const __nv_bfloat16* __restrict__ Xh,
+                                                      const __nv_bfloat16* __restrict__ Xl,
+                                                      const float* __restrict__ A32row,
+                                                      float* __restrict__ Qo, int NR, int NC,
+                                                      int K, int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ float shf[];
+  constexpr int BR = 64, BC = 32;
+  float* xs = shf;                  // [BR][BC+1]
+  float* as = shf + BR * (BC + 1);  // [BR][K]
+  const int t = blockIdx.y;
+  const int j0 = blockIdx.x * BC;
+  const int cl = threadIdx.x >> 3, cg = threadIdx.x & 7;
+  const size_t sl = (size_t)t * NR * NC;
+  float acc[32];
+  const int nc = (K + 7) / 8;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+  for (int i0 = 0; i0 < NR; i0 += BR) {
+    for (int e = threadIdx.x; e < BR * BC; e += kThreads) {
+      int rr = e / BC, cc = e - rr * BC;
+      size_t off = sl + (size_t)(i0 + rr) * NC + j0 + cc;
+      xs[rr * (BC + 1) + cc] = join_bf16(Xh[off], Xl[off]);
+    }
+    for (int e = threadIdx.x; e < BR * K; e += kThreads) as[e] = A32row[(size_t)i0 * K + e];
+    __syncthreads();
+#pragma unroll 4
+    for (int ii = 0; ii < BR; ++ii) {
+      float x = xs[ii * (BC + 1) + cl];
+      const float* ar = as + ii * K;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < nc && cg + 8 * q < K) acc[q] = fmaf(x, ar[cg + 8 * q], acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q < nc && cg + 8 * q < K) Qo[((size_t)t * NC + j0 + cl) * K + cg + 8 * q] = acc[q];
+}
+
+// ---------------------------------------------------------------------------
+// K5: direct residual sum_t ||X_t - (A R_t) A^T||^2 (rescal.py:149-157) over
+// 64x64 tiles of the local block, grid-stride; fp32 reconstruction, fp64
+// accumulation; one partial per block, summed in a fixed order later.
+// rows_valid / cols_valid bound the real (unpadded) entries.
+__global__ void __launch_bounds__(kThreads) k5_residual(const Ctl* __restrict__ ctl,
+                                                        const __nv_bfloat16* __restrict__ Xh,
+                                                        const __nv_bfloat16* __restrict__ Xl,
+                                                        const float* __restrict__ A32row,
+                                                        const float* __restrict__ A32col,
+                                                        const double* __restrict__ R, int NR,
+                                                        int NC, int K, int M, int rows_valid,
+                                                        int cols_valid, double* __restrict__ part,
+                                                        int gate) {
+  // gate: 1 = iteration use — run only in direct mode while tracking
+  if (gate && (ctl->stop || !ctl->direct || !ctl->track || (ctl->iter < 1 && !ctl->tail))) return;
+  extern __shared__ float shf[];
+  constexpr int T = 64;
+  float* ar = shf;               // [T][K+1]  (A R_t)[I]
+  float* aj = ar + T * (K + 1);  // [T][K+1]  A[J]
+  float* rt = aj + T * (K + 1);  // [K][K] (K <= 128), else R read from L2
+  __shared__ double red[32];
+  const int nti = (rows_valid + T - 1) / T, ntj = (cols_valid + T - 1) / T;
+  const long long per_slice = (long long)nti * ntj;
+  const long long ntiles = (long long)M * per_slice;
+  double acc = 0.0;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
+  int cur_t = -1;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int t = (int)(tile / per_slice);
+    const int rem = (int)(tile - (long long)t * per_slice);
+    const int ib = rem / ntj, jb = rem - ib * ntj;
+    __syncthreads();
+    if (t != cur_t && K <= 128) {
+      for (int e = threadIdx.x; e < K * K; e += kThreads) rt[e] = (float)R[(size_t)t * K * K + e];
+      __syncthreads();
+    }
+    cur_t = t;
+    const double* Rg = R + (size_t)t * K * K;
+    for (int e = threadIdx.x; e < T * K; e += kThreads) {
+      int rr = e / K, c = e - rr * K;
+      int i = ib * T + rr, j = jb * T + rr;
+      float s = 0.f;
+      if (i < NR) {
+        const float* a = A32row + (size_t)i * K;
+        if (K <= 128)
+          for (int d = 0; d < K; ++d) s = fmaf(a[d], rt[d * K + c], s);
+        else
+          for (int d = 0; d < K; ++d) s = fmaf(a[d], (float)Rg[d * K + c], s);
+      }
+      ar[rr * (K + 1) + c] = s;
+      aj[rr * (K + 1) + c] = j < NC ? A32col[(size_t)j * K + c] : 0.f;
+    }
+    __syncthreads();
+    const size_t sl = (size_t)t * NR * NC;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int rr = ty + 16 * a;
+      const int i = ib * T + rr;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int cc = tx + 16 * b;
+        const int j = jb * T + cc;
+        if (i < rows_valid && j < cols_valid) {
+          float rec = 0.f;
+          for (int c = 0; c < K; ++c) rec = fmaf(ar[rr * (K + 1) + c], aj[cc * (K + 1) + c], rec);
+          size_t off = sl + (size_t)i * NC + j;
+          float d = join_bf16(Xh[off], Xl[off]) - rec;
+          acc += (double)d * (double)d;
+        }
+      }
+    }
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Upload: one chunk of host rows [r0, r0+rows) of slice t with `cols` valid
+// columns (host row pitch = cols), staged on the device in the host dtype ->
+// bf16 hi/lo planes with row pitch NC. Adds the chunk's fp64 sum of (hi+lo)^2
+// to norm_part[blockIdx.x].
+template <typename T>
+__global__ void __launch_bounds__(kThreads) split_chunk(const T* __restrict__ src, int64_t rows,
+                                                        int64_t cols, __nv_bfloat16* __restrict__ Xh,
+                                                        __nv_bfloat16* __restrict__ Xl, int64_t NR,
+                                                        int64_t NC, int t, int64_t r0,
+                                                        double* __restrict__ norm_part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * kThreads) {
+    int64_t rr = e / cols, cc = e - rr * cols;
+    double v = (double)src[e];
+    __nv_bfloat16 hi, lo;
+    split_bf16(v, hi, lo);
+    size_t off = ((size_t)t * NR + r0 + rr) * NC + cc;
+    Xh[off] = hi;
+    Xl[off] = lo;
+    double w = (double)join_bf16(hi, lo);
+    acc += w * w;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) norm_part[blockIdx.x] += acc;
+}
+
+// Synthetic uniform input directly on the device (benchmarks): element
+// (t, i, j) of the GLOBAL n x n tensor is uniform01_f32(seed, (t*n + i)*n + j).
+// The block holds global rows row0 + [0, rows) and global cols colmap[0, cols).
+__global__ void __launch_bounds__(kThreads) fill_uniform(__nv_bfloat16* __restrict__ Xh,
+                                                         __nv_bfloat16* __restrict__ Xl,
+                                                         int64_t NR, int64_t NC, int64_t rows,
+                                                         int64_t cols, int64_t n_global,
+                                                         int64_t row0,
+                                                         const int64_t* __restrict__ colmap,
+                                                         int M, uint64_t seed,
+                                                         double* __restrict__ norm_part,
+                                                         double* __restrict__ norm_part_exact) {
+  __shared__ double red[32];
+  double acc = 0.0, acc2 = 0.0;
+  const int64_t total = (int64_t)M * rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * kThreads) {
+    int64_t t = e / (rows * cols), rem = e - t * rows * cols, i = rem / cols, j = rem - i * cols;
+    int64_t gj = colmap ? colmap[j] : j;
+    float v = uniform01_f32(seed, (uint64_t)((t * n_global + row0 + i) * n_global + gj));
+    __nv_bfloat16 hi, lo;
+    split_bf16((double)v, hi, lo);
+    size_t off = ((size_t)t * NR + i) * NC + j;
+    Xh[off] = hi;
+    Xl[off] = lo;
+    double w = (double)join_bf16(hi, lo);
+    acc += w * w;
+    acc2 += (double)v * (double)v;
+  }
+  acc = block_sum(acc, red);
+  acc2 = block_sum(acc2, red);
+  if (threadIdx.x == 0) {
+    norm_part[blockIdx.x] = acc;
+    norm_part_exact[blockIdx.x] = acc2;
+  }
+}
+
+// The same counter-based values, for host-side copies of a synthetic input
+// (bench e2e arm and CPU baseline use the identical tensor).
+__global__ void __launch_bounds__(kThreads) uniform_values(float* __restrict__ out, int64_t count,
+                                                           int64_t offset, uint64_t seed) {
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * kThreads)
+    out[e] = uniform01_f32(seed, (uint64_t)(offset + e));
+}
+
+// ---------------------------------------------------------------------------
+// regress_r (rescal.py:293-324): cores refitted with A frozen, starting from
+// all-ones, Jacobi over slices, stop when ||R'-R||_F / ||R||_F < tol (fp64).
+// Single block; G and S_t come from the K2a partials. Work is m*k^3 per sweep.
+__global__ void __launch_bounds__(1024) regress_loop(const double* __restrict__ part, int nb,
+                                                     double* __restrict__ R, double* __restrict__ S,
+                                                     double* __restrict__ G, double* __restrict__ T1,
+                                                     double* __restrict__ Rn, int K, int M,
+                                                     double eps, int max_iters, double tol,
+                                                     int* __restrict__ iters_done) {
+  __shared__ double red[32];
+  const int KK = K * K;
+  const int MKK = M * KK;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    double g = 0.0;
+    for (int b = 0; b < nb; ++b) g += part[(size_t)b * (M + 1) * KK + e];
+    G[e] = g;
+  }
+  for (int e = threadIdx.x; e < MKK; e += blockDim.x) {
+    const int t = e / KK, q = e - t * KK;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[((size_t)b * (M + 1) + 1 + t) * KK + q];
+    S[e] = s;
+    R[e] = 1.0;
+  }
+  __syncthreads();
+  int it = 0;
+  for (; it < max_iters; ++it) {
+    for (int e = threadIdx.x; e < MKK; e += blockDim.x) {  // T1 = R_t G
+      const int t = e / KK, q = e - t * KK, i = q / K, j = q - i * K;
+      const double* Rt = R + (size_t)t * KK;
+      double s = 0.0;
+      for (int l = 0; l < K; ++l) s = fma(Rt[i * K + l], G[l * K + j], s);
+      T1[e] = s;
+    }
+    __syncthreads();
+    double base = 0.0, step = 0.0;
+    for (int e = threadIdx.x; e < MKK; e += blockDim.x) {  // R' = R * S / (G (R G) + eps)
+      const int t = e / KK, q = e - t * KK, i = q / K, j = q - i * K;
+      const double* Tt = T1 + (size_t)t * KK;
+      double s = 0.0;
+      for (int l = 0; l < K; ++l) s = fma(G[i * K + l], Tt[l * K + j], s);
+      const double r = R[e];
+      const double v = r * S[e] / (s + eps);
+      base += r * r;
+      step += (v - r) * (v - r);
+      Rn[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < MKK; e += blockDim.x) R[e] = Rn[e];
+    base = block_sum(base, red);  // block_sum synchronises
+    step = block_sum(step, red);
+    if (tol >= 0.0 && (base == 0.0 || sqrt(step) / sqrt(base) < tol)) {
+      ++it;
+      break;
+    }
+  }
+  if (threadIdx.x == 0) *iters_done = it;
+}
+
+// ---------------------------------------------------------------------------
+// K4: PCG64 (XSL-RR 128/64) resampling field, bit-exact with numpy's
+// default_rng(SeedSequence((base_seed, 3, q))).random((m, n, n))
+// (dist_rescal.py:164-171). Element e = t*n*n + i*n + j consumes draw e; each
+// thread jumps ahead to the start of its run (Brown's algorithm) and steps.
+struct u128 {
+  uint64_t lo, hi;
+};
+RK_DEV u128 mul128(u128 a, u128 b) {
+  u128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+RK_DEV u128 add128(u128 a, u128 b) {
+  u128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+RK_DEV u128 pcg_mult() { return u128{4865540595714422341ull, 2549297995355413924ull}; }
+
+RK_DEV u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+  u128 acc_mult{1ull, 0ull}, acc_plus{0ull, 0ull};
+  u128 cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1ull) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, u128{1ull, 0ull}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  return add128(mul128(acc_mult, state), acc_plus);
+}
+
+RK_DEV double pcg_next_double(u128& state, u128 inc) {
+  state = add128(mul128(state, pcg_mult()), inc);
+  uint64_t x = state.hi ^ state.lo;
+  unsigned rot = (unsigned)(state.hi >> 58);
+  uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
+  return (double)(out >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Raw draws (tests): out[i] = u_{offset+i}.
+__global__ void pcg64_draws(u128 state, u128 inc, uint64_t offset, int64_t count, double* out) {
+  const int64_t per = 64;
+  int64_t start = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * per;
+  if (start >= count) return;
+  u128 s = pcg_advance(state, inc, offset + (uint64_t)start);
+  int64_t end = min(count, start + per);
+  for (int64_t e = start; e < end; ++e) out[e] = pcg_next_double(s, inc);
+}
+
+// Perturb the device tensor: X'[t][il][jl] = X0[t][il][jl] * f(e), with
+// e = t*n*n + (row0+il)*n + colmap[jl] (global element index), f in fp64
+// then cast to the tensor dtype (dist_rescal.py:170-171,198,215).
+// One thread per run of `per` consecutive local columns of one row.
+__global__ void __launch_bounds__(kThreads) perturb_planes(
+    const __nv_bfloat16* __restrict__ Xh0, const __nv_bfloat16* __restrict__ Xl0,
+    __nv_bfloat16* __restrict__ Xh, __nv_bfloat16* __restrict__ Xl, int64_t NR, int64_t NC,
+    int64_t rows, int64_t cols, int M, int64_t n_global, int64_t row0,
+    const int64_t* __restrict__ colmap,
+    u128 state, u128 inc, double delta, int dtype_f32, double* __restrict__ norm_part) {
+  __shared__ double red[32];
+  constexpr int per = 64;
+  const int64_t runs_per_row = (cols + per - 1) / per;
+  const int64_t nruns = (int64_t)M * rows * runs_per_row;
+  double acc = 0.0;
+  for (int64_t run = (int64_t)blockIdx.x * kThreads + threadIdx.x; run < nruns;
+       run += (int64_t)gridDim.x * kThreads) {
+    int64_t t = run / (rows * runs_per_row);
+    int64_t rem = run - t * rows * runs_per_row;
+    int64_t il = rem / runs_per_row;
+    int64_t j0 = (rem - il * runs_per_row) * per;
+    int64_t j1 = min(cols, j0 + per);
+    // contiguous global columns within the run (colmap is piecewise
+    // contiguous; re-jump whenever it is not)
+    int64_t next_e = -1;
+    u128 s{0, 0};
+    for (int64_t jl = j0; jl < j1; ++jl) {
+      int64_t gj = colmap ? colmap[jl] : jl;
+      int64_t e = ((int64_t)t * n_global + row0 + il) * n_global + gj;
+      if (e != next_e) s = pcg_advance(state, inc, (uint64_t)e);
+      double u = pcg_next_double(s, inc);
+      next_e = e + 1;
+      double f = 1.0 + delta * (2.0 * u - 1.0);
+      size_t off = ((size_t)t * NR + il) * NC + jl;
+      double x = (double)join_bf16(Xh0[off], Xl0[off]);
+      double v = dtype_f32 ? (double)((float)x * (float)f) : x * f;
+      __nv_bfloat16 hi, lo;
+      split_bf16(v, hi, lo);
+      Xh[off] = hi;
+      Xl[off] = lo;
+      double w = (double)join_bf16(hi, lo);
+      acc += w * w;
+    }
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) norm_part[blockIdx.x] = acc;
+}
+
+}  // namespace rk

@@ -1,0 +1,243 @@
+"""Drop-in RESCAL MU solver API backed by the sm_100a engine.
+
+Mirrors the public functions of the reference serial solver
+(pkg/src/rescalkit/rescal.py) — same names, signatures, defaults, dtypes and
+error classes — but every tensor contraction runs in ``librescal_b200.so``:
+
+  rescal_solve      rescal.py:186-225   -> rk_set_factors + rk_run + rk_get_factors
+  update_r          rescal.py:228-240   -> rk_update_r
+  update_a          rescal.py:243-258   -> rk_update_a
+  rel_error         rescal.py:269-276   -> rk_residual
+  regress_r         rescal.py:293-324   -> rk_regress_r
+  finalize_normalize, random_init       host k-sized math (identical to the reference)
+
+Numerics: the tensor is held as bf16 hi+lo planes and contracted with 3xBF16
+tcgen05 MMAs (fp32 accumulate); all k x k algebra and the factor masters are
+fp64 on the device. Results are returned in x.dtype (rescal.py:205-209).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .exceptions import DataError, NumericalError
+from .containers import dense_slices, tensor_dtype
+
+_SEED_TAG_A = 1
+_SEED_TAG_R = 2
+
+
+@dataclass
+class SolverConfig:
+    """Solver settings; defaults and validation as rescal.py:30-53.
+
+    ``engine`` (extension): "auto" | "tc" (tcgen05) | "simt" (CUDA cores);
+    ``device`` (extension): CUDA ordinal, default LOCAL_RANK or 0.
+    """
+
+    max_iters: int = 200
+    epsilon: float = 1e-16
+    tolerance: float | None = None
+    init: str = "random"  # "random" | "nndsvd"
+    seed: int = 0
+    track_error: bool = True
+    engine: str = "auto"
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise DataError(f"max_iters must be >= 1, got {self.max_iters}")
+        if not self.epsilon > 0:
+            raise DataError(f"epsilon must be > 0, got {self.epsilon}")
+        if self.init not in ("random", "nndsvd"):
+            raise DataError(f"unknown init {self.init!r}")
+        if self.engine not in _lib.ENGINES:
+            raise DataError(f"unknown engine {self.engine!r}")
+
+
+@dataclass
+class RescalFactors:
+    """Entity matrix A (n x k) and core stack R (m x k x k); rescal.py:56-88."""
+
+    A: np.ndarray
+    R: np.ndarray
+
+    def __post_init__(self):
+        self.A = np.asarray(self.A)
+        self.R = np.asarray(self.R)
+        if self.A.ndim != 2 or self.R.ndim != 3:
+            raise DataError(f"bad factor shapes {self.A.shape}, {self.R.shape}")
+        if self.R.shape[1] != self.R.shape[2] or self.R.shape[1] != self.A.shape[1]:
+            raise DataError(f"inconsistent latent dimension: A {self.A.shape}, R {self.R.shape}")
+        if (self.A.size and self.A.min() < 0) or (self.R.size and self.R.min() < 0):
+            raise DataError("factors must be non-negative")
+
+    @property
+    def n(self) -> int:
+        return self.A.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.A.shape[1]
+
+    @property
+    def m(self) -> int:
+        return self.R.shape[0]
+
+    def copy(self) -> "RescalFactors":
+        return RescalFactors(self.A.copy(), self.R.copy())
+
+
+def random_init(n: int, k: int, m: int, seed, dtype=np.float64) -> RescalFactors:
+    """Seeded uniform start, partition independent (rescal.py:173-183):
+    A from SeedSequence((seed, 1)), R from SeedSequence((seed, 2)), drawn in
+    fp64 then cast."""
+    ga = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_A)))
+    gr = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_R)))
+    return RescalFactors(ga.random((n, k), dtype=np.float64).astype(dtype),
+                         gr.random((m, k, k), dtype=np.float64).astype(dtype))
+
+
+def finalize_normalize(f: RescalFactors) -> RescalFactors:
+    """Unit-norm columns of A with D R_t D compensation (rescal.py:279-290)."""
+    norms = np.linalg.norm(f.A, axis=0)
+    scale = np.where(norms > 0, norms, 1.0).astype(f.A.dtype)
+    return RescalFactors(f.A / scale, f.R * scale[None, :, None] * scale[None, None, :])
+
+
+# ---------------------------------------------------------------------------
+# engine plumbing
+
+
+def _engine_for(x, k, cfg: SolverConfig):
+    eng = _lib.Engine(x.n, x.m, k, device=cfg.device, engine=cfg.engine)
+    eng.upload(dense_slices(x))
+    return eng
+
+
+def _check_shapes(x, f: RescalFactors) -> None:
+    if f.A.shape[0] != x.n or f.R.shape[0] != x.m:
+        raise DataError(
+            f"shape mismatch: tensor (n={x.n}, m={x.m}) vs factors A {f.A.shape}, R {f.R.shape}")
+
+
+def _to_dtype(a, dt):
+    return np.asarray(a).astype(dt, copy=False)
+
+
+def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, counters=None,
+                 engine: "_lib.Engine | None" = None):
+    """Factorize ``x`` at rank ``k``; returns (RescalFactors, error trace).
+
+    Same contract as rescal.py:186-225: ``initial`` is copied, otherwise the
+    seeded random start; the trace holds err_l after each iteration and the
+    loop stops once err_l < tolerance. ``counters`` is accepted for signature
+    compatibility (device timing replaces MAC counting; see Engine.timing).
+    ``engine`` (extension) reuses a device-resident tensor across calls.
+    """
+    cfg = cfg or SolverConfig()
+    if not 1 <= k <= x.n:
+        raise DataError(f"need 1 <= k <= n, got k={k}, n={x.n}")
+    dt = tensor_dtype(x)
+    if initial is not None:
+        f = initial.copy()
+        if f.A.shape != (x.n, k) or f.R.shape != (x.m, k, k):
+            raise DataError("initial factors do not match tensor/k")
+    elif cfg.init == "nndsvd":
+        raise DataError("init='nndsvd' is not available on the device engine (SURVEY.md §8(f)4)")
+    else:
+        f = random_init(x.n, k, x.m, cfg.seed, dtype=dt)
+    # the reference casts the start to x.dtype (rescal.py:206-208)
+    a0 = _to_dtype(f.A, dt).astype(np.float64)
+    r0 = _to_dtype(f.R, dt).astype(np.float64)
+    own = engine is None
+    eng = engine if engine is not None else _engine_for(x, k, cfg)
+    try:
+        if eng.k != k:
+            eng.set_rank(k)
+        eng.set_factors(a0, r0)
+        eps = float(dt.type(cfg.epsilon))
+        _, trace = eng.run(cfg.max_iters, eps, track_error=cfg.track_error, tol=cfg.tolerance)
+        a, r = eng.get_factors()
+        if counters is not None and hasattr(counters, "add_time"):
+            counters.add_time("device_run", eng.timing()["run_ms"] / 1e3)
+    finally:
+        if own:
+            eng.close()
+    return RescalFactors(a.astype(dt), r.astype(dt)), np.asarray(trace)
+
+
+def update_r(x, f: RescalFactors, cfg: SolverConfig | None = None) -> RescalFactors:
+    """One multiplicative pass over all cores with A fixed (rescal.py:228-240)."""
+    cfg = cfg or SolverConfig()
+    _check_shapes(x, f)
+    dt = f.A.dtype
+    with _engine_for(x, f.k, cfg) as eng:
+        eng.set_factors(f.A.astype(np.float64), f.R.astype(np.float64))
+        eng.update_r(float(dt.type(cfg.epsilon)))
+        _, r = eng.get_factors()
+    return RescalFactors(f.A, r.astype(f.R.dtype))
+
+
+def update_a(x, f: RescalFactors, cfg: SolverConfig | None = None) -> RescalFactors:
+    """One accumulated multiplicative update of A, cores fixed (rescal.py:243-258)."""
+    cfg = cfg or SolverConfig()
+    _check_shapes(x, f)
+    dt = f.A.dtype
+    with _engine_for(x, f.k, cfg) as eng:
+        eng.set_factors(f.A.astype(np.float64), f.R.astype(np.float64))
+        eng.update_a(float(dt.type(cfg.epsilon)))
+        a, _ = eng.get_factors()
+    return RescalFactors(a.astype(dt), f.R)
+
+
+def rel_error(x, f: RescalFactors, engine: "_lib.Engine | None" = None) -> float:
+    """|X - A R A^T|_F / |X|_F (rescal.py:269-276), residual on the device."""
+    _check_shapes(x, f)
+    own = engine is None
+    eng = engine if engine is not None else _engine_for(x, f.k, SolverConfig())
+    try:
+        if eng.k != f.k:
+            eng.set_rank(f.k)
+        eng.set_factors(np.asarray(f.A, dtype=np.float64), np.asarray(f.R, dtype=np.float64))
+        res, nrm = eng.residual()
+    finally:
+        if own:
+            eng.close()
+    if nrm == 0.0:
+        raise DataError("relative error undefined: tensor norm is zero")
+    return float(np.sqrt(res / nrm))
+
+
+def regress_r(x, a_fixed: np.ndarray, cfg: SolverConfig | None = None, max_iters: int = 500,
+              tol: float | None = 1e-8, engine: "_lib.Engine | None" = None) -> np.ndarray:
+    """Refit the cores with A frozen, from all-ones (rescal.py:293-324)."""
+    cfg = cfg or SolverConfig()
+    a = np.asarray(a_fixed)
+    if a.ndim != 2 or a.shape[0] != x.n:
+        raise DataError(f"A must be (n, k) with n={x.n}, got {a.shape}")
+    if a.size and a.min() < 0:
+        raise DataError("A must be non-negative")
+    k = a.shape[1]
+    own = engine is None
+    eng = engine if engine is not None else _engine_for(x, k, cfg)
+    try:
+        if eng.k != k:
+            eng.set_rank(k)
+        eng.set_factors(a.astype(np.float64), np.ones((x.m, k, k)))
+        eng.regress_r(max_iters, tol, float(a.dtype.type(cfg.epsilon)))
+        _, r = eng.get_factors()
+    finally:
+        if own:
+            eng.close()
+    if not (np.isfinite(a).all() and np.isfinite(r).all()):
+        raise NumericalError("non-finite value in factors; aborting")
+    return r.astype(a.dtype)
+
+
+def nndsvd_init(x, k: int, r_update_iters: int = 20, eps: float = 1e-16) -> RescalFactors:
+    """Not on the device path (SURVEY.md §8(f)4 ranks it 'next')."""
+    raise DataError("nndsvd_init is not implemented on the B200 engine; pass initial= factors")
