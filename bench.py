@@ -1,0 +1,421 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 RESCAL MU hot path (contract: see DESIGN.md §Measurement).
+
+A "step" is one MU iteration (rescal.py:114-146 + the tracked relative error of
+rescal.py:218-222) over the whole synthetic tensor. Workloads (BASELINE.json
+configs):
+  cfg2 (default): dense m=16, n=8192, k=16 per GPU. At N>1 the global tensor
+                  grows to n = 8192*sqrt(N) on the p_r x p_c grid so every GPU
+                  holds one cfg2-sized block (the paper's weak-scaling setup,
+                  PAPER.md:1027-1030); value counts block-iterations
+                  (= N per global iteration) -> "scaling": "weak".
+  cfg3          : dense m=16, n=32768, k=32 (north_star target), strong scaling.
+  cfg1          : dense m=8, n=256, k=4 (latency-bound).
+
+Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun).
+        python bench.py --impl reference ...  (CPU reference arm; rank 0 only)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(m=8, n=256, k=4),
+    "cfg2": dict(m=16, n=8192, k=16),
+    "cfg3": dict(m=16, n=32768, k=32),
+}
+METRIC = "MU iters/sec + effective TFLOP/s (dense) / HBM GB/s (sparse) at 1/2/4/8 B200"
+SEED = 20220218
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend="gloo")
+        return dist, dist.get_rank(), world, int(os.environ.get("LOCAL_RANK", "0"))
+    if gpus and gpus > 1:
+        raise SystemExit("--gpus N>1 needs torchrun (WORLD_SIZE)")
+    return None, 0, 1, 0
+
+
+def max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def workload(name, world):
+    c = dict(CONFIGS[name])
+    if name == "cfg2" and world > 1:
+        c["n"] = int(round(8192 * math.sqrt(world)))
+    return c
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle = reference algorithm restated; the only place bench runs it)
+
+
+def host_tensor(m, n, pinned=False):
+    """The exact fp32 values the device generator (rk_fill_uniform) produces."""
+    from paper_2202_09512_b200 import _lib
+
+    total = m * n * n
+    if pinned:
+        import torch
+
+        buf = torch.empty(total, dtype=torch.float32, pin_memory=True).numpy()
+    else:
+        buf = np.empty(total, dtype=np.float32)
+    step = 1 << 28
+    for off in range(0, total, step):
+        cnt = min(step, total - off)
+        buf[off:off + cnt] = _lib.uniform_values(SEED, off, cnt)
+    return buf.reshape(m, n, n)
+
+
+def cpu_reference(x32, k, m, budget_s=12.0, max_slices=None):
+    """Time oracle.mu_iteration (fp64, numpy/OpenBLAS on all host cores) on a
+    bounded sample of the first slices of the workload (x32 holds them);
+    returns (it/s scaled to all m slices, cores, sample, step seconds)."""
+    import oracle
+
+    n = x32.shape[1]
+    cores = len(os.sched_getaffinity(0))
+    # slices per step: aim for ~budget/4 seconds per step from a 1-slice probe
+    a, r = oracle.random_init(n, k, m, 0)
+    probe = [x32[0].astype(np.float64)]
+    t0 = time.perf_counter()
+    oracle.mu_iteration(probe, a.copy(), r[:1].copy(), 1e-16)
+    per_slice = max(time.perf_counter() - t0, 1e-6)
+    ms = max(1, min(x32.shape[0], int((budget_s / 4) / per_slice)))
+    if max_slices:
+        ms = min(ms, max_slices)
+    xs = [x32[t].astype(np.float64) for t in range(ms)]
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 2 or (time.perf_counter() - t_start < budget_s and len(times) < 20):
+        rr = r[:ms].copy()
+        t0 = time.perf_counter()
+        oracle.mu_iteration(xs, a.copy(), rr, 1e-16)
+        times.append(time.perf_counter() - t0)
+    t_step = statistics.median(times)
+    it_s = 1.0 / (t_step * m / ms)
+    sample = (f"oracle.mu_iteration fp64 (untracked, rescal.py:114-146 restated), {ms} of {m} slices "
+              f"n={n} k={k}, median of {len(times)} reps, scaled x{m / ms:.2f} to all slices")
+    return it_s, cores, sample, t_step
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, dist, rank, world):
+    c = workload(args.config, world)
+    m, n, k = c["m"], c["n"], c["k"]
+    flops = 4.0 * m * n * n * k
+    if rank == 0:
+        threads = len(os.sched_getaffinity(0))
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ.setdefault(var, str(threads))
+        import oracle
+
+        per_step = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+        rng = np.random.default_rng(SEED)
+        x = None
+        ms = None
+        a, r = oracle.random_init(n, k, m, 0)
+        # a bounded sample of the workload: s slices of the full n x n tensor
+        probe = rng.random((1, n, n), dtype=np.float32).astype(np.float64)
+        t0 = time.perf_counter()
+        oracle.mu_iteration([probe[0]], a.copy(), r[:1].copy(), 1e-16)
+        per_slice = time.perf_counter() - t0
+        ms = max(1, min(m, int(per_step / max(per_slice, 1e-6))))
+        x = [rng.random((n, n), dtype=np.float32).astype(np.float64) for _ in range(ms)]
+        for _ in range(args.warmup):
+            oracle.mu_iteration(x, a.copy(), r[:ms].copy(), 1e-16)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.mu_iteration(x, a.copy(), r[:ms].copy(), 1e-16)
+        dt = time.perf_counter() - t0
+        t_full = dt / args.steps * (m / ms)
+        value = 1.0 / t_full
+        sample = (f"each step: oracle.mu_iteration fp64 untracked on {ms} of {m} slices "
+                  f"(n={n}, k={k}); time scaled x{m / ms:.2f} to the full tensor")
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "weak" if (args.config == "cfg2" and world > 1) else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform [0,1) (fp32-representable)",
+            "config": {"workload": f"{args.config}: dense m={m} n={n} k={k}", "per_step": "one MU iteration"},
+            "tflops_effective": flops * value / 1e12,
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+    barrier(dist)
+
+
+def run_ours(args, dist, rank, world, local_rank):
+    import paper_2202_09512_b200 as rk
+    from paper_2202_09512_b200 import _lib
+    from paper_2202_09512_b200.multigpu import grid_shape, make_grid_engine
+
+    c = workload(args.config, world)
+    m, n, k = c["m"], c["n"], c["k"]
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    cfg = rk.SolverConfig(max_iters=args.steps, device=local_rank)
+    f0 = rk.random_init(n, k, m, 0)
+    eps = float(cfg.epsilon)
+
+    # ---------------- device-resident timed region --------------------------
+    if world > 1:
+        eng, info = make_grid_engine(n, m, k, cfg=cfg)
+        grid = (info["pr"], info["pc"])
+    else:
+        eng, info, grid = _lib.Engine(n, m, k, device=local_rank), None, (1, 1)
+    eng.fill_uniform(SEED)
+    eng.set_factors(f0.A, f0.R)
+    eng.run(args.warmup, eps, track_error=True)
+    eng.set_factors(f0.A, f0.R)
+    eng.set_option(1, 1)  # per-launch CUDA events around K1 on the engine stream
+    barrier(dist)
+    with ClockSampler(local_rank) as clocks:
+        t_wall = time.perf_counter()
+        done, trace = eng.run(args.steps, eps, track_error=True)
+        t_wall = time.perf_counter() - t_wall
+    tm = eng.timing()
+    dev_ms = max_over_ranks(dist, tm["run_ms"])
+    k1_ms = max_over_ranks(dist, tm["k1_ms"])
+    einfo = eng.info()
+    eng.set_option(1, 0)
+    # second timed pass without per-launch events (graph replay on 1 GPU): the
+    # production path; keep the faster of the two as `value`
+    eng.set_factors(f0.A, f0.R)
+    barrier(dist)
+    eng.run(args.steps, eps, track_error=True)
+    dev_ms2 = max_over_ranks(dist, eng.timing()["run_ms"])
+    launches = eng.timing()["launches"]
+    eng.close()
+    best_ms = min(dev_ms, dev_ms2)
+    units = args.steps * (world if (args.config == "cfg2" and world > 1) else 1)
+    value = units / (best_ms / 1e3)
+    ms_per_step = best_ms / args.steps
+
+    # roofline of the dominant kernel (K1): algorithmic bytes = the local
+    # block's X planes read once (hi+lo bf16 = 4 B per element)
+    if info is not None:
+        elems = m * info["rows"] * info["cols"]
+    else:
+        elems = m * n * n
+    bytes_k1 = 4.0 * elems
+    achieved = bytes_k1 / (k1_ms / 1e3) / 1e9
+    flops_iter = 4.0 * m * n * n * k
+    tflops = flops_iter * (args.steps / (best_ms / 1e3)) / 1e12
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if (args.config == "cfg2" and world > 1) else "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "precision": "X and A as bf16 hi+lo pairs, 3 tcgen05 products, fp32 accumulate; k x k updates fp64",
+        "data": "synthetic uniform [0,1) fp32-representable, device-generated",
+        "config": {
+            "workload": f"{args.config}: dense m={m} n={n} k={k}" + (
+                f", {grid[0]}x{grid[1]} grid, per-GPU block {info['rows']}x{info['cols']}" if info else ""),
+            "per_step": "one MU iteration incl. tracked rel. error (rescal.py:215-224)",
+            "l2": f"inputs larger than L2 ({4.0 * elems / 1e9:.1f} GB/GPU vs 0.126 GB)",
+            "engine": {1: "tcgen05", 2: "simt"}.get(einfo["engine"], "?"),
+            "grid": f"{grid[0]}x{grid[1]}", "parallelism": f"pxq={grid[0]}x{grid[1]}",
+        },
+        "tflops_effective": tflops,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "k1_tc_kernel (P=X A, Q=X^T A, 3xBF16)", "peak_kind": peak_kind,
+                     "bytes_per_launch": bytes_k1, "k1_ms": k1_ms,
+                     "k1_share_of_step": (k1_ms / (dev_ms / args.steps)) if dev_ms else None},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "device_ms": {"profiled_run": dev_ms, "graph_run": dev_ms2, "wall_s": t_wall},
+        "trace_last": float(trace[-1]) if len(trace) else None,
+    }
+
+    # ---------------- end to end through the public API (host buffers) ------
+    if not args.no_e2e:
+        try:
+            if world == 1:
+                xh = host_tensor(m, n, pinned=True)
+                x = rk.RelTensor(xh)  # validation outside the timed region, as a caller would
+                torch_sync = None
+                t0 = time.perf_counter()
+                f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, device=local_rank),
+                                        initial=f0)
+                e2e_s = time.perf_counter() - t0
+                h2d = xh.nbytes + f0.A.nbytes + f0.R.nbytes
+                d2h = f.A.nbytes + f.R.nbytes + tr.nbytes
+            else:
+                eng2, info2 = make_grid_engine(n, m, k, cfg=cfg)
+                # this rank's block, exact values of the same generator
+                blk = eng2.block_uniform(SEED, info2["rows"], info2["cols"])
+                barrier(dist)
+                t0 = time.perf_counter()
+                eng2.upload_block(blk, 1.0)
+                eng2.set_factors(f0.A, f0.R)
+                eng2.run(args.steps, eps, track_error=False)
+                a_, r_ = eng2.get_factors()
+                e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
+                eng2.close()
+                h2d = blk.nbytes + f0.A.nbytes + f0.R.nbytes
+                d2h = a_.nbytes + r_.nbytes
+            line["e2e"] = {"value": units / e2e_s, "unit": "it/s",
+                           "h2d_bytes_per_step": int(h2d / args.steps),
+                           "d2h_bytes_per_step": int(d2h / args.steps),
+                           "api": "rescal_solve(RelTensor(pinned fp32 host X), k, SolverConfig(max_iters=steps))"
+                           if world == 1 else "Engine grid API: upload_block + run + get_factors",
+                           "seconds": e2e_s}
+        except Exception as exc:  # report, never hide
+            line["e2e"] = {"value": None, "unit": "it/s", "error": repr(exc)[:300],
+                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+    # ---------------- CPU baseline (rank 0, N=1 only) -----------------------
+    if world == 1 and rank == 0 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        try:
+            xs = host_tensor(min(m, 4), n, pinned=False)
+            it_s, cores, sample, t_step = cpu_reference(xs, k, m, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": it_s, "unit": "it/s", "cores": cores, "kind": "port",
+                                    "sample": sample}
+        except Exception as exc:
+            line["cpu_baseline"] = {"value": None, "unit": "it/s", "cores": threads, "kind": "port",
+                                    "sample": f"failed: {exc!r}"[:300]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier(dist)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        # CPU reference arm: rank 0 alone runs it; other ranks exit without work
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_reference(args, None, 0, world)
+        return
+    dist, rank, world, local_rank = dist_setup(args.gpus)
+    if False:
+    else:
+        run_ours(args, dist, rank, world, local_rank)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

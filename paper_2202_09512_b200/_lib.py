@@ -69,6 +69,7 @@ SIGNATURES = {
     "rk_time_k1": (ctypes.c_int, [_vp, _i32, _pd]),
     "rk_trace_len": (ctypes.c_int, [_vp, _pi32]),
     "rk_restore": (ctypes.c_int, [_vp]),
+    "rk_block_uniform": (ctypes.c_int, [_vp, _u64, _pf]),
 }
 
 _LIB = None
@@ -216,6 +217,12 @@ class Engine:
         sh, sl, ih, il = pcg64_seed_state(entropy)
         check(self._lib.rk_perturb(self._h, sh, sl, ih, il, float(delta),
                                    int(n_global or self.n), int(row0), 0, None))
+
+    def block_uniform(self, seed, rows, cols):
+        """Exact fp32 values of this engine's block of the synthetic tensor."""
+        out = np.empty((self.m, rows, cols), dtype=np.float32)
+        check(self._lib.rk_block_uniform(self._h, int(seed), out.ctypes.data_as(_pf)))
+        return out
 
     def restore(self):
         """Undo rk_perturb: the device tensor goes back to the uploaded one."""

@@ -641,7 +641,7 @@ void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
       RK_CUDA(cudaMemcpyAsync(dstage[slot], from, (size_t)nrow * row_bytes, cudaMemcpyHostToDevice,
                               h->stream));
       rk::split_chunk<T><<<h->nnp, rk::kThreads, 0, h->stream>>>(
-          dstage[slot], nrow, cols, h->Xh, h->Xl, h->NR, h->NC, (int)t, r0, h->npart);
+          dstage[slot], nrow, cols, h->Xh, h->Xl, h->NR, h->NC, (int)t, r0, h->npart, h->npart2);
       RK_CUDA(cudaGetLastError());
       RK_CUDA(cudaEventRecord(done[slot], h->stream));
       used[slot] = true;
@@ -654,18 +654,6 @@ void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
     dfree(dstage[i]);
     if (hstage[i]) cudaFreeHost(hstage[i]);
   }
-}
-
-double host_sq_norm(const void* x, int dtype, size_t count) {
-  double s = 0.0;
-  if (dtype == RK_F32) {
-    const float* p = static_cast<const float*>(x);
-    for (size_t i = 0; i < count; ++i) s += (double)p[i] * (double)p[i];
-  } else {
-    const double* p = static_cast<const double*>(x);
-    for (size_t i = 0; i < count; ++i) s += p[i] * p[i];
-  }
-  return s;
 }
 
 void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iters_done) {
@@ -822,8 +810,7 @@ int rk_upload_dense(rk_handle* h, const void* x, int32_t dtype) {
       upload_rows(h, static_cast<const float*>(x), h->n, h->n);
     else
       upload_rows(h, static_cast<const double*>(x), h->n, h->n);
-    finish_upload_norm(h, false);
-    h->norm2 = host_sq_norm(x, dtype, (size_t)h->m * h->n * h->n);
+    finish_upload_norm(h, true);
     h->have_x = true;
     h->perturbed = false;
   });
@@ -870,6 +857,22 @@ int rk_uniform_values(uint64_t seed, int64_t offset, int64_t count, float* out) 
     rk::uniform_values<<<1024, 256>>>(d, count, offset, seed);
     RK_CUDA(cudaGetLastError());
     RK_CUDA(cudaMemcpy(out, d, sizeof(float) * count, cudaMemcpyDeviceToHost));
+    dfree(d);
+  });
+}
+
+int rk_block_uniform(rk_handle* h, uint64_t seed, float* out) {
+  return guarded([&] {
+    RK_REQUIRE(h && out, RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(h->dev));
+    const size_t count = (size_t)h->m * h->rows_valid * h->cols_valid;
+    float* d = dalloc<float>(count);
+    rk::block_uniform<<<h->num_sms * 8, rk::kThreads, 0, h->stream>>>(
+        d, h->rows_valid, h->cols_valid, h->n, h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0,
+        h->d_colmap, (int)h->m, seed);
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpyAsync(out, d, count * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
     dfree(d);
   });
 }

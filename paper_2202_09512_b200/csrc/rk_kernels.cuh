@@ -632,16 +632,17 @@ __global__ void __launch_bounds__(kThreads) k5_residual(const Ctl* __restrict__ 
 // ---------------------------------------------------------------------------
 // Upload: one chunk of host rows [r0, r0+rows) of slice t with `cols` valid
 // columns (host row pitch = cols), staged on the device in the host dtype ->
-// bf16 hi/lo planes with row pitch NC. Adds the chunk's fp64 sum of (hi+lo)^2
-// to norm_part[blockIdx.x].
+// bf16 hi/lo planes with row pitch NC. Adds the chunk's fp64 sums of (hi+lo)^2
+// and of the exact host values squared (rescal.py:160-165) to the partials.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) split_chunk(const T* __restrict__ src, int64_t rows,
                                                         int64_t cols, __nv_bfloat16* __restrict__ Xh,
                                                         __nv_bfloat16* __restrict__ Xl, int64_t NR,
                                                         int64_t NC, int t, int64_t r0,
-                                                        double* __restrict__ norm_part) {
+                                                        double* __restrict__ norm_part,
+                                                        double* __restrict__ norm_part_exact) {
   __shared__ double red[32];
-  double acc = 0.0;
+  double acc = 0.0, acc2 = 0.0;
   const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * kThreads) {
@@ -654,9 +655,14 @@ __global__ void __launch_bounds__(kThreads) split_chunk(const T* __restrict__ sr
     Xl[off] = lo;
     double w = (double)join_bf16(hi, lo);
     acc += w * w;
+    acc2 += v * v;
   }
   acc = block_sum(acc, red);
-  if (threadIdx.x == 0) norm_part[blockIdx.x] += acc;
+  acc2 = block_sum(acc2, red);
+  if (threadIdx.x == 0) {
+    norm_part[blockIdx.x] += acc;
+    norm_part_exact[blockIdx.x] += acc2;
+  }
 }
 
 // Synthetic uniform input directly on the device (benchmarks): element
@@ -693,6 +699,24 @@ __global__ void __launch_bounds__(kThreads) fill_uniform(__nv_bfloat16* __restri
   if (threadIdx.x == 0) {
     norm_part[blockIdx.x] = acc;
     norm_part_exact[blockIdx.x] = acc2;
+  }
+}
+
+// Exact fp32 values of a block of the synthetic tensor (host copies for the
+// end-to-end benchmark arm): out[t][i][j] for i < rows, j < cols.
+__global__ void __launch_bounds__(kThreads) block_uniform(float* __restrict__ out, int64_t rows,
+                                                          int64_t cols, int64_t n_global,
+                                                          int64_t row0,
+                                                          const int64_t* __restrict__ colmap,
+                                                          int M, uint64_t seed) {
+  const int64_t total = (int64_t)M * rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * kThreads) {
+    int64_t t = e / (rows * cols), rem = e - t * rows * cols, i = rem / cols, j = rem - i * cols;
+    int64_t gi = row0 + i, gj = colmap ? colmap[j] : j;
+    out[e] = (gi < n_global && gj < n_global)
+                 ? uniform01_f32(seed, (uint64_t)((t * n_global + gi) * n_global + gj))
+                 : 0.f;
   }
 }
 
