@@ -410,9 +410,7 @@ def main():
         run_reference(args, None, 0, world)
         return
     dist, rank, world, local_rank = dist_setup(args.gpus)
-    if False:
-    else:
-        run_ours(args, dist, rank, world, local_rank)
+    run_ours(args, dist, rank, world, local_rank)
     if dist is not None:
         dist.destroy_process_group()
 
