@@ -143,9 +143,11 @@ struct rk_handle {
   float *A32row = nullptr, *A32col = nullptr;
   __nv_bfloat16 *ATh_row = nullptr, *ATl_row = nullptr, *ATh_col = nullptr, *ATl_col = nullptr;
   double *R = nullptr, *Rnext = nullptr, *Mt = nullptr, *Mm = nullptr, *tt = nullptr;
-  double* part = nullptr;   // K2a partials [nb][(M+1)K^2]
-  double* red = nullptr;    // reduced partials + residual scalar (grid all-reduce buffer)
-  int nb = 1;
+  double* part = nullptr;   // K2a partials [M+1][nchunks][K^2]
+  double* red = nullptr;    // reduced G, S_t (+ residual scalar): the grid all-reduce buffer
+  int nb = 1;               // K2a row chunks
+  int chunk_rows = 64;
+  unsigned* counters = nullptr;  // last-block tickets (self-resetting)
   double* gscratch = nullptr;
   double *UI = nullptr, *UJ = nullptr;  // grid numerator partials
   double *regS = nullptr, *regG = nullptr, *regT = nullptr, *regRn = nullptr;
@@ -185,7 +187,7 @@ struct rk_handle {
 namespace {
 
 size_t k2f_smem(int K) {
-  size_t s = (size_t)6 * K * K * sizeof(double);
+  size_t s = (size_t)5 * K * K * sizeof(double);
   return s <= 200 * 1024 ? s : 0;
 }
 
@@ -195,7 +197,7 @@ void free_factor_buffers(rk_handle* h) {
     h->graph = nullptr;
   }
   void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
-                  h->part, h->red, h->gscratch, h->UI, h->UJ, h->regS, h->regG, h->regT,
+                  h->part, h->red, h->gscratch, h->counters, h->UI, h->UJ, h->regS, h->regG, h->regT,
                   h->regRn, h->P, h->Q, h->rpart, h->Ppart, h->Qpart, h->d_cta_begin,
                   h->d_cta_slot, h->d_slot_first, h->d_slot_count};
   for (void* p : ptrs) dfree(p);
@@ -207,6 +209,7 @@ void free_factor_buffers(rk_handle* h) {
   h->A32row = h->A32col = nullptr;
   h->ATh_row = h->ATl_row = h->ATh_col = h->ATl_col = nullptr;
   h->R = h->Rnext = h->Mt = h->Mm = h->tt = h->part = h->red = h->gscratch = nullptr;
+  h->counters = nullptr;
   h->UI = h->UJ = h->regS = h->regG = h->regT = h->regRn = nullptr;
   h->P = h->Q = nullptr;
   h->rpart = nullptr;
@@ -314,14 +317,13 @@ void alloc_factor_buffers(rk_handle* h) {
   h->Mt = dalloc<double>(M * KK);
   h->Mm = dalloc<double>(KK);
   h->tt = dalloc<double>(2 * M);
-  // K2a partial blocks: enough parallelism, bounded partial traffic (~16 MB)
-  int64_t rows = std::max(h->NR, (int64_t)h->piece);
-  int nb = (int)std::min<int64_t>(h->num_sms, std::max<int64_t>(1, rows / 64));
-  const size_t per = (size_t)(M + 1) * KK * sizeof(double);
-  nb = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (16ll << 20) / (int64_t)per));
-  h->nb = nb;
-  h->part = dalloc<double>((size_t)nb * (M + 1) * KK);
+  // K2a row chunks: <= 128 chunks of >= 64 rows (bounded partial traffic)
+  const int64_t rows = std::max(h->NR, (int64_t)h->piece);
+  h->chunk_rows = (int)std::max<int64_t>(64, round_up((rows + 127) / 128, 64));
+  h->nb = (int)((rows + h->chunk_rows - 1) / h->chunk_rows);
+  h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
+  h->counters = dalloc<unsigned>((size_t)M + 8);
   if (!k2f_smem(K)) h->gscratch = dalloc<double>((size_t)M * 6 * KK);
   h->P = dalloc<float>((size_t)M * h->NR * K);
   h->Q = dalloc<float>((size_t)M * h->NC * K);
@@ -344,7 +346,11 @@ void alloc_factor_buffers(rk_handle* h) {
   const size_t k5s = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
   RK_CUDA(cudaFuncSetAttribute(rk::k5_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s));
   if (k2f_smem(K))
-    RK_CUDA(cudaFuncSetAttribute(rk::k2f_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
+    RK_CUDA(cudaFuncSetAttribute(rk::k2f_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
+  if (rk::k2b_fused_smem(K, (int)M) <= 200 * 1024)
+    RK_CUDA(cudaFuncSetAttribute(rk::k2b_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rk::k2b_fused_smem(K, (int)M)));
+  RK_CUDA(cudaFuncSetAttribute(rk::k2a_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * K * 8));
   const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
   const size_t k2ps = (size_t)K * (K + 1) * 8 + (256 / K) * K * 4;
@@ -422,40 +428,33 @@ void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
   const double* Aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
   const int Nown = h->grid() ? (int)h->piece : (int)h->NR;
-  rk::k2a_gram_s<<<h->nb, rk::kThreads, 2 * 32 * K * sizeof(double), h->stream>>>(
-      h->ctl, Aown, Nown, h->Arow, h->P, (int)h->NR, K, (int)h->m, h->part, skip);
+  rk::k2a_gs<<<dim3(h->nb, (unsigned)(h->m + 1)), rk::kThreads, 2 * 64 * K * sizeof(double), h->stream>>>(
+      h->ctl, Aown, Nown, h->Arow, h->P, (int)h->NR, K, (int)h->m, h->chunk_rows, h->part, h->red,
+      h->counters, skip);
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }
 
-// On a grid: reduce the K2a partials locally, append the direct-residual
-// scalar, and all-reduce over the world communicator. K2f then reads one
-// partial block (nb = 1) from `red`.
+// On a grid: append the direct-residual scalar to the reduced [G, S_t] and
+// all-reduce over the world communicator (the only fp64 all-reduce of the
+// iteration; it returns identical bytes on every rank, so R stays replicated).
 void grid_allreduce_parts(rk_handle* h, bool with_resid) {
   const int K = h->K;
   const int len = (int)((h->m + 1) * K * K);
-  rk::reduce_parts<<<64, 256, 0, h->stream>>>(h->part, h->nb, len, h->red);
   rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, with_resid ? h->nr : 0, h->red + len);
   RK_NCCL(ncclAllReduce(h->red, h->red, (size_t)len + 1, ncclDouble, ncclSum, h->world, h->stream));
-  h->launches += 2;
-}
-
-void launch_k2f(rk_handle* h, int mode, int skip) {
-  const int K = h->K;
-  const double* part = h->grid() ? h->red : h->part;
-  const int nb = h->grid() ? 1 : h->nb;
-  rk::k2f_core<<<(unsigned)h->m, rk::kThreads, k2f_smem(K), h->stream>>>(
-      h->ctl, part, nb, h->R, h->Rnext, h->Mt, h->tt, K, (int)h->m, h->eps, mode, h->gscratch, skip);
-  RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }
 
-void launch_k2m(rk_handle* h, int mode) {
+// K2f + trace/commit; mode: 0 iteration, 1 tail, 2 update_r, 3 update_a
+void launch_k2f(rk_handle* h, int mode) {
   const int K = h->K;
-  const double* rp = h->grid() ? h->red + (h->m + 1) * K * K : h->rpart;
-  const int nr = h->grid() ? 1 : h->nr;
-  rk::k2m_commit<<<1, rk::kThreads, 0, h->stream>>>(h->ctl, h->tt, h->Mt, h->Mm, h->Rnext, h->R, rp,
-                                                    nr, h->trace_dev, K, (int)h->m, mode);
+  const int len = (int)((h->m + 1) * K * K);
+  const double* rres = h->grid() ? h->red + len : h->rpart;
+  const int nres = h->grid() ? 1 : h->nr;
+  rk::k2f_fused<<<(unsigned)h->m, rk::kThreads, k2f_smem(K), h->stream>>>(
+      h->ctl, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K, (int)h->m,
+      h->eps, mode, h->gscratch, h->counters + h->m + 1);
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }
@@ -483,6 +482,15 @@ void launch_k2b(rk_handle* h) {
   const double eps_m = h->eps * (double)h->m;
   if (!h->grid()) {
     const int rpb = 256 / K;
+    if (rk::k2b_fused_smem(K, (int)h->m) <= 200 * 1024) {
+      rk::k2b_fused<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads,
+                      rk::k2b_fused_smem(K, (int)h->m), h->stream>>>(
+          h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->P, h->Q, h->R, h->Mm, (int)h->NR, K,
+          (int)h->m, eps_m);
+      RK_CUDA(cudaGetLastError());
+      h->launches += 1;
+      return;
+    }
     const size_t smem = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * rpb * K * 4;
     rk::k2b_update_a<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
         h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->P, h->Q, h->R, h->Mm, (int)h->NR, K,
@@ -518,8 +526,7 @@ void enqueue_iteration(rk_handle* h, bool timed) {
   launch_k5(h, 1);
   launch_k2a(h, 1);
   if (h->grid()) grid_allreduce_parts(h, true);
-  launch_k2f(h, 0, 1);
-  launch_k2m(h, 0);
+  launch_k2f(h, 0);
   launch_k2b(h);
 }
 
@@ -529,8 +536,7 @@ void enqueue_tail(rk_handle* h) {
   launch_k5(h, 1);
   launch_k2a(h, 1);
   if (h->grid()) grid_allreduce_parts(h, true);
-  launch_k2f(h, 1, 1);
-  launch_k2m(h, 1);
+  launch_k2f(h, 1);
 }
 
 void reset_ctl(rk_handle* h, int track, double tol, int max_iters) {
@@ -662,14 +668,8 @@ void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iter
   reset_ctl(h, 0, -1.0, 0);
   launch_k1(h, false);
   launch_k2a(h, 0);
-  const double* part = h->part;
-  int nb = h->nb;
-  if (h->grid()) {
-    grid_allreduce_parts(h, false);
-    part = h->red;
-    nb = 1;
-  }
-  rk::regress_loop<<<1, 1024, 0, h->stream>>>(part, nb, h->R, h->regS, h->regG, h->regT, h->regRn,
+  if (h->grid()) grid_allreduce_parts(h, false);
+  rk::regress_loop<<<1, 1024, 0, h->stream>>>(h->red, 1, h->R, h->regS, h->regG, h->regT, h->regRn,
                                              K, (int)h->m, eps, max_iters, tol, h->d_iters);
   RK_CUDA(cudaGetLastError());
   RK_CUDA(cudaStreamSynchronize(h->stream));
@@ -1034,8 +1034,7 @@ int rk_update_r(rk_handle* h, double eps) {
     launch_k1(h, false);
     launch_k2a(h, 0);
     if (h->grid()) grid_allreduce_parts(h, false);
-    launch_k2f(h, 0, 0);
-    launch_k2m(h, 2);
+    launch_k2f(h, 2);
     read_ctl(h);
     if (h->ctl_host->nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};
   });
@@ -1049,8 +1048,7 @@ int rk_update_a(rk_handle* h, double eps) {
     launch_k1(h, false);
     launch_k2a(h, 0);
     if (h->grid()) grid_allreduce_parts(h, false);
-    launch_k2f(h, 3, 0);
-    launch_k2m(h, 2);
+    launch_k2f(h, 3);
     launch_k2b(h);
     read_ctl(h);
     if (h->ctl_host->nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};

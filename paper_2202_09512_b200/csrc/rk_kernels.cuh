@@ -21,71 +21,6 @@ namespace rk {
 
 constexpr int kThreads = 256;
 
-// ---------------------------------------------------------------------------
-// K2a: per-block partials of G = A^T A and S_t = A^T P_t (fp64).
-// part[b][0] = G partial, part[b][1+t] = S_t partial; each K*K.
-// Reference: rescal.py:124 (gram) and :129 (A^T X_t A).
-// G is taken over `Aown` (Nown rows: the whole A on one GPU, the rank's own
-// piece on a grid); S_t over the block's row set `Arow` (NR rows) and P.
-__global__ void __launch_bounds__(kThreads) k2a_gram_s(const Ctl* __restrict__ ctl,
-                                                       const double* __restrict__ Aown, int Nown,
-                                                       const double* __restrict__ Arow,
-                                                       const float* __restrict__ P, int NR, int K,
-                                                       int M, double* __restrict__ part,
-                                                       int skip_if_stopped) {
-  if (skip_if_stopped && ctl->stop) return;
-  extern __shared__ double sh[];
-  constexpr int TR = 32;           // rows per smem tile
-  double* sa = sh;                 // [TR][K]
-  double* sb = sh + TR * K;        // [TR][K]
-  const int b = blockIdx.x;
-  const int KK = K * K;
-  constexpr int Q = 8;             // entries per thread per pass
-  for (int slot = 0; slot <= M; ++slot) {
-    double* out = part + ((size_t)b * (M + 1) + slot) * KK;
-    const int nrows = slot == 0 ? Nown : NR;
-    const int chunk = (nrows + gridDim.x - 1) / gridDim.x;
-    const int r_begin = min(nrows, b * chunk);
-    const int r_end = min(nrows, r_begin + chunk);
-    const double* A = slot == 0 ? Aown : Arow;
-    for (int e0 = 0; e0 < KK; e0 += kThreads * Q) {
-      double acc[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-      for (int r0 = r_begin; r0 < r_end; r0 += TR) {
-        const int rows = min(TR, r_end - r0);
-        for (int idx = threadIdx.x; idx < TR * K; idx += kThreads) {
-          int rr = idx / K, c = idx - rr * K;
-          double av = 0.0, bv = 0.0;
-          if (rr < rows) {
-            av = A[(size_t)(r0 + rr) * K + c];
-            bv = slot == 0 ? av : (double)P[((size_t)(slot - 1) * NR + r0 + rr) * K + c];
-          }
-          sa[idx] = av;
-          sb[idx] = bv;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          int e = e0 + q * kThreads + threadIdx.x;
-          if (e < KK) {
-            int c = e / K, d = e - c * K;
-            double s = acc[q];
-            for (int rr = 0; rr < rows; ++rr) s = fma(sa[rr * K + c], sb[rr * K + d], s);
-            acc[q] = s;
-          }
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        int e = e0 + q * kThreads + threadIdx.x;
-        if (e < KK) out[e] = acc[q];
-      }
-    }
-  }
-}
-
 // C = op(A) * op(B) for K x K fp64 matrices (row-major), all threads of the block.
 RK_DEV void mm_kk(double* __restrict__ C, const double* __restrict__ A, bool ta,
                   const double* __restrict__ B, bool tb, int K) {
@@ -120,44 +55,119 @@ RK_DEV double block_sum(double v, double* scratch) {
 }
 
 // ---------------------------------------------------------------------------
-// K2f: one block per slice t. Reduces G and S_t from the K2a partials, forms
-// the trace terms of the CURRENT (A, R_t) — <R_t, S_t> and <R_t, G R_t G> —
-// then the core update (rescal.py:130-132)
-//     R_t' = R_t * S_t / (G (R_t G) + eps)
-// and this slice's share of the A denominator matrix (rescal.py:138-143)
-//     M_t = R_t'^T G R_t' + R_t' G R_t'^T      (deno_A = A sum_t M_t + m eps).
-// `mode`: 0 = full update, 1 = trace terms only, 3 = no core update (M_t from
-// the current cores; split update_a, rescal.py:243-258).
-// scratch (global) is used when K*K*6 doubles do not fit shared memory.
-__global__ void __launch_bounds__(kThreads) k2f_core(const Ctl* __restrict__ ctl,
-                                                     const double* __restrict__ part, int nb,
-                                                     const double* __restrict__ R,
-                                                     double* __restrict__ Rnext,
-                                                     double* __restrict__ Mt,
-                                                     double* __restrict__ tt, int K, int M,
-                                                     double eps, int mode, double* gscratch,
-                                                     int skip_if_stopped) {
+// K2a (v2): grid (chunks, M+1). Block (c, slot) forms the fp64 partial of
+// slot 0: G = Aown^T Aown, slot 1+t: S_t = Arow^T P_t over rows
+// [c*CH, (c+1)*CH); the last block to finish a slot sums that slot's partials
+// in chunk order (deterministic) into gs[slot]. counters[] self-reset.
+__global__ void __launch_bounds__(kThreads) k2a_gs(const Ctl* __restrict__ ctl,
+                                                   const double* __restrict__ Aown, int Nown,
+                                                   const double* __restrict__ Arow,
+                                                   const float* __restrict__ P, int NR, int K,
+                                                   int M, int CH, double* __restrict__ part,
+                                                   double* __restrict__ gs,
+                                                   unsigned* __restrict__ counters,
+                                                   int skip_if_stopped) {
   if (skip_if_stopped && ctl->stop) return;
   extern __shared__ double sh[];
+  constexpr int TR = 64;
+  double* sa = sh;            // [TR][K]
+  double* sb = sh + TR * K;   // [TR][K]
+  __shared__ bool s_last;
+  const int chunk = blockIdx.x, slot = blockIdx.y, nchunks = gridDim.x;
+  const int nrows = slot == 0 ? Nown : NR;
+  const int r_begin = min(nrows, chunk * CH);
+  const int r_end = min(nrows, r_begin + CH);
+  const double* A = slot == 0 ? Aown : Arow;
+  const int KK = K * K;
+  double* out = part + ((size_t)slot * nchunks + chunk) * KK;
+  constexpr int Q = 8;
+  for (int e0 = 0; e0 < KK; e0 += kThreads * Q) {
+    double acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+    for (int r0 = r_begin; r0 < r_end; r0 += TR) {
+      const int rows = min(TR, r_end - r0);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < TR * K; idx += kThreads) {
+        int rr = idx / K, c = idx - rr * K;
+        double av = 0.0, bv = 0.0;
+        if (rr < rows) {
+          av = A[(size_t)(r0 + rr) * K + c];
+          bv = slot == 0 ? av : (double)P[((size_t)(slot - 1) * NR + r0 + rr) * K + c];
+        }
+        sa[idx] = av;
+        sb[idx] = bv;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int e = e0 + q * kThreads + threadIdx.x;
+        if (e < KK) {
+          int c = e / K, d = e - c * K;
+          double s0 = 0.0, s1 = 0.0;
+          int rr = 0;
+          for (; rr + 1 < rows; rr += 2) {
+            s0 = fma(sa[rr * K + c], sb[rr * K + d], s0);
+            s1 = fma(sa[(rr + 1) * K + c], sb[(rr + 1) * K + d], s1);
+          }
+          if (rr < rows) s0 = fma(sa[rr * K + c], sb[rr * K + d], s0);
+          acc[q] += s0 + s1;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int e = e0 + q * kThreads + threadIdx.x;
+      if (e < KK) out[e] = acc[q];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&counters[slot], 1u) == (unsigned)(nchunks - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double* base = part + (size_t)slot * nchunks * KK;
+  for (int e = threadIdx.x; e < KK; e += kThreads) {
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += __ldcg(base + (size_t)c * KK + e);
+    gs[(size_t)slot * KK + e] = s;
+  }
+  if (threadIdx.x == 0) counters[slot] = 0u;
+}
+
+// K2f (v2): one block per slice on the reduced G / S_t (gs), then the block
+// that finishes last runs the former K2m work: trace of the iterate K1 read,
+// tolerance stop, non-finite check, M = sum_t M_t and the commit R <- R'.
+// mode: 0 iteration, 1 tail (trace only), 2 split update_r (no trace),
+// 3 split update_a (M from the current cores, no trace, no core change).
+__global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
+                                                      const double* __restrict__ gs,
+                                                      double* __restrict__ R,
+                                                      double* __restrict__ Rnext,
+                                                      double* __restrict__ Mt,
+                                                      double* __restrict__ Mout,
+                                                      double* __restrict__ tt,
+                                                      const double* __restrict__ rres, int nres,
+                                                      double* __restrict__ trace, int K, int M,
+                                                      double eps, int mode, double* gscratch,
+                                                      unsigned* __restrict__ counter) {
+  if (ctl->stop) return;
+  extern __shared__ double sh[];
+  __shared__ double red[32];
+  __shared__ bool s_last;
+  __shared__ int s_stop;
   const int t = blockIdx.x;
   const int KK = K * K;
-  double* base = gscratch ? gscratch + (size_t)t * 6 * KK : sh;
+  double* base = gscratch ? gscratch + (size_t)t * 5 * KK : sh;
   double* G = base;
-  double* S = base + KK;
-  double* Rt = base + 2 * KK;
-  double* T1 = base + 3 * KK;
-  double* T2 = base + 4 * KK;
-  double* Rn = base + 5 * KK;
-  __shared__ double red[32];
+  double* Rt = base + KK;
+  double* T1 = base + 2 * KK;
+  double* T2 = base + 3 * KK;
+  double* Rn = base + 4 * KK;
+  const double* S = gs + (size_t)(1 + t) * KK;
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    double g = 0.0, s = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      const double* pb = part + (size_t)b * (M + 1) * KK;
-      g += pb[e];
-      s += pb[(size_t)(1 + t) * KK + e];
-    }
-    G[e] = g;
-    S[e] = s;
+    G[e] = gs[e];
     Rt[e] = R[(size_t)t * KK + e];
   }
   __syncthreads();
@@ -176,54 +186,45 @@ __global__ void __launch_bounds__(kThreads) k2f_core(const Ctl* __restrict__ ctl
     tt[2 * t] = rs;
     tt[2 * t + 1] = rgrg;
   }
-  if (mode == 1) return;
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    double v = mode == 3 ? Rt[e] : Rt[e] * S[e] / (T2[e] + eps);
-    Rn[e] = v;
-    Rnext[(size_t)t * KK + e] = v;
+  if (mode != 1) {
+    for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+      double v = mode == 3 ? Rt[e] : Rt[e] * S[e] / (T2[e] + eps);
+      Rn[e] = v;
+      Rnext[(size_t)t * KK + e] = v;
+    }
+    __syncthreads();
+    mm_kk(T1, G, false, Rn, false, K);  // G R'
+    __syncthreads();
+    mm_kk(T2, Rn, true, T1, false, K);  // R'^T G R'
+    __syncthreads();
+    mm_kk(T1, G, false, Rn, true, K);   // G R'^T
+    __syncthreads();
+    mm_kk(Rt, Rn, false, T1, false, K);  // R' G R'^T
+    __syncthreads();
+    for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + Rt[e];
+  }
+  // ---- last block: trace / stop / commit (former K2m) ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == (unsigned)(M - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    s_stop = 0;
+    *counter = 0u;
   }
   __syncthreads();
-  mm_kk(T1, G, false, Rn, false, K);  // G R'
-  __syncthreads();
-  mm_kk(T2, Rn, true, T1, false, K);  // R'^T G R'
-  __syncthreads();
-  mm_kk(T1, G, false, Rn, true, K);   // G R'^T
-  __syncthreads();
-  mm_kk(S, Rn, false, T1, false, K);  // R' G R'^T  (S no longer needed)
-  __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + S[e];
-}
-
-// ---------------------------------------------------------------------------
-// K2m: single block. Trace bookkeeping for the iterate the K1 pass just read,
-// tolerance stop (rescal.py:218-224), non-finite check of the new cores
-// (rescal.py:168-170), M = sum_t M_t, and the commit R <- R'.
-// mode: 0 = iteration, 1 = tail (trace only), 2 = commit only (split API).
-__global__ void __launch_bounds__(kThreads) k2m_commit(Ctl* __restrict__ ctl,
-                                                       const double* __restrict__ tt,
-                                                       const double* __restrict__ Mt,
-                                                       double* __restrict__ Mout,
-                                                       const double* __restrict__ Rnext,
-                                                       double* __restrict__ R,
-                                                       const double* __restrict__ rpart, int nr,
-                                                       double* __restrict__ trace, int K, int M,
-                                                       int mode) {
-  if (ctl->stop) return;
-  __shared__ double red[32];
-  __shared__ int s_stop;
-  const int KK = K * K;
-  if (threadIdx.x == 0) s_stop = 0;
-  __syncthreads();
-  const bool want_trace = (mode != 2) && ctl->track && (ctl->iter >= 1 || mode == 1);
+  const bool want_trace = (mode == 0 || mode == 1) && ctl->track && (ctl->iter >= 1 || mode == 1);
   if (want_trace) {
     double res;
     if (ctl->direct) {
       double acc = 0.0;
-      for (int i = threadIdx.x; i < nr; i += blockDim.x) acc += rpart[i];
+      for (int i = threadIdx.x; i < nres; i += blockDim.x) acc += __ldcg(rres + i);
       res = block_sum(acc, red);
     } else {
       double acc = 0.0;
-      for (int t = threadIdx.x; t < M; t += blockDim.x) acc += -2.0 * tt[2 * t] + tt[2 * t + 1];
+      for (int q = threadIdx.x; q < M; q += blockDim.x) acc += -2.0 * __ldcg(tt + 2 * q) + __ldcg(tt + 2 * q + 1);
       res = ctl->norm2_dev + block_sum(acc, red);
     }
     if (threadIdx.x == 0) {
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) k2m_commit(Ctl* __restrict__ ctl,
   }
   int bad = 0;
   for (int e = threadIdx.x; e < M * KK; e += blockDim.x) {
-    double v = Rnext[e];
+    double v = __ldcg(Rnext + e);
     if (!isfinite(v)) bad = 1;
     R[e] = v;
   }
@@ -262,10 +263,92 @@ __global__ void __launch_bounds__(kThreads) k2m_commit(Ctl* __restrict__ ctl,
   }
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
     double s = 0.0;
-    for (int t = 0; t < M; ++t) s += Mt[(size_t)t * KK + e];
+    for (int q = 0; q < M; ++q) s += __ldcg(Mt + (size_t)q * KK + e);
     Mout[e] = s;
   }
   if (threadIdx.x == 0) ctl->iter += 1;
+}
+
+// K2b (v2): A update with every core staged once in shared memory (fp32,
+// padded) and the block's P/Q rows for all slices staged once — one load
+// phase, no per-slice barriers. Rows per block = kThreads / K.
+// Used when M*K*(K+1)*4 + 2*M*rows*K*4 fits in 200 KB; else k2b_update_a.
+__global__ void __launch_bounds__(kThreads) k2b_fused(Ctl* __restrict__ ctl,
+                                                      double* __restrict__ A64,
+                                                      float* __restrict__ A32,
+                                                      __nv_bfloat16* __restrict__ ATh,
+                                                      __nv_bfloat16* __restrict__ ATl,
+                                                      const float* __restrict__ P,
+                                                      const float* __restrict__ Q,
+                                                      const double* __restrict__ R,
+                                                      const double* __restrict__ Mm, int N,
+                                                      int K, int M, double eps_m) {
+  if (ctl->stop) return;
+  extern __shared__ float shf[];
+  const int rpb = kThreads / K;
+  const int ld = K + 1;
+  float* Rs = shf;                        // [M][K][K+1]
+  float* Ps = Rs + (size_t)M * K * ld;    // [M][rpb][K]
+  float* Qs = Ps + (size_t)M * rpb * K;   // [M][rpb][K]
+  const int r = threadIdx.x / K, c = threadIdx.x - r * K;
+  const int i0 = blockIdx.x * rpb;
+  for (int e = threadIdx.x; e < M * K * K; e += kThreads) {
+    int t = e / (K * K), q = e - t * K * K, a = q / K, b = q - a * K;
+    Rs[((size_t)t * K + a) * ld + b] = (float)R[e];
+  }
+  const int K4 = K / 4;
+  for (int e = threadIdx.x; e < M * rpb * K4; e += kThreads) {
+    int t = e / (rpb * K4), q = e - t * rpb * K4, a = q / K4, b = q - a * K4;
+    int row = i0 + a;
+    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f), qv = pv;
+    if (row < N) {
+      pv = reinterpret_cast<const float4*>(P + ((size_t)t * N + row) * K)[b];
+      qv = reinterpret_cast<const float4*>(Q + ((size_t)t * N + row) * K)[b];
+    }
+    reinterpret_cast<float4*>(Ps + ((size_t)t * rpb + a) * K)[b] = pv;
+    reinterpret_cast<float4*>(Qs + ((size_t)t * rpb + a) * K)[b] = qv;
+  }
+  __syncthreads();
+  const int i = i0 + r;
+  const bool active = r < rpb && i < N;
+  double anew = 0.0;
+  if (active) {
+    double num = 0.0;
+    for (int t = 0; t < M; ++t) {
+      const float* pr = Ps + ((size_t)t * rpb + r) * K;
+      const float* qr = Qs + ((size_t)t * rpb + r) * K;
+      const float* Rt = Rs + (size_t)t * K * ld;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+      for (int d = 0; d < K; ++d) {
+        s0 = fmaf(pr[d], Rt[c * ld + d], s0);
+        s1 = fmaf(qr[d], Rt[d * ld + c], s1);
+      }
+      num += (double)s0 + (double)s1;
+    }
+    const double* Ai = A64 + (size_t)i * K;
+    double deno = eps_m;
+    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+    anew = Ai[c] * num / deno;
+    if (!isfinite(anew)) {
+      ctl->nonfinite = 1;
+      ctl->stop = 1;
+    }
+  }
+  __syncthreads();
+  if (active) {
+    A64[(size_t)i * K + c] = anew;
+    A32[(size_t)i * K + c] = (float)anew;
+    __nv_bfloat16 hi, lo;
+    split_bf16(anew, hi, lo);
+    ATh[(size_t)c * N + i] = hi;
+    ATl[(size_t)c * N + i] = lo;
+  }
+}
+
+inline size_t k2b_fused_smem(int K, int M) {
+  const int rpb = kThreads / K;
+  return ((size_t)M * K * (K + 1) + 2ull * M * rpb * K) * sizeof(float);
 }
 
 // ---------------------------------------------------------------------------
@@ -440,17 +523,6 @@ __global__ void __launch_bounds__(kThreads) emit_operands(const double* __restri
     split_bf16(v, hi, lo);
     ATh[(size_t)c * rows + i] = hi;
     ATl[(size_t)c * rows + i] = lo;
-  }
-}
-
-// Sum the K2a per-block partials into one (M+1)*K*K buffer (+ trailing
-// scalars copied through) before the world all-reduce.
-__global__ void reduce_parts(const double* __restrict__ part, int nb, int len,
-                             double* __restrict__ out) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[(size_t)b * len + e];
-    out[e] = s;
   }
 }
 
