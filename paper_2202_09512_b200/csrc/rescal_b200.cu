@@ -80,6 +80,9 @@ T* dalloc(size_t count) {
   if (count == 0) count = 1;
   RK_CUDA(cudaMalloc(&p, count * sizeof(T)));
   RK_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+  // the engine stream is non-blocking w.r.t. the legacy stream the memset
+  // ran on: finish the zeroing before any engine kernel can touch the buffer
+  RK_CUDA(cudaDeviceSynchronize());
   return static_cast<T*>(p);
 }
 
@@ -729,6 +732,7 @@ int rk_create(int device, int64_t n, int64_t m, int32_t k, int32_t engine, rk_ha
     RK_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     RK_CUDA(cudaMalloc(&h->ctl, sizeof(Ctl)));
     RK_CUDA(cudaMemset(h->ctl, 0, sizeof(Ctl)));
+    RK_CUDA(cudaDeviceSynchronize());
     RK_CUDA(cudaMallocHost(&h->ctl_host, sizeof(Ctl)));
     RK_CUDA(cudaMallocHost(&h->stop_host, 2 * sizeof(int)));
     RK_CUDA(cudaEventCreate(&h->ev_run0));
