@@ -322,7 +322,7 @@ void alloc_factor_buffers(rk_handle* h) {
   h->tt = dalloc<double>(2 * M);
   // K2a row chunks: <= 128 chunks of >= 64 rows (bounded partial traffic)
   const int64_t rows = std::max(h->NR, (int64_t)h->piece);
-  h->chunk_rows = (int)std::max<int64_t>(64, round_up((rows + 127) / 128, 64));
+  h->chunk_rows = (int)std::max<int64_t>(64, round_up((rows + 47) / 48, 64));
   h->nb = (int)((rows + h->chunk_rows - 1) / h->chunk_rows);
   h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
@@ -486,7 +486,8 @@ void launch_k2b(rk_handle* h) {
   if (!h->grid()) {
     const int rpb = 256 / K;
     if (rk::k2b_fused_smem(K, (int)h->m) <= 200 * 1024) {
-      rk::k2b_fused<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads,
+      const int rows_fused = rk::k2b_fused_rows(K);
+      rk::k2b_fused<<<(unsigned)((h->NR + rows_fused - 1) / rows_fused), rk::kThreads,
                       rk::k2b_fused_smem(K, (int)h->m), h->stream>>>(
           h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->P, h->Q, h->R, h->Mm, (int)h->NR, K,
           (int)h->m, eps_m);

@@ -129,9 +129,15 @@ __global__ void __launch_bounds__(kThreads) k2a_gs(const Ctl* __restrict__ ctl,
   __threadfence();
   const double* base = part + (size_t)slot * nchunks * KK;
   for (int e = threadIdx.x; e < KK; e += kThreads) {
-    double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += __ldcg(base + (size_t)c * KK + e);
-    gs[(size_t)slot * KK + e] = s;
+    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 8 <= nchunks; c += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s8[q] += __ldcg(base + (size_t)(c + q) * KK + e);
+    }
+    for (int q = 0; c < nchunks; ++c, ++q) s8[q] += __ldcg(base + (size_t)c * KK + e);
+    gs[(size_t)slot * KK + e] =
+        ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
   }
   if (threadIdx.x == 0) counters[slot] = 0u;
 }
@@ -269,10 +275,13 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
   if (threadIdx.x == 0) ctl->iter += 1;
 }
 
-// K2b (v2): A update with every core staged once in shared memory (fp32,
-// padded) and the block's P/Q rows for all slices staged once — one load
-// phase, no per-slice barriers. Rows per block = kThreads / K.
-// Used when M*K*(K+1)*4 + 2*M*rows*K*4 fits in 200 KB; else k2b_update_a.
+// K2b (v2): A update. Every core is staged once in shared memory as fp32
+// R and R^T (so both R[c][d] and R[d][c] are read at consecutive addresses
+// across the warp); each thread owns one column c for kRB rows (register
+// blocking: every R value read from shared memory feeds kRB rows) and reads
+// its rows of P/Q as float4 through L1 (the K threads of a row share them).
+constexpr int kRB = 4;
+
 __global__ void __launch_bounds__(kThreads) k2b_fused(Ctl* __restrict__ ctl,
                                                       double* __restrict__ A64,
                                                       float* __restrict__ A32,
@@ -285,71 +294,89 @@ __global__ void __launch_bounds__(kThreads) k2b_fused(Ctl* __restrict__ ctl,
                                                       int K, int M, double eps_m) {
   if (ctl->stop) return;
   extern __shared__ float shf[];
-  const int rpb = kThreads / K;
-  const int ld = K + 1;
-  float* Rs = shf;                        // [M][K][K+1]
-  float* Ps = Rs + (size_t)M * K * ld;    // [M][rpb][K]
-  float* Qs = Ps + (size_t)M * rpb * K;   // [M][rpb][K]
+  const int tpr = kThreads / K;       // thread rows
+  const int rpb = tpr * kRB;          // rows per block
+  float* Rs = shf;                           // [M][K][K]   R_t[d][c] at d*K + c
+  float* RTs = Rs + (size_t)M * K * K;       // [M][K][K]   R_t[c][d] at d*K + c
   const int r = threadIdx.x / K, c = threadIdx.x - r * K;
   const int i0 = blockIdx.x * rpb;
   for (int e = threadIdx.x; e < M * K * K; e += kThreads) {
     int t = e / (K * K), q = e - t * K * K, a = q / K, b = q - a * K;
-    Rs[((size_t)t * K + a) * ld + b] = (float)R[e];
-  }
-  const int K4 = K / 4;
-  for (int e = threadIdx.x; e < M * rpb * K4; e += kThreads) {
-    int t = e / (rpb * K4), q = e - t * rpb * K4, a = q / K4, b = q - a * K4;
-    int row = i0 + a;
-    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f), qv = pv;
-    if (row < N) {
-      pv = reinterpret_cast<const float4*>(P + ((size_t)t * N + row) * K)[b];
-      qv = reinterpret_cast<const float4*>(Q + ((size_t)t * N + row) * K)[b];
-    }
-    reinterpret_cast<float4*>(Ps + ((size_t)t * rpb + a) * K)[b] = pv;
-    reinterpret_cast<float4*>(Qs + ((size_t)t * rpb + a) * K)[b] = qv;
+    float v = (float)R[e];  // R_t[a][b]
+    Rs[(size_t)t * K * K + a * K + b] = v;
+    RTs[(size_t)t * K * K + b * K + a] = v;
   }
   __syncthreads();
-  const int i = i0 + r;
-  const bool active = r < rpb && i < N;
-  double anew = 0.0;
-  if (active) {
-    double num = 0.0;
+  double num[kRB];
+#pragma unroll
+  for (int u = 0; u < kRB; ++u) num[u] = 0.0;
+  if (r < tpr) {
     for (int t = 0; t < M; ++t) {
-      const float* pr = Ps + ((size_t)t * rpb + r) * K;
-      const float* qr = Qs + ((size_t)t * rpb + r) * K;
-      const float* Rt = Rs + (size_t)t * K * ld;
-      float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
-      for (int d = 0; d < K; ++d) {
-        s0 = fmaf(pr[d], Rt[c * ld + d], s0);
-        s1 = fmaf(qr[d], Rt[d * ld + c], s1);
+      const float* Rt = Rs + (size_t)t * K * K;
+      const float* RTt = RTs + (size_t)t * K * K;
+      float s[kRB];
+#pragma unroll
+      for (int u = 0; u < kRB; ++u) s[u] = 0.f;
+      for (int d = 0; d < K; d += 4) {
+        float rt[4], rr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          rt[q] = RTt[(d + q) * K + c];  // R_t[c][d+q]
+          rr[q] = Rt[(d + q) * K + c];   // R_t[d+q][c]
+        }
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          const int row = min(i0 + r + u * tpr, N - 1);  // rows >= N are discarded below
+          const float4 p4 = __ldg(reinterpret_cast<const float4*>(P + ((size_t)t * N + row) * K + d));
+          const float4 q4 = __ldg(reinterpret_cast<const float4*>(Q + ((size_t)t * N + row) * K + d));
+          s[u] = fmaf(p4.x, rt[0], s[u]);
+          s[u] = fmaf(p4.y, rt[1], s[u]);
+          s[u] = fmaf(p4.z, rt[2], s[u]);
+          s[u] = fmaf(p4.w, rt[3], s[u]);
+          s[u] = fmaf(q4.x, rr[0], s[u]);
+          s[u] = fmaf(q4.y, rr[1], s[u]);
+          s[u] = fmaf(q4.z, rr[2], s[u]);
+          s[u] = fmaf(q4.w, rr[3], s[u]);
+        }
       }
-      num += (double)s0 + (double)s1;
-    }
-    const double* Ai = A64 + (size_t)i * K;
-    double deno = eps_m;
-    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
-    anew = Ai[c] * num / deno;
-    if (!isfinite(anew)) {
-      ctl->nonfinite = 1;
-      ctl->stop = 1;
+#pragma unroll
+      for (int u = 0; u < kRB; ++u) num[u] += (double)s[u];
     }
   }
-  __syncthreads();
-  if (active) {
-    A64[(size_t)i * K + c] = anew;
-    A32[(size_t)i * K + c] = (float)anew;
-    __nv_bfloat16 hi, lo;
-    split_bf16(anew, hi, lo);
-    ATh[(size_t)c * N + i] = hi;
-    ATl[(size_t)c * N + i] = lo;
+  double anew[kRB];
+#pragma unroll
+  for (int u = 0; u < kRB; ++u) {
+    const int i = i0 + r + u * tpr;
+    anew[u] = 0.0;
+    if (r < tpr && i < N) {
+      const double* Ai = A64 + (size_t)i * K;
+      double deno = eps_m;
+      for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+      anew[u] = Ai[c] * num[u] / deno;
+      if (!isfinite(anew[u])) {
+        ctl->nonfinite = 1;
+        ctl->stop = 1;
+      }
+    }
+  }
+  __syncthreads();  // the denominators above read whole rows
+#pragma unroll
+  for (int u = 0; u < kRB; ++u) {
+    const int i = i0 + r + u * tpr;
+    if (r < tpr && i < N) {
+      A64[(size_t)i * K + c] = anew[u];
+      A32[(size_t)i * K + c] = (float)anew[u];
+      __nv_bfloat16 hi, lo;
+      split_bf16(anew[u], hi, lo);
+      ATh[(size_t)c * N + i] = hi;
+      ATl[(size_t)c * N + i] = lo;
+    }
   }
 }
 
-inline size_t k2b_fused_smem(int K, int M) {
-  const int rpb = kThreads / K;
-  return ((size_t)M * K * (K + 1) + 2ull * M * rpb * K) * sizeof(float);
-}
+inline size_t k2b_fused_smem(int K, int M) { return 2ull * M * K * K * sizeof(float); }
+
+inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
 
 // ---------------------------------------------------------------------------
 // K2b: accumulated A update (rescal.py:133-145), one thread per (row, column):
