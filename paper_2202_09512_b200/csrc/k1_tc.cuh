@@ -14,7 +14,7 @@
 // an item the P accumulator (128 rows x K) lives in TMEM (double buffered);
 // the c Q accumulators (one per column tile, 128 x K each) live in TMEM for
 // the whole run of items the CTA has in the same (t, strip) — a "segment".
-//   P partial  -> Ppart[t][strip][row][K]      (one writer per (t,strip,row))
+//   P partial  -> Ppart[strip][t][row][K]      (one writer per (t,strip,row))
 //   Q partial  -> Qpart[slot][strip col][K]    (one slot per segment)
 // k1_reduce sums the partials in a fixed order (deterministic, no atomics).
 //
@@ -40,7 +40,7 @@ struct K1Args {
   int nstrips;
   int nrb;        // NR / 128 row blocks
   int ncb;        // NC / 128 column tiles
-  float* Ppart;   // [M][nstrips][NR][K]
+  float* Ppart;   // [nstrips][M][NR][K]
   float* Qpart;   // [nslots][c*128][K]
   const int* cta_begin;  // [grid + 1] item ranges
   const int* cta_slot;   // [grid] first Q slot of the CTA
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&p_empty[pb]));
       float4* dst = reinterpret_cast<float4*>(
-          args.Ppart + ((((size_t)t * nstrips + s) * NR) + (size_t)rb * kTile + row) * K);
+          args.Ppart + ((((size_t)s * args.M + t) * NR) + (size_t)rb * kTile + row) * K);
 #pragma unroll
       for (int h = 0; h < K / 4; ++h) dst[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
       if (last_in_seg) {
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < nstrips; ++s) {
         float4 v = reinterpret_cast<const float4*>(
-            Ppart + ((((size_t)t * nstrips + s) * NR) + i) * K)[q4];
+            Ppart + ((((size_t)s * M + t) * NR) + i) * K)[q4];
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       reinterpret_cast<float4*>(P + ((size_t)t * NR + i) * K)[q4] = acc;

@@ -151,6 +151,10 @@ struct rk_handle {
   int nb = 1;               // K2a row chunks
   int chunk_rows = 64;
   unsigned* counters = nullptr;  // last-block tickets (self-resetting)
+  bool fast = false;             // single GPU, K in {16, 32}: k2a_v3 / k2b_v3 path
+  int nsub = 1;                  // k2a_v3 32-row sub-chunks per block
+  float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v3
+  int *d_simt_first = nullptr, *d_simt_count = nullptr;
   double* gscratch = nullptr;
   double *UI = nullptr, *UJ = nullptr;  // grid numerator partials
   double *regS = nullptr, *regG = nullptr, *regT = nullptr, *regRn = nullptr;
@@ -200,7 +204,8 @@ void free_factor_buffers(rk_handle* h) {
     h->graph = nullptr;
   }
   void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
-                  h->part, h->red, h->gscratch, h->counters, h->UI, h->UJ, h->regS, h->regG, h->regT,
+                  h->part, h->red, h->gscratch, h->counters, h->W32, h->d_simt_first,
+                  h->d_simt_count, h->UI, h->UJ, h->regS, h->regG, h->regT,
                   h->regRn, h->P, h->Q, h->rpart, h->Ppart, h->Qpart, h->d_cta_begin,
                   h->d_cta_slot, h->d_slot_first, h->d_slot_count};
   for (void* p : ptrs) dfree(p);
@@ -213,6 +218,8 @@ void free_factor_buffers(rk_handle* h) {
   h->ATh_row = h->ATl_row = h->ATh_col = h->ATl_col = nullptr;
   h->R = h->Rnext = h->Mt = h->Mm = h->tt = h->part = h->red = h->gscratch = nullptr;
   h->counters = nullptr;
+  h->W32 = nullptr;
+  h->d_simt_first = h->d_simt_count = nullptr;
   h->UI = h->UJ = h->regS = h->regG = h->regT = h->regRn = nullptr;
   h->P = h->Q = nullptr;
   h->rpart = nullptr;
@@ -327,6 +334,21 @@ void alloc_factor_buffers(rk_handle* h) {
   h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
   h->counters = dalloc<unsigned>((size_t)M + 8);
+  h->fast = !h->grid() && (K == 16 || K == 32);
+  if (h->fast) {
+    const int64_t sub_total = (h->NR + rk::kCH - 1) / rk::kCH;
+    h->nsub = (int)std::max<int64_t>(1, (sub_total + 127) / 128);
+    h->nb = (int)((sub_total + h->nsub - 1) / h->nsub);
+    dfree(h->part);
+    h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
+    h->W32 = dalloc<float>((size_t)M * 2 * KK);
+    std::vector<int> first(M), count(M, 1);
+    for (int64_t t = 0; t < M; ++t) first[t] = (int)t;
+    h->d_simt_first = dalloc<int>(M);
+    h->d_simt_count = dalloc<int>(M);
+    RK_CUDA(cudaMemcpy(h->d_simt_first, first.data(), sizeof(int) * M, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(h->d_simt_count, count.data(), sizeof(int) * M, cudaMemcpyHostToDevice));
+  }
   if (!k2f_smem(K)) h->gscratch = dalloc<double>((size_t)M * 6 * KK);
   h->P = dalloc<float>((size_t)M * h->NR * K);
   h->Q = dalloc<float>((size_t)M * h->NC * K);
@@ -400,10 +422,13 @@ void launch_k1(rk_handle* h, bool timed) {
           h->maps[0], h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
-    rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
-                                                      h->d_slot_count, h->P, h->Q, (int)h->NR,
-                                                      (int)h->NC, K, M, h->c, h->nstrips, 1);
-    h->launches += 2;
+    h->launches += 1;
+    if (!h->fast) {  // the fast path folds the partial reduction into k2a_v3 / k2b_v3
+      rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
+                                                        h->d_slot_count, h->P, h->Q, (int)h->NR,
+                                                        (int)h->NC, K, M, h->c, h->nstrips, 1);
+      h->launches += 1;
+    }
   } else {
     const size_t smem = (size_t)(64 * 33 + 64 * K) * sizeof(float);
     rk::k1_simt_p<<<dim3((unsigned)(h->NR / 32), M), rk::kThreads, smem, s>>>(
@@ -429,6 +454,26 @@ void launch_k5(rk_handle* h, int gate) {
 
 void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
+  if (h->fast) {
+    const bool tc = h->engine == RK_ENGINE_TC;
+    const float* src = tc ? h->Ppart : h->P;
+    const int nparts = tc ? h->nstrips : 1;
+    const size_t stride = (size_t)h->m * h->NR * K;
+    float* pout = tc ? h->P : nullptr;
+    const dim3 grid(h->nb, (unsigned)((h->m + 1 + 7) / 8));
+    const size_t smem = (size_t)rk::kCH * K * 8 + (size_t)8 * rk::kCH * K * 4;
+    if (K == 16)
+      rk::k2a_v3<16><<<grid, 256, smem, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout,
+                                                     (int)h->NR, (int)h->m, h->nsub, h->part, h->red,
+                                                     h->counters, skip);
+    else
+      rk::k2a_v3<32><<<grid, 256, smem, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout,
+                                                     (int)h->NR, (int)h->m, h->nsub, h->part, h->red,
+                                                     h->counters, skip);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 1;
+    return;
+  }
   const double* Aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
   const int Nown = h->grid() ? (int)h->piece : (int)h->NR;
   rk::k2a_gs<<<dim3(h->nb, (unsigned)(h->m + 1)), rk::kThreads, 2 * 64 * K * sizeof(double), h->stream>>>(
@@ -457,7 +502,7 @@ void launch_k2f(rk_handle* h, int mode) {
   const int nres = h->grid() ? 1 : h->nr;
   rk::k2f_fused<<<(unsigned)h->m, rk::kThreads, k2f_smem(K), h->stream>>>(
       h->ctl, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K, (int)h->m,
-      h->eps, mode, h->gscratch, h->counters + h->m + 1);
+      h->eps, mode, h->gscratch, h->counters + h->m + 1, h->fast ? h->W32 : nullptr);
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }
@@ -483,6 +528,29 @@ void grid_allgather_a(rk_handle* h) {
 void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
+  if (h->fast) {
+    const bool tc = h->engine == RK_ENGINE_TC;
+    const float* qsrc = tc ? h->Qpart : h->Q;
+    const int* sf = tc ? h->d_slot_first : h->d_simt_first;
+    const int* sc = tc ? h->d_slot_count : h->d_simt_count;
+    const int W = tc ? h->c * 128 : (int)h->NC;
+    const int nstr = tc ? h->nstrips : 1;
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(h->m, (48 * 1024) / (8 * K * K)));
+    const size_t smem = (size_t)tg * 2 * K * K * sizeof(float);
+    const int rb = 128 / (K / 4);
+    const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
+    if (K == 16)
+      rk::k2b_v3<16><<<blocks, 128, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
+                                                       h->ATl_row, h->P, qsrc, sf, sc, W, nstr, h->W32,
+                                                       h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+    else
+      rk::k2b_v3<32><<<blocks, 128, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
+                                                       h->ATl_row, h->P, qsrc, sf, sc, W, nstr, h->W32,
+                                                       h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 1;
+    return;
+  }
   if (!h->grid()) {
     const int rpb = 256 / K;
     if (rk::k2b_fused_smem(K, (int)h->m) <= 200 * 1024) {

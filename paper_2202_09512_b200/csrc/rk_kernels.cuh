@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
                                                       const double* __restrict__ rres, int nres,
                                                       double* __restrict__ trace, int K, int M,
                                                       double eps, int mode, double* gscratch,
-                                                      unsigned* __restrict__ counter) {
+                                                      unsigned* __restrict__ counter,
+                                                      float* __restrict__ W32) {
   if (ctl->stop) return;
   extern __shared__ double sh[];
   __shared__ double red[32];
@@ -258,6 +259,11 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
     double v = __ldcg(Rnext + e);
     if (!isfinite(v)) bad = 1;
     R[e] = v;
+    if (W32) {
+      const int q = e / KK, rem = e - q * KK, a = rem / K, b = rem - a * K;
+      W32[(size_t)q * 2 * KK + b * K + a] = (float)v;       // R_t^T
+      W32[(size_t)q * 2 * KK + KK + a * K + b] = (float)v;  // R_t
+    }
   }
   bad = __syncthreads_or(bad);
   if (bad) {
@@ -377,6 +383,220 @@ __global__ void __launch_bounds__(kThreads) k2b_fused(Ctl* __restrict__ ctl,
 inline size_t k2b_fused_smem(int K, int M) { return 2ull * M * K * K * sizeof(float); }
 
 inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
+
+// ---------------------------------------------------------------------------
+// Fast single-GPU variants for K in {16, 32} (the tcgen05 ranks).
+//
+// k2a_v3: grid (chunks, slot groups of 8). Block (c, g) covers rows
+// [c*nsub*kCH, (c+1)*nsub*kCH) in 32-row sub-chunks; warp w owns slot 8g+w
+// (slot 0: G = A^T A, slot 1+t: S_t = A^T P_t). P_t rows are assembled from
+// the K1 strip partials on the fly (P_t = sum_s Ppart[s][t]) and written back
+// once (by slot group 0) for K2b. Lane l owns entries [l*E, (l+1)*E) of the
+// K x K block (E = 8 or 32): one A value and E/4 float4 P loads feed E fp64
+// FMAs per row. Deterministic last-block reduction per slot as in k2a_gs.
+constexpr int kCH = 32;
+
+template <int K>
+__global__ void __launch_bounds__(256) k2a_v3(const Ctl* __restrict__ ctl,
+                                              const double* __restrict__ A,
+                                              const float* __restrict__ Pparts, int nparts,
+                                              size_t part_stride, float* __restrict__ Pout, int N,
+                                              int M, int nsub, double* __restrict__ part,
+                                              double* __restrict__ gs,
+                                              unsigned* __restrict__ counters, int skip_if_stopped) {
+  static_assert(K == 16 || K == 32, "k2a_v3: K in {16, 32}");
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ double sh[];
+  double* As = sh;                                        // [kCH][K]
+  float* Ps = reinterpret_cast<float*>(As + kCH * K);     // [8][kCH][K]
+  __shared__ bool s_last[8];
+  const int chunk = blockIdx.x, nchunks = gridDim.x;
+  const int slot0 = blockIdx.y * 8;
+  const int nslots = min(8, M + 1 - slot0);
+  constexpr int KK = K * K;
+  constexpr int K4 = K / 4;
+  constexpr int E = KK / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = slot0 + warp;
+  const int c = (lane * E) / K;
+  const int d0 = (lane * E) - c * K;
+  double acc[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) acc[q] = 0.0;
+  for (int sub = 0; sub < nsub; ++sub) {
+    const int i0 = (chunk * nsub + sub) * kCH;
+    const int rows = max(0, min(kCH, N - i0));
+    __syncthreads();
+    for (int e = threadIdx.x; e < kCH * K; e += blockDim.x) {
+      const int rr = e / K;
+      As[e] = rr < rows ? A[(size_t)(i0 + rr) * K + (e - rr * K)] : 0.0;
+    }
+    for (int e = threadIdx.x; e < nslots * kCH * K4; e += blockDim.x) {
+      const int w = e / (kCH * K4), q = e - w * (kCH * K4), rr = q / K4;
+      const int t = slot0 + w - 1;
+      if (t < 0) continue;  // slot 0 reads A
+      float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rr < rows) {
+        const size_t off = ((size_t)t * N + i0) * K + (size_t)q * 4;
+        for (int s = 0; s < nparts; ++s) {
+          const float4 v = *reinterpret_cast<const float4*>(Pparts + s * part_stride + off);
+          v4.x += v.x; v4.y += v.y; v4.z += v.z; v4.w += v.w;
+        }
+        if (Pout) *reinterpret_cast<float4*>(Pout + off) = v4;
+      }
+      *reinterpret_cast<float4*>(Ps + (size_t)w * kCH * K + (size_t)q * 4) = v4;
+    }
+    __syncthreads();
+    if (warp < nslots) {
+      for (int rr = 0; rr < rows; ++rr) {
+        const double a = As[rr * K + c];
+        if (slot == 0) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) acc[q] = fma(a, As[rr * K + d0 + q], acc[q]);
+        } else {
+          const float* pr = Ps + ((size_t)warp * kCH + rr) * K + d0;
+#pragma unroll
+          for (int q = 0; q < E; q += 4) {
+            const float4 p4 = *reinterpret_cast<const float4*>(pr + q);
+            acc[q] = fma(a, (double)p4.x, acc[q]);
+            acc[q + 1] = fma(a, (double)p4.y, acc[q + 1]);
+            acc[q + 2] = fma(a, (double)p4.z, acc[q + 2]);
+            acc[q + 3] = fma(a, (double)p4.w, acc[q + 3]);
+          }
+        }
+      }
+    }
+  }
+  if (warp < nslots) {
+    double* out = part + ((size_t)slot * nchunks + chunk) * KK + lane * E;
+#pragma unroll
+    for (int q = 0; q < E; ++q) out[q] = acc[q];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x < nslots)
+    s_last[threadIdx.x] = atomicAdd(&counters[slot0 + threadIdx.x], 1u) == (unsigned)(nchunks - 1);
+  __syncthreads();
+  for (int w = 0; w < nslots; ++w) {
+    if (!s_last[w]) continue;
+    __threadfence();
+    const double* base = part + (size_t)(slot0 + w) * nchunks * KK;
+    for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+      double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int cc = 0;
+      for (; cc + 8 <= nchunks; cc += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s8[q] += __ldcg(base + (size_t)(cc + q) * KK + e);
+      }
+      for (int q = 0; cc < nchunks; ++cc, ++q) s8[q] += __ldcg(base + (size_t)cc * KK + e);
+      gs[(size_t)(slot0 + w) * KK + e] =
+          ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+    }
+    if (threadIdx.x == 0) counters[slot0 + w] = 0u;
+  }
+}
+
+// k2b_v3: A update for K in {16, 32}. W32 = [R_t^T ; R_t] as fp32 (written by
+// the K2f commit) is staged in shared memory in groups of slices; thread =
+// (row, 4-column group) with float4 loads of its P_t / Q_t row (Q_t summed
+// over the K1 segment slots on the fly). Per 4 d's: 2 global float4 + 8 smem
+// float4 loads feed 32 FMAs.
+template <int K>
+__global__ void __launch_bounds__(128) k2b_v3(Ctl* __restrict__ ctl, double* __restrict__ A64,
+                                              float* __restrict__ A32,
+                                              __nv_bfloat16* __restrict__ ATh,
+                                              __nv_bfloat16* __restrict__ ATl,
+                                              const float* __restrict__ P,
+                                              const float* __restrict__ Qpart,
+                                              const int* __restrict__ slot_first,
+                                              const int* __restrict__ slot_count, int W,
+                                              int nstrips, const float* __restrict__ W32,
+                                              const double* __restrict__ Mm, int N, int M,
+                                              int tg, double eps_m) {
+  static_assert(K == 16 || K == 32, "k2b_v3: K in {16, 32}");
+  if (ctl->stop) return;
+  extern __shared__ float shf[];
+  constexpr int G = K / 4;           // column groups
+  constexpr int RB = 128 / G;        // rows per block
+  const int rl = threadIdx.x / G, cg = threadIdx.x - rl * G;
+  const int i = blockIdx.x * RB + rl;
+  const int iv = min(i, N - 1);
+  const int s = iv / W, jl = iv - s * W;
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int t0 = 0; t0 < M; t0 += tg) {
+    const int nt = min(tg, M - t0);
+    __syncthreads();
+    const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)t0 * 2 * K * K);
+    float4* dst = reinterpret_cast<float4*>(shf);
+    for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = src[e];
+    __syncthreads();
+    for (int tt = 0; tt < nt; ++tt) {
+      const int t = t0 + tt;
+      const float* WrT = shf + (size_t)tt * 2 * K * K;   // R_t^T: [d][c] = R_t[c][d]
+      const float* Wr = WrT + K * K;                      // R_t:   [d][c] = R_t[d][c]
+      const float4* prow = reinterpret_cast<const float4*>(P + ((size_t)t * N + iv) * K);
+      const int f = slot_first[t * nstrips + s], ns = slot_count[t * nstrips + s];
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+      for (int d4 = 0; d4 < K / 4; ++d4) {
+        const float4 p4 = __ldg(prow + d4);
+        float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < ns; ++q) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K) + d4);
+          q4.x += v.x; q4.y += v.y; q4.z += v.z; q4.w += v.w;
+        }
+        const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+        const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int d = d4 * 4 + q;
+          const float4 wr = *reinterpret_cast<const float4*>(WrT + d * K + cg * 4);
+          const float4 wq = *reinterpret_cast<const float4*>(Wr + d * K + cg * 4);
+          a0 = fmaf(pv[q], wr.x, fmaf(qv[q], wq.x, a0));
+          a1 = fmaf(pv[q], wr.y, fmaf(qv[q], wq.y, a1));
+          a2 = fmaf(pv[q], wr.z, fmaf(qv[q], wq.z, a2));
+          a3 = fmaf(pv[q], wr.w, fmaf(qv[q], wq.w, a3));
+        }
+      }
+      num[0] += (double)a0;
+      num[1] += (double)a1;
+      num[2] += (double)a2;
+      num[3] += (double)a3;
+    }
+  }
+  double anew[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool active = i < N;
+  if (active) {
+    const double* Ai = A64 + (size_t)i * K;
+    double deno[4] = {eps_m, eps_m, eps_m, eps_m};
+    for (int d = 0; d < K; ++d) {
+      const double a = Ai[d];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) deno[q] = fma(a, Mm[d * K + cg * 4 + q], deno[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      anew[q] = Ai[cg * 4 + q] * num[q] / deno[q];
+      if (!isfinite(anew[q])) {
+        ctl->nonfinite = 1;
+        ctl->stop = 1;
+      }
+    }
+  }
+  __syncthreads();  // the denominators above read whole rows
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = cg * 4 + q;
+      A64[(size_t)i * K + c] = anew[q];
+      A32[(size_t)i * K + c] = (float)anew[q];
+      __nv_bfloat16 hi, lo;
+      split_bf16(anew[q], hi, lo);
+      ATh[(size_t)c * N + i] = hi;
+      ATl[(size_t)c * N + i] = lo;
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // K2b: accumulated A update (rescal.py:133-145), one thread per (row, column):
