@@ -151,9 +151,8 @@ struct rk_handle {
   int nb = 1;               // K2a row chunks
   int chunk_rows = 64;
   unsigned* counters = nullptr;  // last-block tickets (self-resetting)
-  bool fast = false;             // single GPU, K in {16, 32}: k2a_v3 / k2b_v3 path
-  int nsub = 1;                  // k2a_v3 32-row sub-chunks per block
-  float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v3
+  bool fast = false;             // single GPU, K in {16, 32}: k2a_v4 / k2b_v4 path
+  float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v4
   int *d_simt_first = nullptr, *d_simt_count = nullptr;
   double* gscratch = nullptr;
   double *UI = nullptr, *UJ = nullptr;  // grid numerator partials
@@ -336,11 +335,6 @@ void alloc_factor_buffers(rk_handle* h) {
   h->counters = dalloc<unsigned>((size_t)M + 8);
   h->fast = !h->grid() && (K == 16 || K == 32);
   if (h->fast) {
-    const int64_t sub_total = (h->NR + rk::kCH - 1) / rk::kCH;
-    h->nsub = (int)std::max<int64_t>(1, (sub_total + 127) / 128);
-    h->nb = (int)((sub_total + h->nsub - 1) / h->nsub);
-    dfree(h->part);
-    h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
     h->W32 = dalloc<float>((size_t)M * 2 * KK);
     std::vector<int> first(M), count(M, 1);
     for (int64_t t = 0; t < M; ++t) first[t] = (int)t;
@@ -423,7 +417,7 @@ void launch_k1(rk_handle* h, bool timed) {
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
-    if (!h->fast) {  // the fast path folds the partial reduction into k2a_v3 / k2b_v3
+    if (!h->fast) {  // the fast path folds the partial reduction into k2a_v4
       rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
                                                         h->d_slot_count, h->P, h->Q, (int)h->NR,
                                                         (int)h->NC, K, M, h->c, h->nstrips, 1);
@@ -460,16 +454,16 @@ void launch_k2a(rk_handle* h, int skip) {
     const int nparts = tc ? h->nstrips : 1;
     const size_t stride = (size_t)h->m * h->NR * K;
     float* pout = tc ? h->P : nullptr;
-    const dim3 grid(h->nb, (unsigned)((h->m + 1 + 7) / 8));
-    const size_t smem = (size_t)rk::kCH * K * 8 + (size_t)8 * rk::kCH * K * 4;
+    float* qout = tc ? h->Q : nullptr;
+    const dim3 grid(rk::kCluster, (unsigned)(h->m + 1));
     if (K == 16)
-      rk::k2a_v3<16><<<grid, 256, smem, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout,
-                                                     (int)h->NR, (int)h->m, h->nsub, h->part, h->red,
-                                                     h->counters, skip);
+      rk::k2a_v4<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
+                                                  h->d_slot_first, h->d_slot_count, h->c * 128,
+                                                  h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
     else
-      rk::k2a_v3<32><<<grid, 256, smem, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout,
-                                                     (int)h->NR, (int)h->m, h->nsub, h->part, h->red,
-                                                     h->counters, skip);
+      rk::k2a_v4<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
+                                                  h->d_slot_first, h->d_slot_count, h->c * 128,
+                                                  h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
     RK_CUDA(cudaGetLastError());
     h->launches += 1;
     return;
@@ -529,24 +523,18 @@ void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
   if (h->fast) {
-    const bool tc = h->engine == RK_ENGINE_TC;
-    const float* qsrc = tc ? h->Qpart : h->Q;
-    const int* sf = tc ? h->d_slot_first : h->d_simt_first;
-    const int* sc = tc ? h->d_slot_count : h->d_simt_count;
-    const int W = tc ? h->c * 128 : (int)h->NC;
-    const int nstr = tc ? h->nstrips : 1;
-    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(h->m, (48 * 1024) / (8 * K * K)));
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(h->m, (32 * 1024) / (8 * K * K)));
     const size_t smem = (size_t)tg * 2 * K * K * sizeof(float);
-    const int rb = 128 / (K / 4);
+    const int rb = 2 * (256 / K);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
     if (K == 16)
-      rk::k2b_v3<16><<<blocks, 128, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
-                                                       h->ATl_row, h->P, qsrc, sf, sc, W, nstr, h->W32,
-                                                       h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+      rk::k2b_v4<16><<<blocks, 256, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
+                                                       h->ATl_row, h->P, h->Q, h->W32, h->Mm,
+                                                       (int)h->NR, (int)h->m, tg, eps_m);
     else
-      rk::k2b_v3<32><<<blocks, 128, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
-                                                       h->ATl_row, h->P, qsrc, sf, sc, W, nstr, h->W32,
-                                                       h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+      rk::k2b_v4<32><<<blocks, 256, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,
+                                                       h->ATl_row, h->P, h->Q, h->W32, h->Mm,
+                                                       (int)h->NR, (int)h->m, tg, eps_m);
     RK_CUDA(cudaGetLastError());
     h->launches += 1;
     return;

@@ -15,6 +15,8 @@
 //   Q            f32  [M][NC][K]   Q_t = X_t^T A_row
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "rk_common.cuh"
 
 namespace rk {
@@ -387,214 +389,215 @@ inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
 // ---------------------------------------------------------------------------
 // Fast single-GPU variants for K in {16, 32} (the tcgen05 ranks).
 //
-// k2a_v3: grid (chunks, slot groups of 8). Block (c, g) covers rows
-// [c*nsub*kCH, (c+1)*nsub*kCH) in 32-row sub-chunks; warp w owns slot 8g+w
-// (slot 0: G = A^T A, slot 1+t: S_t = A^T P_t). P_t rows are assembled from
-// the K1 strip partials on the fly (P_t = sum_s Ppart[s][t]) and written back
-// once (by slot group 0) for K2b. Lane l owns entries [l*E, (l+1)*E) of the
-// K x K block (E = 8 or 32): one A value and E/4 float4 P loads feed E fp64
-// FMAs per row. Deterministic last-block reduction per slot as in k2a_gs.
-constexpr int kCH = 32;
+// k2a_v4: one 8-CTA thread-block cluster per slot (slot 0: G = A^T A,
+// slot 1+t: S_t = A^T P_t). CTA r of the cluster covers rows
+// [r*RB, (r+1)*RB); its 8 warps split those rows. A warp stages 8 rows at a
+// time in shared memory — P_t rows assembled from the K1 strip partials
+// (P_t = sum_s Ppart[s][t]), Q_t rows from the K1 segment slots — writing the
+// reduced P/Q back once for K2b; lane l then owns E = K*K/32 entries of the
+// K x K outer-product sum (fp64). Warp partials are summed in the CTA, and
+// CTA 0 sums the 8 CTA partials through distributed shared memory. Fixed
+// orders throughout: deterministic, no atomics, no global partials.
+constexpr int kCluster = 8;
 
 template <int K>
-__global__ void __launch_bounds__(256) k2a_v3(const Ctl* __restrict__ ctl,
-                                              const double* __restrict__ A,
-                                              const float* __restrict__ Pparts, int nparts,
-                                              size_t part_stride, float* __restrict__ Pout, int N,
-                                              int M, int nsub, double* __restrict__ part,
-                                              double* __restrict__ gs,
-                                              unsigned* __restrict__ counters, int skip_if_stopped) {
-  static_assert(K == 16 || K == 32, "k2a_v3: K in {16, 32}");
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
+    k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
+           const float* __restrict__ Pparts, int nparts, size_t part_stride,
+           float* __restrict__ Pout, const float* __restrict__ Qpart,
+           const int* __restrict__ slot_first, const int* __restrict__ slot_count, int W,
+           int nstrips, float* __restrict__ Qout, int N, int M, double* __restrict__ gs,
+           int skip_if_stopped) {
+  static_assert(K == 16 || K == 32, "k2a_v4: K in {16, 32}");
   if (skip_if_stopped && ctl->stop) return;
-  extern __shared__ double sh[];
-  double* As = sh;                                        // [kCH][K]
-  float* Ps = reinterpret_cast<float*>(As + kCH * K);     // [8][kCH][K]
-  __shared__ bool s_last[8];
-  const int chunk = blockIdx.x, nchunks = gridDim.x;
-  const int slot0 = blockIdx.y * 8;
-  const int nslots = min(8, M + 1 - slot0);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
   constexpr int KK = K * K;
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
+  __shared__ __align__(16) float stage[8][8][K];
+  __shared__ double bpart[KK];
+  const int rank = blockIdx.x;  // cluster rank (cluster spans gridDim.x)
+  const int slot = blockIdx.y;
+  const int t = slot - 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = slot0 + warp;
+  const int RB = (((N + kCluster - 1) / kCluster) + 63) / 64 * 64;
+  const int WR = RB / 8;  // rows per warp (multiple of 8)
+  const int r_begin = rank * RB + warp * WR;
+  const int r_end = min(N, r_begin + WR);
   const int c = (lane * E) / K;
   const int d0 = (lane * E) - c * K;
   double acc[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
-  for (int sub = 0; sub < nsub; ++sub) {
-    const int i0 = (chunk * nsub + sub) * kCH;
-    const int rows = max(0, min(kCH, N - i0));
-    __syncthreads();
-    for (int e = threadIdx.x; e < kCH * K; e += blockDim.x) {
-      const int rr = e / K;
-      As[e] = rr < rows ? A[(size_t)(i0 + rr) * K + (e - rr * K)] : 0.0;
-    }
-    for (int e = threadIdx.x; e < nslots * kCH * K4; e += blockDim.x) {
-      const int w = e / (kCH * K4), q = e - w * (kCH * K4), rr = q / K4;
-      const int t = slot0 + w - 1;
-      if (t < 0) continue;  // slot 0 reads A
-      float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rr < rows) {
-        const size_t off = ((size_t)t * N + i0) * K + (size_t)q * 4;
-        for (int s = 0; s < nparts; ++s) {
-          const float4 v = *reinterpret_cast<const float4*>(Pparts + s * part_stride + off);
-          v4.x += v.x; v4.y += v.y; v4.z += v.z; v4.w += v.w;
-        }
-        if (Pout) *reinterpret_cast<float4*>(Pout + off) = v4;
-      }
-      *reinterpret_cast<float4*>(Ps + (size_t)w * kCH * K + (size_t)q * 4) = v4;
-    }
-    __syncthreads();
-    if (warp < nslots) {
-      for (int rr = 0; rr < rows; ++rr) {
-        const double a = As[rr * K + c];
-        if (slot == 0) {
-#pragma unroll
-          for (int q = 0; q < E; ++q) acc[q] = fma(a, As[rr * K + d0 + q], acc[q]);
-        } else {
-          const float* pr = Ps + ((size_t)warp * kCH + rr) * K + d0;
-#pragma unroll
-          for (int q = 0; q < E; q += 4) {
-            const float4 p4 = *reinterpret_cast<const float4*>(pr + q);
-            acc[q] = fma(a, (double)p4.x, acc[q]);
-            acc[q + 1] = fma(a, (double)p4.y, acc[q + 1]);
-            acc[q + 2] = fma(a, (double)p4.z, acc[q + 2]);
-            acc[q + 3] = fma(a, (double)p4.w, acc[q + 3]);
+  for (int b0 = r_begin; b0 < r_end; b0 += 8) {
+    const int nrow = min(8, r_end - b0);
+    if (slot > 0) {
+      for (int item = lane; item < 8 * K4; item += 32) {
+        const int r8 = item / K4, q = item - r8 * K4;
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r8 < nrow) {
+          const int i = b0 + r8;
+          const size_t off = ((size_t)t * N + i) * K + (size_t)q * 4;
+          for (int s = 0; s < nparts; ++s) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(Pparts + s * part_stride + off));
+            v4.x += v.x; v4.y += v.y; v4.z += v.z; v4.w += v.w;
+          }
+          if (Pout) *reinterpret_cast<float4*>(Pout + off) = v4;
+          if (Qout) {
+            const int sq = i / W, jl = i - sq * W;
+            const int f = slot_first[t * nstrips + sq], ns = slot_count[t * nstrips + sq];
+            float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < ns; ++u) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(Qpart + ((size_t)(f + u) * W + jl) * K) + q);
+              w4.x += v.x; w4.y += v.y; w4.z += v.z; w4.w += v.w;
+            }
+            *reinterpret_cast<float4*>(Qout + off) = w4;
           }
         }
+        *reinterpret_cast<float4*>(&stage[warp][r8][q * 4]) = v4;
+      }
+      __syncwarp();
+      for (int r8 = 0; r8 < nrow; ++r8) {
+        const double a = A[(size_t)(b0 + r8) * K + c];
+#pragma unroll
+        for (int q = 0; q < E; q += 4) {
+          const float4 p4 = *reinterpret_cast<const float4*>(&stage[warp][r8][d0 + q]);
+          acc[q] = fma(a, (double)p4.x, acc[q]);
+          acc[q + 1] = fma(a, (double)p4.y, acc[q + 1]);
+          acc[q + 2] = fma(a, (double)p4.z, acc[q + 2]);
+          acc[q + 3] = fma(a, (double)p4.w, acc[q + 3]);
+        }
+      }
+      __syncwarp();
+    } else {
+      for (int r8 = 0; r8 < nrow; ++r8) {
+        const double* Ai = A + (size_t)(b0 + r8) * K;
+        const double a = Ai[c];
+#pragma unroll
+        for (int q = 0; q < E; q += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(Ai + d0 + q);
+          acc[q] = fma(a, v.x, acc[q]);
+          acc[q + 1] = fma(a, v.y, acc[q + 1]);
+        }
       }
     }
   }
-  if (warp < nslots) {
-    double* out = part + ((size_t)slot * nchunks + chunk) * KK + lane * E;
+  // CTA partial: warps add in warp order (fixed, deterministic)
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
 #pragma unroll
-    for (int q = 0; q < E; ++q) out[q] = acc[q];
+      for (int q = 0; q < E; ++q) {
+        double* p = &bpart[lane * E + q];
+        *p = (w == 0 ? 0.0 : *p) + acc[q];
+      }
+    }
+    __syncthreads();
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x < nslots)
-    s_last[threadIdx.x] = atomicAdd(&counters[slot0 + threadIdx.x], 1u) == (unsigned)(nchunks - 1);
-  __syncthreads();
-  for (int w = 0; w < nslots; ++w) {
-    if (!s_last[w]) continue;
-    __threadfence();
-    const double* base = part + (size_t)(slot0 + w) * nchunks * KK;
+  cluster.sync();
+  if (rank == 0) {
     for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-      double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      int cc = 0;
-      for (; cc + 8 <= nchunks; cc += 8) {
+      double v = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s8[q] += __ldcg(base + (size_t)(cc + q) * KK + e);
-      }
-      for (int q = 0; cc < nchunks; ++cc, ++q) s8[q] += __ldcg(base + (size_t)cc * KK + e);
-      gs[(size_t)(slot0 + w) * KK + e] =
-          ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+      for (int r = 0; r < kCluster; ++r) v += cluster.map_shared_rank(bpart, r)[e];
+      gs[(size_t)slot * KK + e] = v;
     }
-    if (threadIdx.x == 0) counters[slot0 + w] = 0u;
   }
+  cluster.sync();
 }
 
-// k2b_v3: A update for K in {16, 32}. W32 = [R_t^T ; R_t] as fp32 (written by
-// the K2f commit) is staged in shared memory in groups of slices; thread =
-// (row, 4-column group) with float4 loads of its P_t / Q_t row (Q_t summed
-// over the K1 segment slots on the fly). Per 4 d's: 2 global float4 + 8 smem
-// float4 loads feed 32 FMAs.
+// k2b_v4: A update for K in {16, 32}; P, Q plain (reduced by k2a_v4).
+// Thread = (2 rows, column c); the cores of a group of slices are staged as
+// fp32 W32 = [R_t^T ; R_t] (written by the K2f commit), so each shared load
+// feeds 2 rows. P/Q rows are read as float4 through L1 (shared by the K
+// threads of a row).
 template <int K>
-__global__ void __launch_bounds__(128) k2b_v3(Ctl* __restrict__ ctl, double* __restrict__ A64,
+__global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __restrict__ A64,
                                               float* __restrict__ A32,
                                               __nv_bfloat16* __restrict__ ATh,
                                               __nv_bfloat16* __restrict__ ATl,
                                               const float* __restrict__ P,
-                                              const float* __restrict__ Qpart,
-                                              const int* __restrict__ slot_first,
-                                              const int* __restrict__ slot_count, int W,
-                                              int nstrips, const float* __restrict__ W32,
-                                              const double* __restrict__ Mm, int N, int M,
-                                              int tg, double eps_m) {
-  static_assert(K == 16 || K == 32, "k2b_v3: K in {16, 32}");
+                                              const float* __restrict__ Q,
+                                              const float* __restrict__ W32,
+                                              const double* __restrict__ Mm, int N, int M, int tg,
+                                              double eps_m) {
+  static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
   if (ctl->stop) return;
   extern __shared__ float shf[];
-  constexpr int G = K / 4;           // column groups
-  constexpr int RB = 128 / G;        // rows per block
-  const int rl = threadIdx.x / G, cg = threadIdx.x - rl * G;
-  const int i = blockIdx.x * RB + rl;
-  const int iv = min(i, N - 1);
-  const int s = iv / W, jl = iv - s * W;
-  double num[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int t0 = 0; t0 < M; t0 += tg) {
-    const int nt = min(tg, M - t0);
+  constexpr int TR = 256 / K;      // thread rows
+  constexpr int RB = 2 * TR;       // rows per block
+  const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
+  const int i0 = blockIdx.x * RB + rl, i1 = i0 + TR;
+  const int j0 = min(i0, N - 1), j1 = min(i1, N - 1);
+  double n0 = 0.0, n1 = 0.0;
+  for (int tb = 0; tb < M; tb += tg) {
+    const int nt = min(tg, M - tb);
     __syncthreads();
-    const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)t0 * 2 * K * K);
+    const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)tb * 2 * K * K);
     float4* dst = reinterpret_cast<float4*>(shf);
-    for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = src[e];
+    for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = __ldg(src + e);
     __syncthreads();
-    for (int tt = 0; tt < nt; ++tt) {
-      const int t = t0 + tt;
-      const float* WrT = shf + (size_t)tt * 2 * K * K;   // R_t^T: [d][c] = R_t[c][d]
-      const float* Wr = WrT + K * K;                      // R_t:   [d][c] = R_t[d][c]
-      const float4* prow = reinterpret_cast<const float4*>(P + ((size_t)t * N + iv) * K);
-      const int f = slot_first[t * nstrips + s], ns = slot_count[t * nstrips + s];
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (int u = 0; u < nt; ++u) {
+      const int t = tb + u;
+      const float* WrT = shf + (size_t)u * 2 * K * K;  // [d][c] = R_t[c][d]
+      const float* Wr = WrT + K * K;                   // [d][c] = R_t[d][c]
+      const float4* p0 = reinterpret_cast<const float4*>(P + ((size_t)t * N + j0) * K);
+      const float4* p1 = reinterpret_cast<const float4*>(P + ((size_t)t * N + j1) * K);
+      const float4* q0 = reinterpret_cast<const float4*>(Q + ((size_t)t * N + j0) * K);
+      const float4* q1 = reinterpret_cast<const float4*>(Q + ((size_t)t * N + j1) * K);
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int d4 = 0; d4 < K / 4; ++d4) {
-        const float4 p4 = __ldg(prow + d4);
-        float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int q = 0; q < ns; ++q) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K) + d4);
-          q4.x += v.x; q4.y += v.y; q4.z += v.z; q4.w += v.w;
-        }
-        const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-        const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+        const float4 a0 = __ldg(p0 + d4), a1 = __ldg(p1 + d4);
+        const float4 b0 = __ldg(q0 + d4), b1 = __ldg(q1 + d4);
+        const float pa[4] = {a0.x, a0.y, a0.z, a0.w}, pb[4] = {a1.x, a1.y, a1.z, a1.w};
+        const float qa[4] = {b0.x, b0.y, b0.z, b0.w}, qb[4] = {b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int d = d4 * 4 + q;
-          const float4 wr = *reinterpret_cast<const float4*>(WrT + d * K + cg * 4);
-          const float4 wq = *reinterpret_cast<const float4*>(Wr + d * K + cg * 4);
-          a0 = fmaf(pv[q], wr.x, fmaf(qv[q], wq.x, a0));
-          a1 = fmaf(pv[q], wr.y, fmaf(qv[q], wq.y, a1));
-          a2 = fmaf(pv[q], wr.z, fmaf(qv[q], wq.z, a2));
-          a3 = fmaf(pv[q], wr.w, fmaf(qv[q], wq.w, a3));
+          const float wr = WrT[d * K + c], wq = Wr[d * K + c];
+          s0 = fmaf(pa[q], wr, fmaf(qa[q], wq, s0));
+          s1 = fmaf(pb[q], wr, fmaf(qb[q], wq, s1));
         }
       }
-      num[0] += (double)a0;
-      num[1] += (double)a1;
-      num[2] += (double)a2;
-      num[3] += (double)a3;
+      n0 += (double)s0;
+      n1 += (double)s1;
     }
   }
-  double anew[4] = {0.0, 0.0, 0.0, 0.0};
-  const bool active = i < N;
-  if (active) {
-    const double* Ai = A64 + (size_t)i * K;
-    double deno[4] = {eps_m, eps_m, eps_m, eps_m};
-    for (int d = 0; d < K; ++d) {
-      const double a = Ai[d];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) deno[q] = fma(a, Mm[d * K + cg * 4 + q], deno[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      anew[q] = Ai[cg * 4 + q] * num[q] / deno[q];
-      if (!isfinite(anew[q])) {
-        ctl->nonfinite = 1;
-        ctl->stop = 1;
-      }
-    }
+  double an0 = 0.0, an1 = 0.0;
+  const bool v0 = i0 < N, v1 = i1 < N;
+  if (v0) {
+    const double* Ai = A64 + (size_t)i0 * K;
+    double deno = eps_m;
+    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+    an0 = Ai[c] * n0 / deno;
+  }
+  if (v1) {
+    const double* Ai = A64 + (size_t)i1 * K;
+    double deno = eps_m;
+    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+    an1 = Ai[c] * n1 / deno;
+  }
+  if ((v0 && !isfinite(an0)) || (v1 && !isfinite(an1))) {
+    ctl->nonfinite = 1;
+    ctl->stop = 1;
   }
   __syncthreads();  // the denominators above read whole rows
-  if (active) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = cg * 4 + q;
-      A64[(size_t)i * K + c] = anew[q];
-      A32[(size_t)i * K + c] = (float)anew[q];
-      __nv_bfloat16 hi, lo;
-      split_bf16(anew[q], hi, lo);
-      ATh[(size_t)c * N + i] = hi;
-      ATl[(size_t)c * N + i] = lo;
-    }
+  if (v0) {
+    A64[(size_t)i0 * K + c] = an0;
+    A32[(size_t)i0 * K + c] = (float)an0;
+    __nv_bfloat16 hi, lo;
+    split_bf16(an0, hi, lo);
+    ATh[(size_t)c * N + i0] = hi;
+    ATl[(size_t)c * N + i0] = lo;
+  }
+  if (v1) {
+    A64[(size_t)i1 * K + c] = an1;
+    A32[(size_t)i1 * K + c] = (float)an1;
+    __nv_bfloat16 hi, lo;
+    split_bf16(an1, hi, lo);
+    ATh[(size_t)c * N + i1] = hi;
+    ATl[(size_t)c * N + i1] = lo;
   }
 }
 
