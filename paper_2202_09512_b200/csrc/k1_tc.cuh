@@ -46,6 +46,7 @@ struct K1Args {
   const int* cta_slot;   // [grid] first Q slot of the CTA
   const Ctl* ctl;
   int skip_if_stopped;
+  int debug;  // experiments only: 1 = no MMA (stream X), 2 = no Q-drain wait
 };
 
 // ------------------------------- PTX helpers -------------------------------
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ts = item / nrb;
         const bool first_in_seg = item == item_b || (item - 1) / nrb != ts;
         const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
-        if (first_in_seg && seg > 0) {
+        if (first_in_seg && seg > 0 && !(args.debug & 2)) {
           mbar_wait(smem_u32(q_empty), qe_phase);  // previous segment's Q drained
           qe_phase ^= 1;
           tc_fence_after();
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ajh = st + kStageX, ajl = st + kStageX + 2 * kABox;
           const uint32_t q_tmem = tmem + (uint32_t)(cb * K);
 #pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
+          for (int ks = 0; ks < ((args.debug & 1) ? 0 : 8); ++ks) {
             // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
             const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
             const uint32_t aoff = (ks >> 2) * kABox + (ks & 3) * 32;

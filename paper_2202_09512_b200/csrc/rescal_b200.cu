@@ -151,6 +151,7 @@ struct rk_handle {
   int nb = 1;               // K2a row chunks
   int chunk_rows = 64;
   unsigned* counters = nullptr;  // last-block tickets (self-resetting)
+  int k1_debug = 0;              // K1 experiment switches (bench/profiling only)
   bool fast = false;             // single GPU, K in {16, 32}: k2a_v4 / k2b_v4 path
   float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v4
   int *d_simt_first = nullptr, *d_simt_count = nullptr;
@@ -408,6 +409,7 @@ void launch_k1(rk_handle* h, bool timed) {
     a.cta_slot = h->d_cta_slot;
     a.ctl = h->ctl;
     a.skip_if_stopped = 1;
+    a.debug = h->k1_debug;
     if (K == 16)
       rk::tc::k1_tc_kernel<16><<<h->grid_tc, rk::tc::kThreads, h->smem_tc, s>>>(
           h->maps[0], h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
@@ -417,7 +419,7 @@ void launch_k1(rk_handle* h, bool timed) {
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
-    if (!h->fast) {  // the fast path folds the partial reduction into k2a_v4
+    {
       rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
                                                         h->d_slot_count, h->P, h->Q, (int)h->NR,
                                                         (int)h->NC, K, M, h->c, h->nstrips, 1);
@@ -450,11 +452,12 @@ void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
   if (h->fast) {
     const bool tc = h->engine == RK_ENGINE_TC;
-    const float* src = tc ? h->Ppart : h->P;
-    const int nparts = tc ? h->nstrips : 1;
-    const size_t stride = (size_t)h->m * h->NR * K;
-    float* pout = tc ? h->P : nullptr;
-    float* qout = tc ? h->Q : nullptr;
+    (void)tc;
+    const float* src = h->P;  // P/Q already reduced (k1_reduce / SIMT K1)
+    const int nparts = 1;
+    const size_t stride = 0;
+    float* pout = nullptr;
+    float* qout = nullptr;
     const dim3 grid(rk::kCluster, (unsigned)(h->m + 1));
     if (K == 16)
       rk::k2a_v4<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
@@ -848,6 +851,7 @@ int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     if (key == 1) h->profile = value != 0;
+    else if (key == 3) h->k1_debug = (int)value;
     else if (key == 2) {
       h->use_graph = value != 0;
       if (!h->use_graph && h->graph) {
