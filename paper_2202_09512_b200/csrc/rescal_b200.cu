@@ -371,6 +371,15 @@ void alloc_factor_buffers(rk_handle* h) {
     RK_CUDA(cudaFuncSetAttribute(rk::k2b_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)rk::k2b_fused_smem(K, (int)M)));
   RK_CUDA(cudaFuncSetAttribute(rk::k2a_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * K * 8));
+  if (K == 16 || K == 32) {
+    const int rb = 2 * (256 / K);
+    const int tg = rk::k2b_v4_tg(K, (int)M);
+    const int smem = tg * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
+    if (K == 16)
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    else
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
   const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
   const size_t k2ps = (size_t)K * (K + 1) * 8 + (256 / K) * K * 4;
@@ -460,7 +469,7 @@ void launch_k2a(rk_handle* h, int skip) {
     float* qout = nullptr;
     const dim3 grid(rk::kCluster, (unsigned)(h->m + 1));
     if (K == 16)
-      rk::k2a_v4<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
+      rk::k2a_v4<16><<<grid, 512, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
                                                   h->d_slot_first, h->d_slot_count, h->c * 128,
                                                   h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
     else
@@ -526,9 +535,9 @@ void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
   if (h->fast) {
-    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>(h->m, (32 * 1024) / (8 * K * K)));
-    const size_t smem = (size_t)tg * 2 * K * K * sizeof(float);
     const int rb = 2 * (256 / K);
+    const int tg = rk::k2b_v4_tg(K, (int)h->m);
+    const size_t smem = (size_t)tg * (2 * K * K + 2 * rb * K) * sizeof(float);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
     if (K == 16)
       rk::k2b_v4<16><<<blocks, 256, smem, h->stream>>>(h->ctl, h->Arow, h->A32row, h->ATh_row,

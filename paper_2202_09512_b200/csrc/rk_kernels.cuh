@@ -401,7 +401,7 @@ inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
 constexpr int kCluster = 8;
 
 template <int K>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512 : 256)
     k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
            const float* __restrict__ Pparts, int nparts, size_t part_stride,
            float* __restrict__ Pout, const float* __restrict__ Qpart,
@@ -415,14 +415,16 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
   constexpr int KK = K * K;
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
-  __shared__ __align__(16) float stage[8][8][K];
+  constexpr int kWarps = K == 16 ? 16 : 8;
+  __shared__ __align__(16) float stage[kWarps][8][K];
+  __shared__ __align__(16) double astage[kWarps][8][K];
   __shared__ double bpart[KK];
   const int rank = blockIdx.x;  // cluster rank (cluster spans gridDim.x)
   const int slot = blockIdx.y;
   const int t = slot - 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RB = (((N + kCluster - 1) / kCluster) + 63) / 64 * 64;
-  const int WR = RB / 8;  // rows per warp (multiple of 8)
+  const int RB = (((N + kCluster - 1) / kCluster) + 127) / 128 * 128;
+  const int WR = RB / kWarps;  // rows per warp (multiple of 8)
   const int r_begin = rank * RB + warp * WR;
   const int r_end = min(N, r_begin + WR);
   const int c = (lane * E) / K;
@@ -432,6 +434,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
   for (int b0 = r_begin; b0 < r_end; b0 += 8) {
     const int nrow = min(8, r_end - b0);
+    for (int item = lane; item < 8 * (K / 2); item += 32) {
+      const int r8 = item / (K / 2), q = item - r8 * (K / 2);
+      double2 v = make_double2(0.0, 0.0);
+      if (r8 < nrow) v = __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q);
+      *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = v;
+    }
     if (slot > 0) {
       for (int item = lane; item < 8 * K4; item += 32) {
         const int r8 = item / K4, q = item - r8 * K4;
@@ -459,7 +467,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
       }
       __syncwarp();
       for (int r8 = 0; r8 < nrow; ++r8) {
-        const double a = A[(size_t)(b0 + r8) * K + c];
+        const double a = astage[warp][r8][c];
 #pragma unroll
         for (int q = 0; q < E; q += 4) {
           const float4 p4 = *reinterpret_cast<const float4*>(&stage[warp][r8][d0 + q]);
@@ -471,20 +479,17 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
       }
       __syncwarp();
     } else {
+      __syncwarp();
       for (int r8 = 0; r8 < nrow; ++r8) {
-        const double* Ai = A + (size_t)(b0 + r8) * K;
-        const double a = Ai[c];
+        const double a = astage[warp][r8][c];
 #pragma unroll
-        for (int q = 0; q < E; q += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(Ai + d0 + q);
-          acc[q] = fma(a, v.x, acc[q]);
-          acc[q + 1] = fma(a, v.y, acc[q + 1]);
-        }
+        for (int q = 0; q < E; ++q) acc[q] = fma(a, astage[warp][r8][d0 + q], acc[q]);
       }
     }
+    __syncwarp();
   }
   // CTA partial: warps add in warp order (fixed, deterministic)
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < kWarps; ++w) {
     if (warp == w) {
 #pragma unroll
       for (int q = 0; q < E; ++q) {
@@ -506,11 +511,11 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(256)
   cluster.sync();
 }
 
-// k2b_v4: A update for K in {16, 32}; P, Q plain (reduced by k2a_v4).
-// Thread = (2 rows, column c); the cores of a group of slices are staged as
-// fp32 W32 = [R_t^T ; R_t] (written by the K2f commit), so each shared load
-// feeds 2 rows. P/Q rows are read as float4 through L1 (shared by the K
-// threads of a row).
+// k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
+// block stages W32 = [R_t^T ; R_t] (fp32, written by the K2f commit) and its
+// RB rows of P_t / Q_t in shared memory with coalesced float4 loads (one
+// latency per group); thread = (2 rows, column c) then runs from shared
+// memory: every W value feeds 2 rows, P/Q reads are broadcasts.
 template <int K>
 __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __restrict__ A64,
                                               float* __restrict__ A32,
@@ -526,30 +531,47 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
   extern __shared__ float shf[];
   constexpr int TR = 256 / K;      // thread rows
   constexpr int RB = 2 * TR;       // rows per block
+  constexpr int K4 = K / 4;
+  float* Ws = shf;                                   // [tg][2][K][K]
+  float* PQs = shf + (size_t)tg * 2 * K * K;         // [tg][2][RB][K]
   const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
-  const int i0 = blockIdx.x * RB + rl, i1 = i0 + TR;
-  const int j0 = min(i0, N - 1), j1 = min(i1, N - 1);
+  const int rbase = blockIdx.x * RB;
+  const int i0 = rbase + rl, i1 = i0 + TR;
   double n0 = 0.0, n1 = 0.0;
   for (int tb = 0; tb < M; tb += tg) {
     const int nt = min(tg, M - tb);
     __syncthreads();
-    const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)tb * 2 * K * K);
-    float4* dst = reinterpret_cast<float4*>(shf);
-    for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = __ldg(src + e);
+    {
+      const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)tb * 2 * K * K);
+      float4* dst = reinterpret_cast<float4*>(Ws);
+      for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = __ldg(src + e);
+      float4* pq = reinterpret_cast<float4*>(PQs);
+      for (int e = threadIdx.x; e < nt * 2 * RB * K4; e += blockDim.x) {
+        const int u = e / (2 * RB * K4), rem = e - u * 2 * RB * K4;
+        const int which = rem / (RB * K4), rem2 = rem - which * RB * K4;
+        const int r = rem2 / K4, q = rem2 - r * K4;
+        const int row = rbase + r;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < N)
+          v = __ldg(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + q);
+        pq[e] = v;
+      }
+    }
     __syncthreads();
     for (int u = 0; u < nt; ++u) {
-      const int t = tb + u;
-      const float* WrT = shf + (size_t)u * 2 * K * K;  // [d][c] = R_t[c][d]
-      const float* Wr = WrT + K * K;                   // [d][c] = R_t[d][c]
-      const float4* p0 = reinterpret_cast<const float4*>(P + ((size_t)t * N + j0) * K);
-      const float4* p1 = reinterpret_cast<const float4*>(P + ((size_t)t * N + j1) * K);
-      const float4* q0 = reinterpret_cast<const float4*>(Q + ((size_t)t * N + j0) * K);
-      const float4* q1 = reinterpret_cast<const float4*>(Q + ((size_t)t * N + j1) * K);
+      const float* WrT = Ws + (size_t)u * 2 * K * K;  // [d][c] = R_t[c][d]
+      const float* Wr = WrT + K * K;                  // [d][c] = R_t[d][c]
+      const float* pr0 = PQs + ((size_t)u * 2 * RB + rl) * K;
+      const float* pr1 = pr0 + TR * K;
+      const float* qr0 = PQs + ((size_t)u * 2 * RB + RB + rl) * K;
+      const float* qr1 = qr0 + TR * K;
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int d4 = 0; d4 < K / 4; ++d4) {
-        const float4 a0 = __ldg(p0 + d4), a1 = __ldg(p1 + d4);
-        const float4 b0 = __ldg(q0 + d4), b1 = __ldg(q1 + d4);
+      for (int d4 = 0; d4 < K4; ++d4) {
+        const float4 a0 = *reinterpret_cast<const float4*>(pr0 + 4 * d4);
+        const float4 a1 = *reinterpret_cast<const float4*>(pr1 + 4 * d4);
+        const float4 b0 = *reinterpret_cast<const float4*>(qr0 + 4 * d4);
+        const float4 b1 = *reinterpret_cast<const float4*>(qr1 + 4 * d4);
         const float pa[4] = {a0.x, a0.y, a0.z, a0.w}, pb[4] = {a1.x, a1.y, a1.z, a1.w};
         const float qa[4] = {b0.x, b0.y, b0.z, b0.w}, qb[4] = {b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -599,6 +621,12 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
     ATh[(size_t)c * N + i1] = hi;
     ATl[(size_t)c * N + i1] = lo;
   }
+}
+
+inline int k2b_v4_tg(int K, int M) {
+  const int RB = 2 * (256 / K);
+  const size_t per = (size_t)(2 * K * K + 2 * RB * K) * sizeof(float);
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (96 * 1024) / per));
 }
 
 // ---------------------------------------------------------------------------
