@@ -29,6 +29,7 @@
 namespace rk {
 namespace tc {
 
+constexpr int kStages = 2;
 constexpr int kTile = 128;
 constexpr int kThreads = 192;
 constexpr uint32_t kXBox = 128 * 64 * 2;  // one 128-row x 64-col bf16 box = 16 KB
@@ -159,21 +160,6 @@ RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
 }
 
 // ------------------------------- the kernel --------------------------------
-// Shared-memory ring: kHalves half-stages of 32 KB, each holding ONE plane
-// (hi or lo) of one 128x128 X tile (two 64-column TMA boxes). A tile uses two
-// consecutive half-stages (hi then lo), so the hi half is released to the
-// producer while the lo-plane MMAs still run. The column operand A_J (hi+lo
-// planes of A_col^T for the tile's 128 columns) has its own 2-slot ring; the
-// row operand A_I (per item) its own 2-slot ring.
-constexpr int kHalves = 5;
-constexpr uint32_t kHalfBytes = 2 * kXBox;  // 32 KB
-
-template <int K>
-constexpr uint32_t k1_smem_bytes() {
-  return 1024 /*align slack*/ + kHalves * kHalfBytes + 2 * (4 * K * 128) /*A_J*/ +
-         2 * (4 * K * 128) /*A_I*/ + 256 /*barriers*/;
-}
-
 template <int K>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -184,8 +170,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
   // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
   static_assert(K == 16 || K == 32, "tcgen05 path supports k_pad 16 or 32");
-  constexpr uint32_t kABox = K * 128;  // K rows x 64 bf16
-  constexpr uint32_t kAJBytes = 4 * kABox;
+  constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
+  constexpr uint32_t kStageX = 4 * kXBox;          // Xh0 Xh1 Xl0 Xl1
+  constexpr uint32_t kStageBytes = kStageX + 4 * kABox;
   constexpr uint32_t kAIBytes = 4 * kABox;
 
   if (args.skip_if_stopped && args.ctl->stop) return;
@@ -193,21 +180,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (of the shared-window address) for SWIZZLE_128B atoms
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* half_base = smem;                                  // kHalves * 32 KB
-  uint8_t* aj_base = smem + kHalves * kHalfBytes;             // 2 * kAJBytes
-  uint8_t* ai_base = aj_base + 2 * kAJBytes;                  // 2 * kAIBytes
+  uint8_t* stage_base = smem;                                  // kStages * kStageBytes
+  uint8_t* ai_base = smem + kStages * kStageBytes;             // 2 * kAIBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(ai_base + 2 * kAIBytes);
-  uint64_t* full = bars;                 // [kHalves]
-  uint64_t* empty = bars + kHalves;      // [kHalves]
-  uint64_t* aj_full = bars + 10;         // [2]
-  uint64_t* aj_empty = bars + 12;        // [2]
-  uint64_t* ai_full = bars + 14;         // [2]
-  uint64_t* ai_empty = bars + 16;        // [2]
-  uint64_t* p_full = bars + 18;          // [2]
-  uint64_t* p_empty = bars + 20;         // [2]
-  uint64_t* q_full = bars + 22;          // [1]
-  uint64_t* q_empty = bars + 23;         // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  // barrier slots
+  uint64_t* full = bars;             // [kStages]
+  uint64_t* empty = bars + 2;        // [kStages]
+  uint64_t* ai_full = bars + 4;      // [2]
+  uint64_t* ai_empty = bars + 6;     // [2]
+  uint64_t* p_full = bars + 8;       // [2]
+  uint64_t* p_empty = bars + 10;     // [2]
+  uint64_t* q_full = bars + 12;      // [1]
+  uint64_t* q_empty = bars + 13;     // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -216,13 +201,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nstrips = args.nstrips, nrb = args.nrb, ncb = args.ncb, c = args.c, NR = args.NR;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kHalves; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
       mbar_init(smem_u32(&empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&aj_full[i]), 1);
-      mbar_init(smem_u32(&aj_empty[i]), 1);
       mbar_init(smem_u32(&ai_full[i]), 1);
       mbar_init(smem_u32(&ai_empty[i]), 1);
       mbar_init(smem_u32(&p_full[i]), 1);
@@ -255,16 +238,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ============================ TMA producer ============================
     if (lane == 0) {
-      int hs = 0;
-      uint32_t hphase = 0;
-      int tile = 0;  // running tile count (A_J ring index)
+      int stage = 0;
+      uint32_t phase = 0;
       for (int item = item_b; item < item_e; ++item) {
         int t, s, rb;
         decode_item(item, nstrips, nrb, t, s, rb);
         const int ct = strip_tiles(s, nstrips, c, ncb);
         const int ab = (item - item_b) & 1;
         const uint32_t ap = ((item - item_b) >> 1) & 1;
-        // A_row^T[:, I] (B operand of Q) for this row block
+        // A^T[:, I] (row operand of Q) for this row block
         mbar_wait(smem_u32(&ai_empty[ab]), ap ^ 1);
         const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
         const uint32_t aib = smem_u32(&ai_full[ab]);
@@ -274,33 +256,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(ai + 2 * kABox, &map_rl, rb * kTile, 0, aib);
         tma_load_2d(ai + 3 * kABox, &map_rl, rb * kTile + 64, 0, aib);
         const int xrow = t * NR + rb * kTile;
-        for (int cb = 0; cb < ct; ++cb, ++tile) {
+        for (int cb = 0; cb < ct; ++cb) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_expect_tx(fb, kStageBytes);
           const int j0 = (s * c + cb) * kTile;
-          // A_col^T[:, J] (B operand of P)
-          const int jb = tile & 1;
-          const uint32_t jp = (tile >> 1) & 1;
-          mbar_wait(smem_u32(&aj_empty[jb]), jp ^ 1);
-          const uint32_t aj = smem_u32(aj_base + jb * kAJBytes);
-          const uint32_t ajb = smem_u32(&aj_full[jb]);
-          mbar_expect_tx(ajb, kAJBytes);
-          tma_load_2d(aj + 0 * kABox, &map_ch, j0, 0, ajb);
-          tma_load_2d(aj + 1 * kABox, &map_ch, j0 + 64, 0, ajb);
-          tma_load_2d(aj + 2 * kABox, &map_cl, j0, 0, ajb);
-          tma_load_2d(aj + 3 * kABox, &map_cl, j0 + 64, 0, ajb);
-          // X tile: hi plane, then lo plane, each into its own half-stage
-#pragma unroll
-          for (int plane = 0; plane < 2; ++plane) {
-            mbar_wait(smem_u32(&empty[hs]), hphase ^ 1);
-            const uint32_t st = smem_u32(half_base + hs * kHalfBytes);
-            const uint32_t fb = smem_u32(&full[hs]);
-            mbar_expect_tx(fb, kHalfBytes);
-            const CUtensorMap* mp = plane == 0 ? &map_xh : &map_xl;
-            tma_load_2d(st, mp, j0, xrow, fb);
-            tma_load_2d(st + kXBox, mp, j0 + 64, xrow, fb);
-            if (++hs == kHalves) {
-              hs = 0;
-              hphase ^= 1;
-            }
+          tma_load_2d(st + 0 * kXBox, &map_xh, j0, xrow, fb);
+          tma_load_2d(st + 1 * kXBox, &map_xh, j0 + 64, xrow, fb);
+          tma_load_2d(st + 2 * kXBox, &map_xl, j0, xrow, fb);
+          tma_load_2d(st + 3 * kXBox, &map_xl, j0 + 64, xrow, fb);
+          tma_load_2d(st + kStageX + 0 * kABox, &map_ch, j0, 0, fb);
+          tma_load_2d(st + kStageX + 1 * kABox, &map_ch, j0 + 64, 0, fb);
+          tma_load_2d(st + kStageX + 2 * kABox, &map_cl, j0, 0, fb);
+          tma_load_2d(st + kStageX + 3 * kABox, &map_cl, j0 + 64, 0, fb);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -310,10 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t id_p = idesc_bf16(K, 0);  // A = X tile, K-major (K-dim = j)
       const uint32_t id_q = idesc_bf16(K, 1);  // A = X tile, MN-major (M = j, K-dim = i)
-      const bool do_mma = !(args.debug & 1);
-      int hs = 0;
-      uint32_t hphase = 0;
-      int tile = 0;
+      int stage = 0;
+      uint32_t phase = 0;
       uint32_t qe_phase = 0;
       int seg = 0;
       for (int item = item_b; item < item_e; ++item) {
@@ -338,49 +308,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
         const uint32_t p_tmem = tmem + (uint32_t)(c * K + pb * K);
-        for (int cb = 0; cb < ct; ++cb, ++tile) {
-          const int jb = tile & 1;
-          const uint32_t jp = (tile >> 1) & 1;
-          mbar_wait(smem_u32(&aj_full[jb]), jp);
-          const uint32_t ajh = smem_u32(aj_base + jb * kAJBytes);
-          const uint32_t ajl = ajh + 2 * kABox;
+        for (int cb = 0; cb < ct; ++cb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+          const uint32_t xh = st, xl = st + 2 * kXBox;
+          const uint32_t ajh = st + kStageX, ajl = st + kStageX + 2 * kABox;
           const uint32_t q_tmem = tmem + (uint32_t)(cb * K);
 #pragma unroll
-          for (int plane = 0; plane < 2; ++plane) {
-            mbar_wait(smem_u32(&full[hs]), hphase);
-            tc_fence_after();
-            const uint32_t x = smem_u32(half_base + hs * kHalfBytes);
-            if (do_mma) {
-#pragma unroll
-              for (int ks = 0; ks < 8; ++ks) {
-                // P: rows i (M=128), K-dim j — 16 columns per MMA
-                const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
-                const uint32_t aoff = (ks >> 2) * kABox + (ks & 3) * 32;
-                const uint64_t dx = umma_desc(x + xoff, 16, 1024);
-                const uint64_t dah = umma_desc(ajh + aoff, 16, 1024);
-                // Q: rows j (M=128, MN-major), K-dim i — 16 rows per MMA
-                const uint64_t qx = umma_desc(x + ks * 16 * 128, kXBox, 1024);
-                const uint64_t qah = umma_desc(ai + aoff, 16, 1024);
-                if (plane == 0) {
-                  const uint64_t dal = umma_desc(ajl + aoff, 16, 1024);
-                  const uint64_t qal = umma_desc(ai + 2 * kABox + aoff, 16, 1024);
-                  tc_mma(p_tmem, dx, dah, id_p, (cb > 0 || ks > 0) ? 1u : 0u);
-                  tc_mma(p_tmem, dx, dal, id_p, 1u);
-                  tc_mma(q_tmem, qx, qah, id_q, (first_in_seg && ks == 0) ? 0u : 1u);
-                  tc_mma(q_tmem, qx, qal, id_q, 1u);
-                } else {
-                  tc_mma(p_tmem, dx, dah, id_p, 1u);
-                  tc_mma(q_tmem, qx, qah, id_q, 1u);
-                }
-              }
-            }
-            tc_commit(smem_u32(&empty[hs]));
-            if (++hs == kHalves) {
-              hs = 0;
-              hphase ^= 1;
-            }
+          for (int ks = 0; ks < ((args.debug & 1) ? 0 : 8); ++ks) {
+            // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
+            const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
+            const uint32_t aoff = (ks >> 2) * kABox + (ks & 3) * 32;
+            const uint64_t dxh = umma_desc(xh + xoff, 16, 1024);
+            const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
+            const uint64_t dah = umma_desc(ajh + aoff, 16, 1024);
+            const uint64_t dal = umma_desc(ajl + aoff, 16, 1024);
+            const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
+            tc_mma(p_tmem, dxh, dah, id_p, accp);
+            tc_mma(p_tmem, dxh, dal, id_p, 1u);
+            tc_mma(p_tmem, dxl, dah, id_p, 1u);
+            // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
+            const uint32_t roff = ks * 16 * 128;
+            const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
+            const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
+            const uint64_t qah = umma_desc(ai + aoff, 16, 1024);
+            const uint64_t qal = umma_desc(ai + 2 * kABox + aoff, 16, 1024);
+            const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
+            tc_mma(q_tmem, qxh, qah, id_q, accq);
+            tc_mma(q_tmem, qxh, qal, id_q, 1u);
+            tc_mma(q_tmem, qxl, qah, id_q, 1u);
           }
-          tc_commit(smem_u32(&aj_empty[jb]));
+          tc_commit(smem_u32(&empty[stage]));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
         tc_commit(smem_u32(&p_full[pb]));
         tc_commit(smem_u32(&ai_empty[ab]));
@@ -448,6 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+template <int K>
+constexpr uint32_t k1_smem_bytes() {
+  return 1024 /*align slack*/ + kStages * (4 * kXBox + 4 * K * 128) + 2 * (4 * K * 128) + 256;
 }
 
 // Deterministic reduction of the partials:
