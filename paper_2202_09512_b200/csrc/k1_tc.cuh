@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
   const int K4 = K / 4;
   const int64_t totalP = (int64_t)M * NR * K4;
   const int64_t total = totalP + (int64_t)M * NC * K4;
+#pragma unroll 2
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     if (e < totalP) {

@@ -429,7 +429,7 @@ void launch_k1(rk_handle* h, bool timed) {
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
     {
-      rk::tc::k1_reduce<<<h->num_sms * 4, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
+      rk::tc::k1_reduce<<<h->num_sms * 8, 256, 0, s>>>(h->ctl, h->Ppart, h->Qpart, h->d_slot_first,
                                                         h->d_slot_count, h->P, h->Q, (int)h->NR,
                                                         (int)h->NC, K, M, h->c, h->nstrips, 1);
       h->launches += 1;

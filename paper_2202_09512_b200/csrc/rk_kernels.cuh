@@ -434,11 +434,22 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
   for (int b0 = r_begin; b0 < r_end; b0 += 8) {
     const int nrow = min(8, r_end - b0);
-    for (int item = lane; item < 8 * (K / 2); item += 32) {
-      const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-      double2 v = make_double2(0.0, 0.0);
-      if (r8 < nrow) v = __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q);
-      *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = v;
+    {
+      constexpr int NA = 8 * (K / 2) / 32;  // double2 items per lane (2 or 4)
+      double2 v[NA];
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int item = lane + 32 * u;
+        const int r8 = item / (K / 2), q = item - r8 * (K / 2);
+        v[u] = r8 < nrow ? __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q)
+                         : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int item = lane + 32 * u;
+        const int r8 = item / (K / 2), q = item - r8 * (K / 2);
+        *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = v[u];
+      }
     }
     if (slot > 0) {
       for (int item = lane; item < 8 * K4; item += 32) {
@@ -544,17 +555,42 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
     {
       const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)tb * 2 * K * K);
       float4* dst = reinterpret_cast<float4*>(Ws);
-      for (int e = threadIdx.x; e < nt * 2 * K * K / 4; e += blockDim.x) dst[e] = __ldg(src + e);
+      const int nw = nt * 2 * K * K / 4;
+      for (int e0 = threadIdx.x; e0 < nw; e0 += 4 * blockDim.x) {
+        float4 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = e0 + q * blockDim.x;
+          v[q] = e < nw ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = e0 + q * blockDim.x;
+          if (e < nw) dst[e] = v[q];
+        }
+      }
       float4* pq = reinterpret_cast<float4*>(PQs);
-      for (int e = threadIdx.x; e < nt * 2 * RB * K4; e += blockDim.x) {
-        const int u = e / (2 * RB * K4), rem = e - u * 2 * RB * K4;
-        const int which = rem / (RB * K4), rem2 = rem - which * RB * K4;
-        const int r = rem2 / K4, q = rem2 - r * K4;
-        const int row = rbase + r;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < N)
-          v = __ldg(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + q);
-        pq[e] = v;
+      const int npq = nt * 2 * RB * K4;
+      for (int e0 = threadIdx.x; e0 < npq; e0 += 8 * blockDim.x) {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = e0 + q * blockDim.x;
+          v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < npq) {
+            const int u = e / (2 * RB * K4), rem = e - u * 2 * RB * K4;
+            const int which = rem / (RB * K4), rem2 = rem - which * RB * K4;
+            const int r = rem2 / K4, qq = rem2 - r * K4;
+            const int row = rbase + r;
+            if (row < N)
+              v[q] = __ldg(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + qq);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = e0 + q * blockDim.x;
+          if (e < npq) pq[e] = v[q];
+        }
       }
     }
     __syncthreads();
