@@ -1,0 +1,30 @@
+"""Multi-GPU NCCL grid parity (needs >= 2 GPUs; skipped on a 1-GPU box)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    from paper_2202_09512_b200 import _lib
+    return _lib.device_count()
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_grid_matches_oracle(nproc):
+    if _gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc),
+           os.path.join(ROOT, "tools", "grid_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert out.returncode == 0 and line, out.stdout[-2000:] + out.stderr[-2000:]
+    rep = json.loads(line[-1])
+    assert rep["ok"], rep

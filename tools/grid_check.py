@@ -1,0 +1,41 @@
+"""Multi-GPU parity check (run under torchrun, one rank per GPU): the NCCL
+p_r x p_c grid path vs the CPU oracle on identical inputs."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch.distributed as dist
+
+import oracle
+import paper_2202_09512_b200 as rk
+
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+results = []
+ok = True
+for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "auto"), (700, 2, 32, 12, "auto"),
+                                 (257, 2, 4, 25, "simt")]:
+    x = np.random.default_rng(n).random((m, n, n), dtype=np.float32).astype(np.float64)
+    f0 = rk.random_init(n, k, m, 1)
+    f, tr, info = rk.solve_on_grid(rk.RelTensor(x), k, rk.SolverConfig(max_iters=iters, engine=engine),
+                                   initial=f0)
+    rb = [None] * world
+    dist.all_gather_object(rb, f.R.tobytes())
+    if rank == 0:
+        ao, ro, tro = oracle.solve([x[t] for t in range(m)], k, oracle.OracleConfig(max_iters=iters),
+                                   initial=(f0.A, f0.R))
+        rel_a = float(np.linalg.norm(f.A - ao) / np.linalg.norm(ao))
+        rel_r = float(np.linalg.norm(f.R - ro) / np.linalg.norm(ro))
+        derr = float(np.max(np.abs(tr - tro)))
+        same_r = len(set(rb)) == 1
+        good = rel_a <= 1e-4 and rel_r <= 1e-4 and derr <= 1e-5 and same_r and len(tr) == iters
+        ok = ok and good
+        results.append(dict(n=n, m=m, k=k, iters=iters, engine=engine, grid=[info["pr"], info["pc"]],
+                            relA=rel_a, relR=rel_r, dErr=derr, R_replicated=same_r, ok=good))
+if rank == 0:
+    print(json.dumps({"world": world, "ok": ok, "cases": results}))
+dist.destroy_process_group()
+sys.exit(0 if ok or rank != 0 else 1)
