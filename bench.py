@@ -339,20 +339,40 @@ def run_ours(args, dist, rank, world, local_rank):
     # ---------------- end to end through the public API (host buffers) ------
     if not args.no_e2e:
         try:
+            phases = {}
             if world == 1:
                 xh = host_tensor(m, n, pinned=True)
                 x = rk.RelTensor(xh)  # validation outside the timed region, as a caller would
-                torch_sync = None
                 t0 = time.perf_counter()
                 f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, device=local_rank),
                                         initial=f0)
                 e2e_s = time.perf_counter() - t0
                 h2d = xh.nbytes + f0.A.nbytes + f0.R.nbytes
                 d2h = f.A.nbytes + f.R.nbytes + tr.nbytes
+                # phase breakdown of the same work through the Engine API (not the headline)
+                tp = time.perf_counter()
+                e3 = _lib.Engine(n, m, k, device=local_rank)
+                phases["create_s"] = time.perf_counter() - tp
+                tp = time.perf_counter()
+                e3.upload(xh)
+                phases["upload_s"] = time.perf_counter() - tp
+                tp = time.perf_counter()
+                e3.set_factors(f0.A, f0.R)
+                e3.run(args.steps, eps, track_error=True)
+                phases["run_s"] = time.perf_counter() - tp
+                tp = time.perf_counter()
+                e3.get_factors()
+                phases["download_s"] = time.perf_counter() - tp
+                e3.close()
             else:
                 eng2, info2 = make_grid_engine(n, m, k, cfg=cfg)
                 # this rank's block, exact values of the same generator
-                blk = eng2.block_uniform(SEED, info2["rows"], info2["cols"])
+                import torch
+
+                blk0 = eng2.block_uniform(SEED, info2["rows"], info2["cols"])
+                blk = torch.empty(blk0.size, dtype=torch.float32, pin_memory=True).numpy().reshape(blk0.shape)
+                blk[...] = blk0
+                del blk0
                 barrier(dist)
                 t0 = time.perf_counter()
                 eng2.upload_block(blk, 1.0)
@@ -368,7 +388,7 @@ def run_ours(args, dist, rank, world, local_rank):
                            "d2h_bytes_per_step": int(d2h / args.steps),
                            "api": "rescal_solve(RelTensor(pinned fp32 host X), k, SolverConfig(max_iters=steps))"
                            if world == 1 else "Engine grid API: upload_block + run + get_factors",
-                           "seconds": e2e_s}
+                           "seconds": e2e_s, "phases": phases}
         except Exception as exc:  # report, never hide
             line["e2e"] = {"value": None, "unit": "it/s", "error": repr(exc)[:300],
                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
