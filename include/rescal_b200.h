@@ -64,6 +64,18 @@ int rk_device_count(int* out);
 int rk_create(int device, int64_t n, int64_t m, int32_t k, int32_t engine, rk_handle** out);
 void rk_destroy(rk_handle* h);
 
+/* Sparse tensor engine (cfg4 path): m CSR slices of n x n, rank k <= 32.
+ * Replaces the SparseRelTensor operand path (tensor.py:86-139; scipy CSR
+ * X_t @ A and X_t.T @ (A R_t) inside rescal.py:128,134-135). */
+int rk_create_sparse(int device, int64_t n, int64_t m, int32_t k, rk_handle** out);
+
+/* All slices at once: indptr is (m, n+1) int64 GLOBAL offsets into the
+ * concatenated indices (int32 column ids, sorted per row, no duplicates —
+ * the SparseRelTensor canonical form, tensor.py:96-104) and data (dtype).
+ * The CSC (transposed) index arrays are built on the device. */
+int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, const void* data,
+                  int32_t dtype, int64_t nnz);
+
 /* Host tensor -> device. x is (m, n, n) C-contiguous in `dtype`. Replaces the
  * dense RelTensor.slice_ops() operand view (tensor.py:67-69). Also records
  * ||X||^2 in fp64 from the host values (rescal.py:160-165). */

@@ -45,6 +45,8 @@ SIGNATURES = {
     "rk_destroy": (None, [_vp]),
     "rk_upload_dense": (ctypes.c_int, [_vp, _vp, _i32]),
     "rk_upload_block": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _f64]),
+    "rk_create_sparse": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i32, ctypes.POINTER(_vp)]),
+    "rk_upload_csr": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _vp, _i32, _i64]),
     "rk_fill_uniform": (ctypes.c_int, [_vp, _u64]),
     "rk_set_factors": (ctypes.c_int, [_vp, _pd, _pd]),
     "rk_get_factors": (ctypes.c_int, [_vp, _pd, _pd]),
@@ -70,6 +72,10 @@ SIGNATURES = {
     "rk_trace_len": (ctypes.c_int, [_vp, _pi32]),
     "rk_restore": (ctypes.c_int, [_vp]),
     "rk_block_uniform": (ctypes.c_int, [_vp, _u64, _pf]),
+    "rk_csc_copy": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _pf]),
+    "rk_csr_copy": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _pf]),
+    "rk_fill_sparse_uniform": (ctypes.c_int, [_vp, _u64, _i64]),
+    "rk_nnz": (ctypes.c_int, [_vp, _pi64]),
 }
 
 _LIB = None
@@ -117,13 +123,17 @@ def pcg64_seed_state(entropy):
 class Engine:
     """One device-resident RESCAL problem (tensor + factors) on one GPU."""
 
-    def __init__(self, n, m, k, device=None, engine="auto"):
+    def __init__(self, n, m, k, device=None, engine="auto", sparse=False):
         lib = load()
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", "0"))
         self.n, self.m, self.k = int(n), int(m), int(k)
+        self.sparse = bool(sparse)
         self._h = _vp()
-        check(lib.rk_create(int(device), self.n, self.m, self.k, ENGINES[engine], ctypes.byref(self._h)))
+        if self.sparse:
+            check(lib.rk_create_sparse(int(device), self.n, self.m, self.k, ctypes.byref(self._h)))
+        else:
+            check(lib.rk_create(int(device), self.n, self.m, self.k, ENGINES[engine], ctypes.byref(self._h)))
         self._lib = lib
 
     # lifecycle -----------------------------------------------------------
@@ -152,6 +162,52 @@ class Engine:
         if x.shape != (self.m, self.n, self.n):
             raise DataError(f"tensor shape {x.shape} != ({self.m}, {self.n}, {self.n})")
         check(self._lib.rk_upload_dense(self._h, x.ctypes.data_as(_vp), RK_F32 if x.dtype == np.float32 else RK_F64))
+
+    def upload_csr(self, slices):
+        """Canonical CSR slices (scipy) -> device CSR + device-built CSC."""
+        if len(slices) != self.m:
+            raise DataError(f"expected {self.m} slices, got {len(slices)}")
+        nnz = np.array([s.nnz for s in slices], dtype=np.int64)
+        base = np.concatenate([[0], np.cumsum(nnz)[:-1]])
+        indptr = np.concatenate([s.indptr.astype(np.int64) + b for s, b in zip(slices, base)])
+        indices = np.ascontiguousarray(np.concatenate([s.indices for s in slices]).astype(np.int32))
+        data = np.concatenate([s.data for s in slices])
+        data = np.ascontiguousarray(data if data.dtype in (np.float32, np.float64) else data.astype(np.float64))
+        indptr = np.ascontiguousarray(indptr)
+        check(self._lib.rk_upload_csr(self._h, indptr.ctypes.data_as(_pi64),
+                                      indices.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      data.ctypes.data_as(_vp), RK_F32 if data.dtype == np.float32 else RK_F64,
+                                      int(nnz.sum())))
+
+    def fill_sparse_uniform(self, seed, nnz_per_slice):
+        """Synthetic uniform-random sparse slices generated on the device."""
+        check(self._lib.rk_fill_sparse_uniform(self._h, int(seed), int(nnz_per_slice)))
+
+    @property
+    def nnz(self):
+        out = _i64(0)
+        check(self._lib.rk_nnz(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    def csr_arrays(self):
+        nnz = self.nnz
+        indptr = np.empty(self.m * (self.n + 1), dtype=np.int64)
+        indices = np.empty(nnz, dtype=np.int32)
+        data = np.empty(nnz, dtype=np.float32)
+        check(self._lib.rk_csr_copy(self._h, indptr.ctypes.data_as(_pi64),
+                                    indices.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                    data.ctypes.data_as(_pf)))
+        return indptr.reshape(self.m, self.n + 1), indices, data
+
+    def csc_arrays(self, nnz):
+        """Device-built CSC (tests: index construction must match scipy)."""
+        indptr = np.empty(self.m * (self.n + 1), dtype=np.int64)
+        indices = np.empty(nnz, dtype=np.int32)
+        data = np.empty(nnz, dtype=np.float32)
+        check(self._lib.rk_csc_copy(self._h, indptr.ctypes.data_as(_pi64),
+                                    indices.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                    data.ctypes.data_as(_pf)))
+        return indptr.reshape(self.m, self.n + 1), indices, data
 
     def upload_block(self, xb, sq_norm_global):
         xb = np.ascontiguousarray(xb)

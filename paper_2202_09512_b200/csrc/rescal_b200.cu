@@ -27,6 +27,10 @@
 #include "../../include/rescal_b200.h"
 #include "k1_tc.cuh"
 #include "rk_kernels.cuh"
+#include "sparse.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 using rk::Ctl;
 
@@ -188,6 +192,14 @@ struct rk_handle {
   int k1_count = 0, launches = 0, iter_launches = 0;
   double eps = 1e-16;
 
+  // sparse tensor (CSR + device-built CSC, fp32 values)
+  bool sparse = false;
+  int64_t nnz = 0;
+  int64_t *csr_ptr = nullptr, *csc_ptr = nullptr;
+  int *csr_idx = nullptr, *csc_idx = nullptr;
+  float *csr_val = nullptr, *csc_val = nullptr, *csr_val0 = nullptr, *csc_val0 = nullptr;
+  double* numer = nullptr;  // [n][K] A numerator (sparse path)
+
   bool grid() const { return pr * pc > 1; }
 };
 
@@ -203,6 +215,8 @@ void free_factor_buffers(rk_handle* h) {
     cudaGraphExecDestroy(h->graph);
     h->graph = nullptr;
   }
+  dfree(h->numer);
+  h->numer = nullptr;
   void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
                   h->part, h->red, h->gscratch, h->counters, h->W32, h->d_simt_first,
                   h->d_simt_count, h->UI, h->UJ, h->regS, h->regG, h->regT,
@@ -335,6 +349,15 @@ void alloc_factor_buffers(rk_handle* h) {
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
   h->counters = dalloc<unsigned>((size_t)M + 8);
   h->fast = !h->grid() && (K == 16 || K == 32);
+  if (h->sparse) {
+    h->numer = dalloc<double>((size_t)h->NR * K);
+    const size_t wsm = (size_t)M * 2 * KK * sizeof(float);
+    RK_REQUIRE(wsm <= 200 * 1024, RK_ERR_DATA, "sparse engine: m*k_pad^2 too large for the staged cores");
+    if (K == 16)
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    else
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+  }
   if (h->fast) {
     h->W32 = dalloc<float>((size_t)M * 2 * KK);
     std::vector<int> first(M), count(M, 1);
@@ -355,6 +378,7 @@ void alloc_factor_buffers(rk_handle* h) {
   h->regRn = dalloc<double>(M * KK);
   // engine
   int eng = h->requested_engine;
+  if (h->sparse) eng = RK_ENGINE_SIMT;  // gather-bound CSR/CSC kernels (no GEMM reshaping)
   if (eng == RK_ENGINE_AUTO) eng = (K == 16 || K == 32) ? RK_ENGINE_TC : RK_ENGINE_SIMT;
   RK_REQUIRE(!(eng == RK_ENGINE_TC && !(K == 16 || K == 32)), RK_ERR_DATA,
              "tcgen05 engine needs k_pad in {16, 32}");
@@ -402,7 +426,18 @@ void launch_k1(rk_handle* h, bool timed) {
     }
     RK_CUDA(cudaEventRecord(h->ev_k1[i], s));
   }
-  if (h->engine == RK_ENGINE_TC) {
+  if (h->sparse) {
+    const int grid = h->num_sms * 16;
+    if (K == 16)
+      rk::sp::sp_csr_pass<16><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32row,
+                                                  h->P, (int)h->n, (int)h->NR, M, 1);
+    else
+      rk::sp::sp_csr_pass<32><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32row,
+                                                  h->P, (int)h->n, (int)h->NR, M, 1);
+    RK_CUDA(cudaGetLastError());
+    if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
+    h->launches += 1;
+  } else if (h->engine == RK_ENGINE_TC) {
     rk::tc::K1Args a;
     a.NR = (int)h->NR;
     a.NC = (int)h->NC;
@@ -448,6 +483,7 @@ void launch_k1(rk_handle* h, bool timed) {
 }
 
 void launch_k5(rk_handle* h, int gate) {
+  if (h->sparse) return;  // the sparse trace uses the Gram identity (no dense residual)
   const int K = h->K;
   const size_t smem = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
   rk::k5_residual<<<h->nr, rk::kThreads, smem, h->stream>>>(
@@ -534,6 +570,26 @@ void grid_allgather_a(rk_handle* h) {
 void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
+  if (h->sparse) {
+    const int grid = h->num_sms * 8;
+    const size_t wsm = (size_t)h->m * 2 * K * K * sizeof(float);
+    if (K == 16) {
+      rk::sp::sp_csc_numer<16><<<grid, 256, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
+                                                               h->A32row, h->P, h->W32, h->numer,
+                                                               (int)h->n, (int)h->NR, (int)h->m);
+      rk::sp::sp_apply_a<16><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,
+                                                                    h->Mm, (int)h->n, eps_m);
+    } else {
+      rk::sp::sp_csc_numer<32><<<grid, 256, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
+                                                               h->A32row, h->P, h->W32, h->numer,
+                                                               (int)h->n, (int)h->NR, (int)h->m);
+      rk::sp::sp_apply_a<32><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,
+                                                                    h->Mm, (int)h->n, eps_m);
+    }
+    RK_CUDA(cudaGetLastError());
+    h->launches += 2;
+    return;
+  }
   if (h->fast) {
     const int rb = 2 * (256 / K);
     const int tg = rk::k2b_v4_tg(K, (int)h->m);
@@ -619,7 +675,7 @@ void reset_ctl(rk_handle* h, int track, double tol, int max_iters) {
   c.eps = h->eps;
   c.norm2 = h->norm2;
   c.norm2_dev = h->norm2_dev;
-  c.direct_thresh = 0.2;
+  c.direct_thresh = h->sparse ? -1.0 : 0.2;
   c.max_iters = max_iters;
   *h->ctl_host = c;
   RK_CUDA(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
@@ -677,6 +733,7 @@ void set_block_dims(rk_handle* h, int64_t rows_valid, int64_t cols_valid, int64_
 }
 
 void alloc_tensor(rk_handle* h) {
+  if (h->sparse) return;
   dfree(h->Xh);
   dfree(h->Xl);
   dfree(h->Xh0);
@@ -750,6 +807,43 @@ void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iter
   if (iters_done) *iters_done = it;
 }
 
+}  // namespace
+
+namespace {
+// Shared tail of the CSR uploads: build the CSC copy on the device.
+void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
+  const int64_t n = h->n, M = h->m;
+  int64_t max_nnz = 0;
+  for (int64_t t = 0; t < M; ++t)
+    max_nnz = std::max(max_nnz, indptr_host[t * (n + 1) + n] - indptr_host[t * (n + 1)]);
+  uint64_t* keys = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
+  uint64_t* keys2 = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
+  int* counts = dalloc<int>((size_t)n);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, h->csr_val, h->csc_val,
+                                  (int)std::max<int64_t>(1, max_nnz), 0, 64, h->stream);
+  void* tmp = dalloc<uint8_t>(tmp_bytes + 16);
+  for (int64_t t = 0; t < M; ++t) {
+    const int64_t base = indptr_host[t * (n + 1)], cnt = indptr_host[t * (n + 1) + n] - base;
+    RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * n, h->stream));
+    if (cnt > 0) {
+      rk::sp::sp_make_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(h->csr_ptr + t * (n + 1), h->csr_idx,
+                                                                   (int)n, base, cnt, keys);
+      const int bits = 32 + (int)std::ceil(std::log2((double)std::max<int64_t>(2, n)));
+      RK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, h->csr_val + base,
+                                              h->csc_val + base, (int)cnt, 0, std::min(64, bits),
+                                              h->stream));
+      rk::sp::sp_split_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(keys2, cnt, h->csc_idx + base, counts);
+    }
+    rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)n, base, h->csc_ptr + t * (n + 1));
+    RK_CUDA(cudaGetLastError());
+  }
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  dfree(keys);
+  dfree(keys2);
+  dfree(counts);
+  dfree(tmp);
+}
 }  // namespace
 
 // =============================== C ABI ======================================
@@ -831,6 +925,9 @@ void rk_destroy(rk_handle* h) {
   dfree(h->d_iters);
   dfree(h->trace_dev);
   dfree(h->d_colmap);
+  void* sps[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
+                 h->csc_val0};
+  for (void* p : sps) dfree(p);
   if (h->ctl_host) cudaFreeHost(h->ctl_host);
   if (h->stop_host) cudaFreeHost(h->stop_host);
   for (auto e : h->ev_k1) cudaEventDestroy(e);
@@ -843,10 +940,183 @@ void rk_destroy(rk_handle* h) {
   delete h;
 }
 
+int rk_create_sparse(int device, int64_t n, int64_t m, int32_t k, rk_handle** out) {
+  return guarded([&] {
+    RK_REQUIRE(out, RK_ERR_DATA, "null output handle");
+    *out = nullptr;
+    RK_REQUIRE(n >= 1 && m >= 1, RK_ERR_DATA, "need n >= 1 and m >= 1");
+    RK_REQUIRE(1 <= k && k <= n, RK_ERR_DATA,
+               "need 1 <= k <= n, got k=" + std::to_string(k) + ", n=" + std::to_string(n));
+    RK_REQUIRE(k <= 32, RK_ERR_DATA, "sparse engine supports k <= 32");
+    RK_REQUIRE(n < (1ll << 31), RK_ERR_DATA, "sparse engine: n must fit int32 indices");
+    int ndev = 0;
+    RK_CUDA(cudaGetDeviceCount(&ndev));
+    RK_REQUIRE(device >= 0 && device < ndev, RK_ERR_DEVICE, "no such CUDA device");
+    RK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RK_CUDA(cudaGetDeviceProperties(&prop, device));
+    RK_REQUIRE(prop.major == 10, RK_ERR_DEVICE,
+               std::string("sm_100a build needs a Blackwell (cc 10.x) GPU, found ") + prop.name);
+    rk_handle* h = new rk_handle();
+    h->sparse = true;
+    h->dev = device;
+    h->num_sms = prop.multiProcessorCount;
+    h->n = n;
+    h->m = m;
+    h->k = k;
+    h->K = k <= 16 ? 16 : 32;
+    h->requested_engine = RK_ENGINE_SIMT;
+    h->piece = n;
+    set_block_dims(h, n, n, round_up(n, 128), round_up(n, 128));
+    RK_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    RK_CUDA(cudaMalloc(&h->ctl, sizeof(Ctl)));
+    RK_CUDA(cudaMemset(h->ctl, 0, sizeof(Ctl)));
+    RK_CUDA(cudaDeviceSynchronize());
+    RK_CUDA(cudaMallocHost(&h->ctl_host, sizeof(Ctl)));
+    RK_CUDA(cudaMallocHost(&h->stop_host, 2 * sizeof(int)));
+    RK_CUDA(cudaEventCreate(&h->ev_run0));
+    RK_CUDA(cudaEventCreate(&h->ev_run1));
+    h->nnp = h->num_sms * 4;
+    h->npart = dalloc<double>(h->nnp);
+    h->npart2 = dalloc<double>(h->nnp);
+    h->d_iters = dalloc<int>(1);
+    alloc_factor_buffers(h);
+    *out = h;
+  });
+}
+
+int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, const void* data,
+                  int32_t dtype, int64_t nnz) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "rk_upload_csr needs a sparse handle");
+    RK_REQUIRE(indptr && (nnz == 0 || (indices && data)), RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(h->dev));
+    const int64_t n = h->n, M = h->m;
+    RK_REQUIRE(indptr[0] == 0 && indptr[M * (n + 1) - 1] == nnz, RK_ERR_DATA, "inconsistent indptr");
+    void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
+                   h->csc_val0};
+    for (void* p : old) dfree(p);
+    h->csr_val0 = h->csc_val0 = nullptr;
+    h->nnz = nnz;
+    h->csr_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    h->csc_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    h->csr_idx = dalloc<int>((size_t)nnz);
+    h->csc_idx = dalloc<int>((size_t)nnz);
+    h->csr_val = dalloc<float>((size_t)nnz);
+    h->csc_val = dalloc<float>((size_t)nnz);
+    // values -> fp32, ||X||^2 in fp64 from the host values (rescal.py:160-165)
+    std::vector<float> v32((size_t)nnz);
+    double s2 = 0.0;
+    for (int64_t e = 0; e < nnz; ++e) {
+      const double v = dtype == RK_F32 ? (double)static_cast<const float*>(data)[e]
+                                       : static_cast<const double*>(data)[e];
+      RK_REQUIRE(v >= 0.0, RK_ERR_DATA, "negative value in tensor");
+      s2 += v * v;
+      v32[e] = (float)v;
+    }
+    RK_CUDA(cudaMemcpy(h->csr_ptr, indptr, sizeof(int64_t) * M * (n + 1), cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(h->csr_idx, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(h->csr_val, v32.data(), sizeof(float) * nnz, cudaMemcpyHostToDevice));
+    build_csc(h, std::vector<int64_t>(indptr, indptr + M * (n + 1)));
+    h->norm2 = h->norm2_dev = h->norm2_orig = s2;
+    h->have_x = true;
+    h->perturbed = false;
+  });
+}
+
+
+int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_slice) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    const int64_t n = h->n, M = h->m, cnt = nnz_target_per_slice;
+    void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
+                   h->csc_val0};
+    for (void* p : old) dfree(p);
+    h->csr_val0 = h->csc_val0 = nullptr;
+    const size_t cap = (size_t)M * cnt;
+    h->csr_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    h->csc_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    h->csr_idx = dalloc<int>(cap);
+    h->csc_idx = dalloc<int>(cap);
+    h->csr_val = dalloc<float>(cap);
+    h->csc_val = dalloc<float>(cap);
+    uint64_t* keys = dalloc<uint64_t>(cnt);
+    uint64_t* keys2 = dalloc<uint64_t>(cnt);
+    int* flag = dalloc<int>(cnt);
+    int* pos = dalloc<int>(cnt);
+    int* counts = dalloc<int>(n);
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, keys2, (int)cnt, 0, 64, h->stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, pos, (int)cnt, h->stream);
+    void* tmp = dalloc<uint8_t>(std::max(t1, t2) + 16);
+    size_t tmp_bytes = std::max(t1, t2);
+    std::vector<int64_t> ptr_host((size_t)M * (n + 1));
+    int64_t base = 0;
+    for (int64_t t = 0; t < M; ++t) {
+      rk::sp::sp_gen_keys<<<h->num_sms * 8, 256, 0, h->stream>>>(seed, (int)t, cnt, (int)n, keys);
+      RK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys2, (int)cnt, 0, 64, h->stream));
+      rk::sp::sp_mark_unique<<<h->num_sms * 8, 256, 0, h->stream>>>(keys2, cnt, flag);
+      RK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, pos, (int)cnt, h->stream));
+      RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * n, h->stream));
+      rk::sp::sp_scatter_unique<<<h->num_sms * 8, 256, 0, h->stream>>>(keys2, flag, pos, cnt, base, h->csr_idx,
+                                                                        h->csr_val, counts, seed, (int)t);
+      rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)n, base, h->csr_ptr + t * (n + 1));
+      RK_CUDA(cudaGetLastError());
+      RK_CUDA(cudaMemcpyAsync(&ptr_host[t * (n + 1)], h->csr_ptr + t * (n + 1), sizeof(int64_t) * (n + 1),
+                              cudaMemcpyDeviceToHost, h->stream));
+      RK_CUDA(cudaStreamSynchronize(h->stream));
+      base = ptr_host[t * (n + 1) + n];
+    }
+    h->nnz = base;
+    dfree(keys);
+    dfree(keys2);
+    dfree(flag);
+    dfree(pos);
+    dfree(counts);
+    dfree(tmp);
+    build_csc(h, ptr_host);
+    rk::sp::sp_sq_norm<<<h->nnp, 256, 0, h->stream>>>(h->csr_val, h->nnz, h->npart);
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    std::vector<double> p(h->nnp);
+    RK_CUDA(cudaMemcpy(p.data(), h->npart, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
+    double s2 = 0.0;
+    for (double v : p) s2 += v;
+    h->norm2 = h->norm2_dev = h->norm2_orig = s2;
+    h->have_x = true;
+    h->perturbed = false;
+  });
+}
+
+int rk_csr_copy(rk_handle* h, int64_t* indptr, int32_t* indices, float* data) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaMemcpy(indptr, h->csr_ptr, sizeof(int64_t) * h->m * (h->n + 1), cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(indices, h->csr_idx, sizeof(int) * h->nnz, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(data, h->csr_val, sizeof(float) * h->nnz, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rk_nnz(rk_handle* h, int64_t* out) {
+  return guarded([&] { *out = h->nnz; });
+}
+
+int rk_csc_copy(rk_handle* h, int64_t* indptr, int32_t* indices, float* data) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaMemcpy(indptr, h->csc_ptr, sizeof(int64_t) * h->m * (h->n + 1), cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(indices, h->csc_idx, sizeof(int) * h->nnz, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(data, h->csc_val, sizeof(float) * h->nnz, cudaMemcpyDeviceToHost));
+  });
+}
+
 int rk_set_rank(rk_handle* h, int32_t k) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     RK_REQUIRE(1 <= k && k <= h->n && k <= 256, RK_ERR_DATA, "bad rank");
+    RK_REQUIRE(!h->sparse || k <= 32, RK_ERR_DATA, "sparse engine supports k <= 32");
     RK_CUDA(cudaSetDevice(h->dev));
     RK_CUDA(cudaStreamSynchronize(h->stream));
     free_factor_buffers(h);
@@ -1133,6 +1403,20 @@ int rk_residual(rk_handle* h, double* sq_residual, double* sq_norm) {
   return guarded([&] {
     check_ready(h);
     reset_ctl(h, 0, -1.0, 0);
+    if (h->sparse) {
+      // ||X - A R A^T||^2 = ||X||^2 - 2 sum <R_t, A^T X_t A> + sum <R_t, G R_t G>
+      launch_k1(h, false);
+      launch_k2a(h, 0);
+      launch_k2f(h, 1);
+      RK_CUDA(cudaStreamSynchronize(h->stream));
+      std::vector<double> tt(2 * h->m);
+      RK_CUDA(cudaMemcpy(tt.data(), h->tt, tt.size() * 8, cudaMemcpyDeviceToHost));
+      double res = h->norm2;
+      for (int64_t t = 0; t < h->m; ++t) res += -2.0 * tt[2 * t] + tt[2 * t + 1];
+      if (sq_residual) *sq_residual = std::max(res, 0.0);
+      if (sq_norm) *sq_norm = h->norm2;
+      return;
+    }
     launch_k5(h, 0);
     double* out = h->red;
     rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, h->nr, out);
@@ -1167,6 +1451,30 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
       h->norm2_dev0 = h->norm2_dev;
       h->norm2_orig = h->norm2;
     }
+    if (h->sparse) {
+      if (!h->csr_val0) {
+        h->csr_val0 = dalloc<float>(h->nnz);
+        h->csc_val0 = dalloc<float>(h->nnz);
+        RK_CUDA(cudaMemcpy(h->csr_val0, h->csr_val, h->nnz * 4, cudaMemcpyDeviceToDevice));
+        RK_CUDA(cudaMemcpy(h->csc_val0, h->csc_val, h->nnz * 4, cudaMemcpyDeviceToDevice));
+        h->norm2_orig = h->norm2;
+      }
+      rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+      rk::sp::sp_perturb<<<h->num_sms * 8, 256, 0, h->stream>>>(h->csr_ptr, h->csr_idx, h->csr_val0, h->csr_val,
+                                                                 (int)h->n, (int)h->m, 0, st, inc, delta, h->nnz);
+      rk::sp::sp_perturb<<<h->num_sms * 8, 256, 0, h->stream>>>(h->csc_ptr, h->csc_idx, h->csc_val0, h->csc_val,
+                                                                 (int)h->n, (int)h->m, 1, st, inc, delta, h->nnz);
+      RK_CUDA(cudaGetLastError());
+      rk::sp::sp_sq_norm<<<h->nnp, 256, 0, h->stream>>>(h->csr_val, h->nnz, h->npart);
+      RK_CUDA(cudaStreamSynchronize(h->stream));
+      std::vector<double> p(h->nnp);
+      RK_CUDA(cudaMemcpy(p.data(), h->npart, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
+      double s2 = 0.0;
+      for (double v : p) s2 += v;
+      h->norm2 = h->norm2_dev = s2;
+      h->perturbed = true;
+      return;
+    }
     rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
     RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
     rk::perturb_planes<<<h->nnp, rk::kThreads, 0, h->stream>>>(
@@ -1183,6 +1491,15 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
 int rk_restore(rk_handle* h) {
   return guarded([&] {
     check_ready(h);
+    if (h->sparse) {
+      if (h->csr_val0) {
+        RK_CUDA(cudaMemcpy(h->csr_val, h->csr_val0, h->nnz * 4, cudaMemcpyDeviceToDevice));
+        RK_CUDA(cudaMemcpy(h->csc_val, h->csc_val0, h->nnz * 4, cudaMemcpyDeviceToDevice));
+        h->norm2 = h->norm2_dev = h->norm2_orig;
+      }
+      h->perturbed = false;
+      return;
+    }
     if (h->Xh0) {
       const size_t count = (size_t)h->m * h->NR * h->NC;
       RK_CUDA(cudaMemcpyAsync(h->Xh, h->Xh0, count * 2, cudaMemcpyDeviceToDevice, h->stream));

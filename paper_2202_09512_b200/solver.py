@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _lib
 from .exceptions import DataError, NumericalError
-from .containers import dense_slices, tensor_dtype
+from .containers import dense_slices, is_sparse, tensor_dtype
 
 _SEED_TAG_A = 1
 _SEED_TAG_R = 2
@@ -113,6 +113,12 @@ def finalize_normalize(f: RescalFactors) -> RescalFactors:
 
 
 def _engine_for(x, k, cfg: SolverConfig):
+    """Device engine holding ``x``: the CSR/CSC engine for sparse tensors
+    (k <= 32), the dense tcgen05/SIMT engine otherwise."""
+    if is_sparse(x) and k <= 32:
+        eng = _lib.Engine(x.n, x.m, k, device=cfg.device, sparse=True)
+        eng.upload_csr(list(x.slices))
+        return eng
     eng = _lib.Engine(x.n, x.m, k, device=cfg.device, engine=cfg.engine)
     eng.upload(dense_slices(x))
     return eng
