@@ -1442,15 +1442,6 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
     check_ready(h);
     (void)col0;
     (void)col_map;
-    if (!h->Xh0) {
-      const size_t count = (size_t)h->m * h->NR * h->NC;
-      h->Xh0 = dalloc<__nv_bfloat16>(count);
-      h->Xl0 = dalloc<__nv_bfloat16>(count);
-      RK_CUDA(cudaMemcpyAsync(h->Xh0, h->Xh, count * 2, cudaMemcpyDeviceToDevice, h->stream));
-      RK_CUDA(cudaMemcpyAsync(h->Xl0, h->Xl, count * 2, cudaMemcpyDeviceToDevice, h->stream));
-      h->norm2_dev0 = h->norm2_dev;
-      h->norm2_orig = h->norm2;
-    }
     if (h->sparse) {
       if (!h->csr_val0) {
         h->csr_val0 = dalloc<float>(h->nnz);
@@ -1474,6 +1465,15 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
       h->norm2 = h->norm2_dev = s2;
       h->perturbed = true;
       return;
+    }
+    if (!h->Xh0) {
+      const size_t count = (size_t)h->m * h->NR * h->NC;
+      h->Xh0 = dalloc<__nv_bfloat16>(count);
+      h->Xl0 = dalloc<__nv_bfloat16>(count);
+      RK_CUDA(cudaMemcpyAsync(h->Xh0, h->Xh, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      RK_CUDA(cudaMemcpyAsync(h->Xl0, h->Xl, count * 2, cudaMemcpyDeviceToDevice, h->stream));
+      h->norm2_dev0 = h->norm2_dev;
+      h->norm2_orig = h->norm2;
     }
     rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
     RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
