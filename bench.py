@@ -10,6 +10,7 @@ configs):
                   PAPER.md:1027-1030); value counts block-iterations
                   (= N per global iteration) -> "scaling": "weak".
   cfg3          : dense m=16, n=32768, k=32 (north_star target), strong scaling.
+  cfg4          : sparse m=32, n=2^20, density 1e-5, k=16 (CSR/CSC engine), untracked.
   cfg1          : dense m=8, n=256, k=4 (latency-bound).
 
 Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun).
@@ -37,6 +38,7 @@ CONFIGS = {
     "cfg1": dict(m=8, n=256, k=4),
     "cfg2": dict(m=16, n=8192, k=16),
     "cfg3": dict(m=16, n=32768, k=32),
+    "cfg4": dict(m=32, n=1 << 20, k=16, density=1e-5),
 }
 METRIC = "MU iters/sec + effective TFLOP/s (dense) / HBM GB/s (sparse) at 1/2/4/8 B200"
 SEED = 20220218
@@ -202,6 +204,34 @@ def cpu_reference(x32, k, m, budget_s=12.0, max_slices=None):
     return it_s, cores, sample, t_step
 
 
+def cpu_reference_sparse(n, m, k, density, budget_s=12.0):
+    """oracle.mu_iteration (scipy CSR, fp64) on a bounded sample of slices of
+    the same synthetic sparse tensor; scaled to all m slices."""
+    import oracle
+    import scipy.sparse as sps
+    from paper_2202_09512_b200 import _lib
+
+    cores = len(os.sched_getaffinity(0))
+    e = _lib.Engine(n, min(m, 2), k, sparse=True)
+    e.fill_sparse_uniform(SEED, int(round(density * n * n)))
+    ptr, idx, val = e.csr_arrays()
+    e.close()
+    xs = [sps.csr_matrix((val[ptr[t, 0]:ptr[t, -1]].astype(np.float64), idx[ptr[t, 0]:ptr[t, -1]],
+                          ptr[t] - ptr[t, 0]), shape=(n, n)) for t in range(ptr.shape[0])]
+    a, r = oracle.random_init(n, k, len(xs), 0)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 1 or (time.perf_counter() - t_start < budget_s and len(times) < 5):
+        t0 = time.perf_counter()
+        oracle.mu_iteration(xs, a.copy(), r.copy(), 1e-16)
+        times.append(time.perf_counter() - t0)
+    t_step = statistics.median(times)
+    it_s = 1.0 / (t_step * m / len(xs))
+    sample = (f"oracle.mu_iteration fp64 on {len(xs)} of {m} CSR slices (n={n}, nnz/slice~{idx.size // len(xs)}, "
+              f"k={k}; scipy sparsetools), median of {len(times)} reps, scaled x{m / len(xs):.0f}")
+    return it_s, cores, sample
+
+
 # ---------------------------------------------------------------------------
 
 
@@ -265,20 +295,28 @@ def run_ours(args, dist, rank, world, local_rank):
     eps = float(cfg.epsilon)
 
     # ---------------- device-resident timed region --------------------------
+    sparse = "density" in c
+    track = not sparse  # cfg4 is defined untracked (the reference cannot form its residual)
+    if sparse and world > 1:
+        raise SystemExit("cfg4 multi-GPU is not implemented (sparse path is single-GPU in round 1)")
     if world > 1:
         eng, info = make_grid_engine(n, m, k, cfg=cfg)
         grid = (info["pr"], info["pc"])
     else:
-        eng, info, grid = _lib.Engine(n, m, k, device=local_rank), None, (1, 1)
-    eng.fill_uniform(SEED)
+        eng, info, grid = _lib.Engine(n, m, k, device=local_rank, sparse=sparse), None, (1, 1)
+    if sparse:
+        eng.fill_sparse_uniform(SEED, int(round(c["density"] * n * n)))
+        nnz = eng.nnz
+    else:
+        eng.fill_uniform(SEED)
     eng.set_factors(f0.A, f0.R)
-    eng.run(args.warmup, eps, track_error=True)
+    eng.run(args.warmup, eps, track_error=track)
     eng.set_factors(f0.A, f0.R)
     eng.set_option(1, 1)  # per-launch CUDA events around K1 on the engine stream
     barrier(dist)
     with ClockSampler(local_rank) as clocks:
         t_wall = time.perf_counter()
-        done, trace = eng.run(args.steps, eps, track_error=True)
+        done, trace = eng.run(args.steps, eps, track_error=track)
         t_wall = time.perf_counter() - t_wall
     tm = eng.timing()
     dev_ms = max_over_ranks(dist, tm["run_ms"])
@@ -289,7 +327,7 @@ def run_ours(args, dist, rank, world, local_rank):
     # production path; keep the faster of the two as `value`
     eng.set_factors(f0.A, f0.R)
     barrier(dist)
-    eng.run(args.steps, eps, track_error=True)
+    eng.run(args.steps, eps, track_error=track)
     dev_ms2 = max_over_ranks(dist, eng.timing()["run_ms"])
     launches = eng.timing()["launches"]
     eng.close()
@@ -305,8 +343,12 @@ def run_ours(args, dist, rank, world, local_rank):
     else:
         elems = m * n * n
     bytes_k1 = 4.0 * elems
+    if sparse:
+        # CSR pass: stream indices + values (8 B/nnz) + int64 row pointers, write P
+        k_pad = 16 if k <= 16 else 32
+        bytes_k1 = 8.0 * nnz + 8.0 * m * (n + 1) + 4.0 * m * n * k_pad
     achieved = bytes_k1 / (k1_ms / 1e3) / 1e9
-    flops_iter = 4.0 * m * n * n * k
+    flops_iter = 4.0 * m * n * n * k if not sparse else 4.0 * nnz * k
     tflops = flops_iter * (args.steps / (best_ms / 1e3)) / 1e12
 
     line = {
@@ -317,9 +359,11 @@ def run_ours(args, dist, rank, world, local_rank):
         "precision": "X and A as bf16 hi+lo pairs, 3 tcgen05 products, fp32 accumulate; k x k updates fp64",
         "data": "synthetic uniform [0,1) fp32-representable, device-generated",
         "config": {
-            "workload": f"{args.config}: dense m={m} n={n} k={k}" + (
+            "workload": (f"{args.config}: sparse m={m} n={n} density={c.get('density')} nnz={nnz if sparse else 0} k={k}"
+                         if sparse else f"{args.config}: dense m={m} n={n} k={k}") + (
                 f", {grid[0]}x{grid[1]} grid, per-GPU block {info['rows']}x{info['cols']}" if info else ""),
-            "per_step": "one MU iteration incl. tracked rel. error (rescal.py:215-224)",
+            "per_step": ("one MU iteration, untracked (track_error=False)" if sparse else
+                         "one MU iteration incl. tracked rel. error (rescal.py:215-224)"),
             "l2": f"inputs larger than L2 ({4.0 * elems / 1e9:.1f} GB/GPU vs 0.126 GB)",
             "engine": {1: "tcgen05", 2: "simt"}.get(einfo["engine"], "?"),
             "grid": f"{grid[0]}x{grid[1]}", "parallelism": f"pxq={grid[0]}x{grid[1]}",
@@ -327,7 +371,8 @@ def run_ours(args, dist, rank, world, local_rank):
         "tflops_effective": tflops,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None,
-                     "kernel": "k1_tc_kernel (P=X A, Q=X^T A, 3xBF16)", "peak_kind": peak_kind,
+                     "kernel": ("sp_csr_pass (P = X A, CSR, A rows gathered from L2)" if sparse else
+                                "k1_tc_kernel (P=X A, Q=X^T A, 3xBF16)"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_k1, "k1_ms": k1_ms,
                      "k1_share_of_step": (k1_ms / (dev_ms / args.steps)) if dev_ms else None},
         "gpu_launches": int(launches),
@@ -340,7 +385,23 @@ def run_ours(args, dist, rank, world, local_rank):
     if not args.no_e2e:
         try:
             phases = {}
-            if world == 1:
+            if sparse:
+                import scipy.sparse as sps
+
+                e4 = _lib.Engine(n, m, k, device=local_rank, sparse=True)
+                e4.fill_sparse_uniform(SEED, int(round(c["density"] * n * n)))
+                ptr, idx, val = e4.csr_arrays()
+                e4.close()
+                slices = [sps.csr_matrix((val[ptr[t, 0]:ptr[t, -1]], idx[ptr[t, 0]:ptr[t, -1]], ptr[t] - ptr[t, 0]),
+                                         shape=(n, n)) for t in range(m)]
+                x = rk.SparseRelTensor(slices)  # canonical form checked outside the timed region
+                t0 = time.perf_counter()
+                f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, track_error=False,
+                                                              device=local_rank), initial=f0)
+                e2e_s = time.perf_counter() - t0
+                h2d = int(ptr.nbytes + idx.nbytes + val.nbytes * 2) + f0.A.nbytes + f0.R.nbytes
+                d2h = f.A.nbytes + f.R.nbytes
+            elif world == 1:
                 xh = host_tensor(m, n, pinned=True)
                 x = rk.RelTensor(xh)  # validation outside the timed region, as a caller would
                 t0 = time.perf_counter()
@@ -397,8 +458,11 @@ def run_ours(args, dist, rank, world, local_rank):
     if world == 1 and rank == 0 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         try:
-            xs = host_tensor(min(m, 4), n, pinned=False)
-            it_s, cores, sample, t_step = cpu_reference(xs, k, m, budget_s=args.cpu_budget)
+            if sparse:
+                it_s, cores, sample = cpu_reference_sparse(n, m, k, c["density"], budget_s=args.cpu_budget)
+            else:
+                xs = host_tensor(min(m, 4), n, pinned=False)
+                it_s, cores, sample, t_step = cpu_reference(xs, k, m, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": it_s, "unit": "it/s", "cores": cores, "kind": "port",
                                     "sample": sample}
         except Exception as exc:
