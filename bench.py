@@ -355,16 +355,20 @@ def run_ours(args, dist, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak" if (args.config == "cfg2" and world > 1) else "strong",
-        "vs_baseline": None, "dtype": "bf16",
-        "precision": "X and A as bf16 hi+lo pairs, 3 tcgen05 products, fp32 accumulate; k x k updates fp64",
-        "data": "synthetic uniform [0,1) fp32-representable, device-generated",
+        "vs_baseline": None, "dtype": "f32" if sparse else "bf16",
+        "precision": ("CSR/CSC values and A in fp32, fp32 accumulate per nonzero row; k x k updates fp64"
+                      if sparse else
+                      "X and A as bf16 hi+lo pairs, 3 tcgen05 products, fp32 accumulate; k x k updates fp64"),
+        "data": ("synthetic uniform-random (i,j) pattern, values U(0,1], device-generated, canonical CSR"
+                 if sparse else "synthetic uniform [0,1) fp32-representable, device-generated"),
         "config": {
             "workload": (f"{args.config}: sparse m={m} n={n} density={c.get('density')} nnz={nnz if sparse else 0} k={k}"
                          if sparse else f"{args.config}: dense m={m} n={n} k={k}") + (
                 f", {grid[0]}x{grid[1]} grid, per-GPU block {info['rows']}x{info['cols']}" if info else ""),
             "per_step": ("one MU iteration, untracked (track_error=False)" if sparse else
                          "one MU iteration incl. tracked rel. error (rescal.py:215-224)"),
-            "l2": f"inputs larger than L2 ({4.0 * elems / 1e9:.1f} GB/GPU vs 0.126 GB)",
+            "l2": (f"inputs larger than L2 ({(8.0 * nnz * 2) / 1e9:.1f} GB CSR+CSC vs 0.126 GB)" if sparse else
+                   f"inputs larger than L2 ({4.0 * elems / 1e9:.1f} GB/GPU vs 0.126 GB)"),
             "engine": {1: "tcgen05", 2: "simt"}.get(einfo["engine"], "?"),
             "grid": f"{grid[0]}x{grid[1]}", "parallelism": f"pxq={grid[0]}x{grid[1]}",
         },
@@ -447,8 +451,10 @@ def run_ours(args, dist, rank, world, local_rank):
             line["e2e"] = {"value": units / e2e_s, "unit": "it/s",
                            "h2d_bytes_per_step": int(h2d / args.steps),
                            "d2h_bytes_per_step": int(d2h / args.steps),
-                           "api": "rescal_solve(RelTensor(pinned fp32 host X), k, SolverConfig(max_iters=steps))"
-                           if world == 1 else "Engine grid API: upload_block + run + get_factors",
+                           "api": ("rescal_solve(SparseRelTensor(host CSR), k, SolverConfig(max_iters=steps, "
+                                   "track_error=False))" if sparse else
+                                   "rescal_solve(RelTensor(pinned fp32 host X), k, SolverConfig(max_iters=steps))"
+                                   if world == 1 else "Engine grid API: upload_block + run + get_factors"),
                            "seconds": e2e_s, "phases": phases}
         except Exception as exc:  # report, never hide
             line["e2e"] = {"value": None, "unit": "it/s", "error": repr(exc)[:300],
