@@ -160,6 +160,19 @@ RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
 }
 
 // ------------------------------- the kernel --------------------------------
+// Operand merging: with MERGE_P the B operand of P is [A_hi ; A_lo] as ONE
+// N = 2K MMA (X_hi is read once for both), the accumulator is 2K columns wide
+// ([X_hi A_hi + X_lo A_hi | X_hi A_lo]) and the epilogue adds the halves.
+// MERGE_Q does the same for Q. Halves the X_hi shared-memory reads of the
+// MMA phase (the N = 16 MMAs are smem-read bound, not tensor bound).
+template <int K>
+struct K1Cfg {
+  static constexpr bool kMergeP = true;
+  static constexpr bool kMergeQ = (K == 16);
+  static constexpr int kPW = kMergeP ? 2 * K : K;  // TMEM columns per P buffer
+  static constexpr int kQW = kMergeQ ? 2 * K : K;  // TMEM columns per Q accumulator
+};
+
 template <int K>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -170,7 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
   // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
   static_assert(K == 16 || K == 32, "tcgen05 path supports k_pad 16 or 32");
+  constexpr bool kMergeP = K1Cfg<K>::kMergeP, kMergeQ = K1Cfg<K>::kMergeQ;
+  constexpr int kPW = K1Cfg<K>::kPW, kQW = K1Cfg<K>::kQW;
   constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
+  // A operand tiles hold the boxes as [hi b0][lo b0][hi b1][lo b1] so that
+  // the hi and lo rows of one 64-column K chunk are contiguous (N = 2K view)
   constexpr uint32_t kStageX = 4 * kXBox;          // Xh0 Xh1 Xl0 Xl1
   constexpr uint32_t kStageBytes = kStageX + 4 * kABox;
   constexpr uint32_t kAIBytes = 4 * kABox;
@@ -252,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t aib = smem_u32(&ai_full[ab]);
         mbar_expect_tx(aib, kAIBytes);
         tma_load_2d(ai + 0 * kABox, &map_rh, rb * kTile, 0, aib);
-        tma_load_2d(ai + 1 * kABox, &map_rh, rb * kTile + 64, 0, aib);
-        tma_load_2d(ai + 2 * kABox, &map_rl, rb * kTile, 0, aib);
+        tma_load_2d(ai + 1 * kABox, &map_rl, rb * kTile, 0, aib);
+        tma_load_2d(ai + 2 * kABox, &map_rh, rb * kTile + 64, 0, aib);
         tma_load_2d(ai + 3 * kABox, &map_rl, rb * kTile + 64, 0, aib);
         const int xrow = t * NR + rb * kTile;
         for (int cb = 0; cb < ct; ++cb) {
@@ -267,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(st + 2 * kXBox, &map_xl, j0, xrow, fb);
           tma_load_2d(st + 3 * kXBox, &map_xl, j0 + 64, xrow, fb);
           tma_load_2d(st + kStageX + 0 * kABox, &map_ch, j0, 0, fb);
-          tma_load_2d(st + kStageX + 1 * kABox, &map_ch, j0 + 64, 0, fb);
-          tma_load_2d(st + kStageX + 2 * kABox, &map_cl, j0, 0, fb);
+          tma_load_2d(st + kStageX + 1 * kABox, &map_cl, j0, 0, fb);
+          tma_load_2d(st + kStageX + 2 * kABox, &map_ch, j0 + 64, 0, fb);
           tma_load_2d(st + kStageX + 3 * kABox, &map_cl, j0 + 64, 0, fb);
           if (++stage == kStages) {
             stage = 0;
@@ -282,6 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t id_p = idesc_bf16(K, 0);  // A = X tile, K-major (K-dim = j)
       const uint32_t id_q = idesc_bf16(K, 1);  // A = X tile, MN-major (M = j, K-dim = i)
+      const uint32_t id_p2 = idesc_bf16(2 * K, 0);  // merged [hi ; lo] B operand
+      const uint32_t id_q2 = idesc_bf16(2 * K, 1);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t qe_phase = 0;
@@ -307,37 +326,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(&p_empty[pb]), pp ^ 1);
         tc_fence_after();
         const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
-        const uint32_t p_tmem = tmem + (uint32_t)(c * K + pb * K);
+        const uint32_t p_tmem = tmem + (uint32_t)(c * kQW + pb * kPW);
         for (int cb = 0; cb < ct; ++cb) {
           mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
           const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
           const uint32_t xh = st, xl = st + 2 * kXBox;
-          const uint32_t ajh = st + kStageX, ajl = st + kStageX + 2 * kABox;
-          const uint32_t q_tmem = tmem + (uint32_t)(cb * K);
+          const uint32_t aj = st + kStageX;
+          const uint32_t q_tmem = tmem + (uint32_t)(cb * kQW);
+          if (!(args.debug & 1)) {
 #pragma unroll
-          for (int ks = 0; ks < ((args.debug & 1) ? 0 : 8); ++ks) {
-            // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
-            const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
-            const uint32_t aoff = (ks >> 2) * kABox + (ks & 3) * 32;
-            const uint64_t dxh = umma_desc(xh + xoff, 16, 1024);
-            const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
-            const uint64_t dah = umma_desc(ajh + aoff, 16, 1024);
-            const uint64_t dal = umma_desc(ajl + aoff, 16, 1024);
-            const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
-            tc_mma(p_tmem, dxh, dah, id_p, accp);
-            tc_mma(p_tmem, dxh, dal, id_p, 1u);
-            tc_mma(p_tmem, dxl, dah, id_p, 1u);
-            // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
-            const uint32_t roff = ks * 16 * 128;
-            const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
-            const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
-            const uint64_t qah = umma_desc(ai + aoff, 16, 1024);
-            const uint64_t qal = umma_desc(ai + 2 * kABox + aoff, 16, 1024);
-            const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
-            tc_mma(q_tmem, qxh, qah, id_q, accq);
-            tc_mma(q_tmem, qxh, qal, id_q, 1u);
-            tc_mma(q_tmem, qxl, qah, id_q, 1u);
+            for (int ks = 0; ks < 8; ++ks) {
+              // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
+              const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
+              const uint32_t hoff = (ks >> 2) * 2 * kABox + (ks & 3) * 32;  // hi box of this chunk
+              const uint32_t loff = hoff + kABox;                            // lo box
+              const uint64_t dxh = umma_desc(xh + xoff, 16, 1024);
+              const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
+              const uint64_t dah = umma_desc(aj + hoff, 16, 1024);
+              const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
+              if (kMergeP) {
+                tc_mma(p_tmem, dxh, dah, id_p2, accp);  // [Xh Ah | Xh Al], N = 2K
+              } else {
+                tc_mma(p_tmem, dxh, dah, id_p, accp);
+                tc_mma(p_tmem, dxh, umma_desc(aj + loff, 16, 1024), id_p, 1u);
+              }
+              tc_mma(p_tmem, dxl, dah, id_p, 1u);  // Xl Ah into the first half
+              // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
+              const uint32_t roff = ks * 16 * 128;
+              const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
+              const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
+              const uint64_t qah = umma_desc(ai + hoff, 16, 1024);
+              const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
+              if (kMergeQ) {
+                tc_mma(q_tmem, qxh, qah, id_q2, accq);
+              } else {
+                tc_mma(q_tmem, qxh, qah, id_q, accq);
+                tc_mma(q_tmem, qxh, umma_desc(ai + loff, 16, 1024), id_q, 1u);
+              }
+              tc_mma(q_tmem, qxl, qah, id_q, 1u);
+            }
           }
           tc_commit(smem_u32(&empty[stage]));
           if (++stage == kStages) {
@@ -374,7 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       float v[K];
 #pragma unroll
       for (int h = 0; h < K / 16; ++h)
-        tmem_ld16(tmem + lane_base + (uint32_t)(c * K + pb * K + 16 * h), v + 16 * h);
+        tmem_ld16(tmem + lane_base + (uint32_t)(c * kQW + pb * kPW + 16 * h), v + 16 * h);
+      if (kMergeP) {
+        float v2[K];
+#pragma unroll
+        for (int h = 0; h < K / 16; ++h)
+          tmem_ld16(tmem + lane_base + (uint32_t)(c * kQW + pb * kPW + K + 16 * h), v2 + 16 * h);
+#pragma unroll
+        for (int d = 0; d < K; ++d) v[d] += v2[d];
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&p_empty[pb]));
@@ -391,7 +427,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           float w[K];
 #pragma unroll
           for (int h = 0; h < K / 16; ++h)
-            tmem_ld16(tmem + lane_base + (uint32_t)(cb * K + 16 * h), w + 16 * h);
+            tmem_ld16(tmem + lane_base + (uint32_t)(cb * kQW + 16 * h), w + 16 * h);
+          if (kMergeQ) {
+            float w2[K];
+#pragma unroll
+            for (int h = 0; h < K / 16; ++h)
+              tmem_ld16(tmem + lane_base + (uint32_t)(cb * kQW + K + 16 * h), w2 + 16 * h);
+#pragma unroll
+            for (int d = 0; d < K; ++d) w[d] += w2[d];
+          }
           float4* qd = reinterpret_cast<float4*>(qdst + ((size_t)cb * kTile + row) * K);
 #pragma unroll
           for (int h = 0; h < K / 4; ++h)

@@ -245,7 +245,9 @@ void free_factor_buffers(rk_handle* h) {
 void plan_tc(rk_handle* h) {
   const int K = h->K;
   const int nrb = (int)(h->NR / 128), ncb = (int)(h->NC / 128);
-  const int cmax = 512 / K - 2;
+  const int pw = K == 16 ? rk::tc::K1Cfg<16>::kPW : rk::tc::K1Cfg<32>::kPW;
+  const int qw = K == 16 ? rk::tc::K1Cfg<16>::kQW : rk::tc::K1Cfg<32>::kQW;
+  const int cmax = (512 - 2 * pw) / qw;  // TMEM columns: c Q accumulators + 2 P buffers
   int c = std::min(cmax, ncb);
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
