@@ -497,7 +497,9 @@ void launch_k5(rk_handle* h, int gate) {
 
 void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
-  if (h->fast) {
+  if (h->fast || (h->grid() && (K == 16 || K == 32))) {
+    const double* aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
+    const int nown = h->grid() ? (int)h->piece : (int)h->NR;
     const bool tc = h->engine == RK_ENGINE_TC;
     (void)tc;
     const float* src = h->P;  // P/Q already reduced (k1_reduce / SIMT K1)
@@ -507,11 +509,11 @@ void launch_k2a(rk_handle* h, int skip) {
     float* qout = nullptr;
     const dim3 grid(rk::kCluster, (unsigned)(h->m + 1));
     if (K == 16)
-      rk::k2a_v4<16><<<grid, 512, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
+      rk::k2a_v4<16><<<grid, 512, 0, h->stream>>>(h->ctl, h->Arow, aown, nown, src, nparts, stride, pout, h->Qpart,
                                                   h->d_slot_first, h->d_slot_count, h->c * 128,
                                                   h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
     else
-      rk::k2a_v4<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, src, nparts, stride, pout, h->Qpart,
+      rk::k2a_v4<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, aown, nown, src, nparts, stride, pout, h->Qpart,
                                                   h->d_slot_first, h->d_slot_count, h->c * 128,
                                                   h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
     RK_CUDA(cudaGetLastError());

@@ -403,6 +403,7 @@ constexpr int kCluster = 8;
 template <int K>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512 : 256)
     k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
+           const double* __restrict__ Aown, int Nown,
            const float* __restrict__ Pparts, int nparts, size_t part_stride,
            float* __restrict__ Pout, const float* __restrict__ Qpart,
            const int* __restrict__ slot_first, const int* __restrict__ slot_count, int W,
@@ -422,6 +423,11 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   const int rank = blockIdx.x;  // cluster rank (cluster spans gridDim.x)
   const int slot = blockIdx.y;
   const int t = slot - 1;
+  // slot 0 (G) runs over the rank's OWN piece of A (the whole A on one GPU)
+  if (slot == 0) {
+    A = Aown;
+    N = Nown;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int RB = (((N + kCluster - 1) / kCluster) + 127) / 128 * 128;
   const int WR = RB / kWarps;  // rows per warp (multiple of 8)
