@@ -351,6 +351,8 @@ void alloc_factor_buffers(rk_handle* h) {
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
   h->counters = dalloc<unsigned>((size_t)M + 8);
   h->fast = !h->grid() && (K == 16 || K == 32);
+  const bool grid_fast = h->grid() && (K == 16 || K == 32);
+  if (grid_fast) h->W32 = dalloc<float>((size_t)M * 2 * KK);
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
     const size_t wsm = (size_t)M * 2 * KK * sizeof(float);
@@ -398,6 +400,13 @@ void alloc_factor_buffers(rk_handle* h) {
                                  (int)rk::k2b_fused_smem(K, (int)M)));
   RK_CUDA(cudaFuncSetAttribute(rk::k2a_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * K * 8));
   if (K == 16 || K == 32) {
+    const int rbu = 2 * (256 / K);
+    const int tgu = rk::k2b_u4_tg(K, (int)M);
+    const int smu = tgu * (K * K + rbu * K) * (int)sizeof(float);
+    if (K == 16)
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
+    else
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
     const int rb = 2 * (256 / K);
     const int tg = rk::k2b_v4_tg(K, (int)M);
     const int smem = tg * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
@@ -548,7 +557,7 @@ void launch_k2f(rk_handle* h, int mode) {
   const int nres = h->grid() ? 1 : h->nr;
   rk::k2f_fused<<<(unsigned)h->m, rk::kThreads, k2f_smem(K), h->stream>>>(
       h->ctl, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K, (int)h->m,
-      h->eps, mode, h->gscratch, h->counters + h->m + 1, h->fast ? h->W32 : nullptr);
+      h->eps, mode, h->gscratch, h->counters + h->m + 1, h->W32);
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }
@@ -567,8 +576,10 @@ void launch_emit(rk_handle* h) {
 // Grid: gather the owned pieces into the row / col operand sets.
 void grid_allgather_a(rk_handle* h) {
   const size_t cnt = (size_t)h->piece * h->K;
+  RK_NCCL(ncclGroupStart());
   RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Arow, cnt, ncclDouble, h->rowc, h->stream));
   RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Acol, cnt, ncclDouble, h->colc, h->stream));
+  RK_NCCL(ncclGroupEnd());
 }
 
 void launch_k2b(rk_handle* h) {
@@ -632,18 +643,34 @@ void launch_k2b(rk_handle* h) {
     return;
   }
   const int rpb = 256 / K;
-  const size_t smem = (size_t)K * (K + 1) * 8 + rpb * K * 4;
-  rk::k2b_partial<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
-      h->ctl, h->P, h->R, (int)h->NR, K, (int)h->m, 1, h->UI);
-  rk::k2b_partial<<<(unsigned)((h->NC + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
-      h->ctl, h->Q, h->R, (int)h->NC, K, (int)h->m, 0, h->UJ);
+  if (h->W32) {
+    const int rb = 2 * (256 / K);
+    const int tg = rk::k2b_u4_tg(K, (int)h->m);
+    const size_t smem = (size_t)tg * (K * K + rb * K) * sizeof(float);
+    if (K == 16) {
+      rk::k2b_u4<16><<<(unsigned)((h->NR + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->P, h->W32, 0, (int)h->NR, (int)h->m, tg, h->UI);
+      rk::k2b_u4<16><<<(unsigned)((h->NC + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->Q, h->W32, 1, (int)h->NC, (int)h->m, tg, h->UJ);
+    } else {
+      rk::k2b_u4<32><<<(unsigned)((h->NR + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->P, h->W32, 0, (int)h->NR, (int)h->m, tg, h->UI);
+      rk::k2b_u4<32><<<(unsigned)((h->NC + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->Q, h->W32, 1, (int)h->NC, (int)h->m, tg, h->UJ);
+    }
+  } else {
+    const size_t smem = (size_t)K * (K + 1) * 8 + rpb * K * 4;
+    rk::k2b_partial<<<(unsigned)((h->NR + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
+        h->ctl, h->P, h->R, (int)h->NR, K, (int)h->m, 1, h->UI);
+    rk::k2b_partial<<<(unsigned)((h->NC + rpb - 1) / rpb), rk::kThreads, smem, h->stream>>>(
+        h->ctl, h->Q, h->R, (int)h->NC, K, (int)h->m, 0, h->UJ);
+  }
   RK_CUDA(cudaGetLastError());
   const size_t cnt = (size_t)h->piece * K;
-  // reduce-scatter in place: the own piece's sum lands at its slot
+  // reduce-scatter in place: the own piece's sum lands at its slot; the row
+  // and col collectives are independent -> one NCCL group
+  RK_NCCL(ncclGroupStart());
   RK_NCCL(ncclReduceScatter(h->UI, h->UI + (size_t)h->gj * cnt, cnt, ncclDouble, ncclSum, h->rowc,
                             h->stream));
   RK_NCCL(ncclReduceScatter(h->UJ, h->UJ + (size_t)h->gi * cnt, cnt, ncclDouble, ncclSum, h->colc,
                             h->stream));
+  RK_NCCL(ncclGroupEnd());
   rk::k2b_apply_own<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
       h->ctl, h->Arow + (size_t)h->gj * cnt, h->UI + (size_t)h->gj * cnt, h->UJ + (size_t)h->gi * cnt,
       h->Mm, (int)h->piece, K, eps_m);

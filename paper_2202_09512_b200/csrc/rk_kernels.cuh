@@ -665,6 +665,84 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
   }
 }
 
+// Grid numerator (K in {16, 32}): U[row] = sum_t PQ_t[row] W_t with W_t =
+// R_t^T (which = 0, P side) or R_t (which = 1, Q side), staged like k2b_v4.
+template <int K>
+__global__ void __launch_bounds__(256) k2b_u4(const Ctl* __restrict__ ctl,
+                                              const float* __restrict__ PQ,
+                                              const float* __restrict__ W32, int which, int N,
+                                              int M, int tg, double* __restrict__ U) {
+  static_assert(K == 16 || K == 32, "k2b_u4: K in {16, 32}");
+  if (ctl->stop) return;
+  extern __shared__ float shf[];
+  constexpr int TR = 256 / K;
+  constexpr int RB = 2 * TR;
+  constexpr int K4 = K / 4;
+  float* Ws = shf;                            // [tg][K][K]
+  float* Ps = shf + (size_t)tg * K * K;       // [tg][RB][K]
+  const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
+  const int rbase = blockIdx.x * RB;
+  const int i0 = rbase + rl, i1 = i0 + TR;
+  double n0 = 0.0, n1 = 0.0;
+  for (int tb = 0; tb < M; tb += tg) {
+    const int nt = min(tg, M - tb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * K * K / 4; e += blockDim.x) {
+      const int u = e / (K * K / 4), q = e - u * (K * K / 4);
+      reinterpret_cast<float4*>(Ws)[e] =
+          __ldg(reinterpret_cast<const float4*>(W32 + ((size_t)(tb + u) * 2 + which) * K * K) + q);
+    }
+    const int npq = nt * RB * K4;
+    for (int e0 = threadIdx.x; e0 < npq; e0 += 4 * blockDim.x) {
+      float4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * blockDim.x;
+        v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < npq) {
+          const int u = e / (RB * K4), rem = e - u * RB * K4, r = rem / K4, qq = rem - r * K4;
+          if (rbase + r < N)
+            v[q] = __ldg(reinterpret_cast<const float4*>(PQ + ((size_t)(tb + u) * N + rbase + r) * K) + qq);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * blockDim.x;
+        if (e < npq) reinterpret_cast<float4*>(Ps)[e] = v[q];
+      }
+    }
+    __syncthreads();
+    for (int u = 0; u < nt; ++u) {
+      const float* Wt = Ws + (size_t)u * K * K;  // [d][c]
+      const float* p0 = Ps + ((size_t)u * RB + rl) * K;
+      const float* p1 = p0 + TR * K;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int d4 = 0; d4 < K4; ++d4) {
+        const float4 a0 = *reinterpret_cast<const float4*>(p0 + 4 * d4);
+        const float4 a1 = *reinterpret_cast<const float4*>(p1 + 4 * d4);
+        const float pa[4] = {a0.x, a0.y, a0.z, a0.w}, pb[4] = {a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float w = Wt[(d4 * 4 + q) * K + c];
+          s0 = fmaf(pa[q], w, s0);
+          s1 = fmaf(pb[q], w, s1);
+        }
+      }
+      n0 += (double)s0;
+      n1 += (double)s1;
+    }
+  }
+  if (i0 < N) U[(size_t)i0 * K + c] = n0;
+  if (i1 < N) U[(size_t)i1 * K + c] = n1;
+}
+
+inline int k2b_u4_tg(int K, int M) {
+  const int RB = 2 * (256 / K);
+  const size_t per = (size_t)(K * K + RB * K) * sizeof(float);
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (48 * 1024) / per));
+}
+
 inline int k2b_v4_tg(int K, int M) {
   const int RB = 2 * (256 / K);
   const size_t per = (size_t)(2 * K * K + 2 * RB * K) * sizeof(float);
