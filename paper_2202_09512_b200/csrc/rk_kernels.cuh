@@ -417,7 +417,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
   constexpr int kWarps = K == 16 ? 16 : 8;
-  __shared__ __align__(16) float stage[kWarps][8][K];
+  __shared__ __align__(16) double stage[kWarps][8][K];   // P rows, converted once to fp64
   __shared__ __align__(16) double astage[kWarps][8][K];
   __shared__ double bpart[KK];
   const int rank = blockIdx.x;  // cluster rank (cluster spans gridDim.x)
@@ -480,18 +480,18 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
             *reinterpret_cast<float4*>(Qout + off) = w4;
           }
         }
-        *reinterpret_cast<float4*>(&stage[warp][r8][q * 4]) = v4;
+        double2* dst = reinterpret_cast<double2*>(&stage[warp][r8][q * 4]);
+        dst[0] = make_double2((double)v4.x, (double)v4.y);
+        dst[1] = make_double2((double)v4.z, (double)v4.w);
       }
       __syncwarp();
       for (int r8 = 0; r8 < nrow; ++r8) {
         const double a = astage[warp][r8][c];
 #pragma unroll
-        for (int q = 0; q < E; q += 4) {
-          const float4 p4 = *reinterpret_cast<const float4*>(&stage[warp][r8][d0 + q]);
-          acc[q] = fma(a, (double)p4.x, acc[q]);
-          acc[q + 1] = fma(a, (double)p4.y, acc[q + 1]);
-          acc[q + 2] = fma(a, (double)p4.z, acc[q + 2]);
-          acc[q + 3] = fma(a, (double)p4.w, acc[q + 3]);
+        for (int q = 0; q < E; q += 2) {
+          const double2 p2 = *reinterpret_cast<const double2*>(&stage[warp][r8][d0 + q]);
+          acc[q] = fma(a, p2.x, acc[q]);
+          acc[q + 1] = fma(a, p2.y, acc[q + 1]);
         }
       }
       __syncwarp();
