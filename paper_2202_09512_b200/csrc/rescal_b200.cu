@@ -355,24 +355,6 @@ void alloc_factor_buffers(rk_handle* h) {
   if (grid_fast) h->W32 = dalloc<float>((size_t)M * 2 * KK);
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
-    // keep the gathered factor rows L2-resident while CSR/CSC stream past
-    int max_persist = 0, max_window = 0;
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
-    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
-    const size_t abytes = (size_t)h->NR * K * sizeof(float);
-    if (max_persist > 0 && max_window > 0) {
-      const size_t want = std::min<size_t>(abytes, (size_t)max_persist);
-      RK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-      cudaStreamAttrValue av;
-      std::memset(&av, 0, sizeof(av));
-      av.accessPolicyWindow.base_ptr = h->A32row;
-      av.accessPolicyWindow.num_bytes = std::min<size_t>(abytes, (size_t)max_window);
-      av.accessPolicyWindow.hitRatio =
-          (float)std::min(1.0, (double)want / (double)av.accessPolicyWindow.num_bytes);
-      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      RK_CUDA(cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &av));
-    }
     const size_t wsm = (size_t)M * 2 * KK * sizeof(float);
     RK_REQUIRE(wsm <= 200 * 1024, RK_ERR_DATA, "sparse engine: m*k_pad^2 too large for the staged cores");
     if (K == 16)

@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
       float4 a[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        j[u] = __ldcs(idx + p + u);   // streamed once: evict-first
-        v[u] = __ldcs(val + p + u);
+        j[u] = __ldg(idx + p + u);
+        v[u] = __ldg(val + p + u);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) a[u] = __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j[u] * K) + q);
@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
       }
     }
     for (; p < e; ++p) {
-      const int j = __ldcs(idx + p);
-      const float v = __ldcs(val + p);
+      const int j = __ldg(idx + p);
+      const float v = __ldg(val + p);
       const float4 a = __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j * K) + q);
       y.x = fmaf(v, a.x, y.x);
       y.y = fmaf(v, a.y, y.y);
@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(256) sp_csc_numer(const Ctl* __restrict__ ctl,
         float4 a[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          ii[u] = __ldcs(idx + p + u);
-          v[u] = __ldcs(val + p + u);
+          ii[u] = __ldg(idx + p + u);
+          v[u] = __ldg(val + p + u);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(256) sp_csc_numer(const Ctl* __restrict__ ctl,
         }
       }
       for (; p < e; ++p) {
-        const int i = __ldcs(idx + p);
-        const float v = __ldcs(val + p);
+        const int i = __ldg(idx + p);
+        const float v = __ldg(val + p);
         const float4 a = __ldg(reinterpret_cast<const float4*>(A32 + (size_t)i * K) + q);
         z.x = fmaf(v, a.x, z.x);
         z.y = fmaf(v, a.y, z.y);
