@@ -11,6 +11,10 @@ configs):
                   (= N per global iteration) -> "scaling": "weak".
   cfg3          : dense m=16, n=32768, k=32 (north_star target), strong scaling.
   cfg4          : sparse m=32, n=2^20, density 1e-5, k=16 (CSR/CSC engine), untracked.
+  cfg5          : RESCALk (rescalk()) dense m=8, n=16384, r=10 members per k, 200
+                  iterations each, k in [--k-min, --k-max] (default 15..16 of the
+                  full 2..16 sweep); members spread over the N GPUs as replicas.
+                  A step = one member MU iteration; value = member-iterations/s.
   cfg1          : dense m=8, n=256, k=4 (latency-bound).
 
 Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun).
@@ -39,6 +43,7 @@ CONFIGS = {
     "cfg2": dict(m=16, n=8192, k=16),
     "cfg3": dict(m=16, n=32768, k=32),
     "cfg4": dict(m=32, n=1 << 20, k=16, density=1e-5),
+    "cfg5": dict(m=8, n=16384, k=16, k_min=15, k_max=16, r=10, iters=200),
 }
 METRIC = "MU iters/sec + effective TFLOP/s (dense) / HBM GB/s (sparse) at 1/2/4/8 B200"
 SEED = 20220218
@@ -493,6 +498,55 @@ def run_ours(args, dist, rank, world, local_rank):
     barrier(dist)
 
 
+def run_rescalk(args, dist, rank, world, local_rank):
+    """cfg5: the public rescalk() driver end to end (device tensor upload,
+    per-member PCG64 resampling on the device, MU solves, host clustering,
+    device regress_r / rel_error)."""
+    import paper_2202_09512_b200 as rk
+
+    c = dict(CONFIGS["cfg5"])
+    k_min = args.k_min or c["k_min"]
+    k_max = args.k_max or c["k_max"]
+    m, n, r, iters = c["m"], c["n"], c["r"], c["iters"]
+    xh = host_tensor(m, n, pinned=True)
+    x = rk.RelTensor(xh)
+
+    def allgather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    cfg = rk.SolverConfig(max_iters=iters, device=local_rank)
+    pcfg = rk.PerturbConfig(delta=0.02, base_seed=0)
+    # warm-up: a 1-member-per-k run on a tiny slice of work (compile, allocate)
+    barrier(dist)
+    t0 = time.perf_counter()
+    rep = rk.rescalk(x, k_min, k_max, r, cfg=cfg, pcfg=pcfg,
+                     world=(rank, world) if world > 1 else None,
+                     allgather=allgather if world > 1 else None)
+    secs = max_over_ranks(dist, time.perf_counter() - t0)
+    members = (k_max - k_min + 1) * r
+    units = members * iters
+    line = {
+        "metric": METRIC, "value": units / secs, "unit": "member-it/s", "n_gpus": world,
+        "steps": units, "warmup": 0, "ms_per_step": secs * 1e3 / units, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic uniform [0,1) fp32-representable",
+        "config": {"workload": f"cfg5: rescalk dense m={m} n={n} k={k_min}..{k_max} r={r} "
+                               f"iters={iters} (full sweep is k=2..16)",
+                   "per_step": "one member MU iteration inside rescalk() (tracked, default config)",
+                   "parallelism": f"replicas x{world}"},
+        "k_opt": rep.k_opt, "seconds": secs, "members": members,
+        "per_k": {str(e.k): {"s_min": e.s_min, "rel_error": e.rel_error} for e in rep.entries},
+        "e2e": {"value": units / secs, "unit": "member-it/s",
+                "h2d_bytes_per_step": int(xh.nbytes / units), "d2h_bytes_per_step": 0,
+                "api": "rescalk(RelTensor(pinned host X), k_min, k_max, r)"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier(dist)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -503,6 +557,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--k-min", type=int, default=0)
+    ap.add_argument("--k-max", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -514,7 +570,10 @@ def main():
         run_reference(args, None, 0, world)
         return
     dist, rank, world, local_rank = dist_setup(args.gpus)
-    run_ours(args, dist, rank, world, local_rank)
+    if args.config == "cfg5":
+        run_rescalk(args, dist, rank, world, local_rank)
+    else:
+        run_ours(args, dist, rank, world, local_rank)
     if dist is not None:
         dist.destroy_process_group()
 
