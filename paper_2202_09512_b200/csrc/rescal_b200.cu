@@ -1508,9 +1508,14 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
     }
     rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
     RK_CUDA(cudaMemsetAsync(h->npart2, 0, sizeof(double) * h->nnp, h->stream));
-    rk::perturb_planes<<<h->nnp, rk::kThreads, 0, h->stream>>>(
-        h->Xh0, h->Xl0, h->Xh, h->Xl, h->NR, h->NC, h->rows_valid, h->cols_valid, (int)h->m,
-        n_global, row0, h->d_colmap, st, inc, delta, 0, h->npart);
+    if (h->d_colmap == nullptr)
+      rk::perturb_rows<<<h->nnp, rk::kThreads, 0, h->stream>>>(
+          h->Xh0, h->Xl0, h->Xh, h->Xl, h->NR, h->NC, h->rows_valid, h->cols_valid, (int)h->m,
+          n_global, row0, st, inc, delta, h->npart);
+    else
+      rk::perturb_planes<<<h->nnp, rk::kThreads, 0, h->stream>>>(
+          h->Xh0, h->Xl0, h->Xh, h->Xl, h->NR, h->NC, h->rows_valid, h->cols_valid, (int)h->m,
+          n_global, row0, h->d_colmap, st, inc, delta, 0, h->npart);
     RK_CUDA(cudaGetLastError());
     finish_upload_norm(h, false);
     // the trace denominator of a resampled tensor is its own norm

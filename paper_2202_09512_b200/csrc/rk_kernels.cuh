@@ -1304,6 +1304,93 @@ RK_DEV double pcg_next_double(u128& state, u128 inc) {
   return (double)(out >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// LCG coefficients of a fixed jump of `delta` steps: state' = mult*state + plus.
+RK_DEV void pcg_jump_coeffs(u128 inc, uint64_t delta, u128& mult, u128& plus) {
+  u128 acc_mult{1ull, 0ull}, acc_plus{0ull, 0ull};
+  u128 cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1ull) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, u128{1ull, 0ull}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  mult = acc_mult;
+  plus = acc_plus;
+}
+
+RK_DEV double pcg_out_double(u128 state) {
+  uint64_t x = state.hi ^ state.lo;
+  unsigned rot = (unsigned)(state.hi >> 58);
+  uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
+  return (double)(out >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Coalesced resampling for whole-row tensors (single GPU): a warp owns a
+// 2048-element segment of one row; lane l draws elements base+64c+2l and +1.
+// Each lane jumps once per segment (log-time), then per 64-element chunk uses
+// the fixed 62-step coefficients: ~1.5 LCG steps per draw, and every load and
+// store is a coalesced bf16x2 access. Draws are bit-identical to the per-run
+// kernel (same element -> same PCG64 output).
+constexpr int kSeg = 2048;
+
+__global__ void __launch_bounds__(256) perturb_rows(
+    const __nv_bfloat16* __restrict__ Xh0, const __nv_bfloat16* __restrict__ Xl0,
+    __nv_bfloat16* __restrict__ Xh, __nv_bfloat16* __restrict__ Xl, int64_t NR, int64_t NC,
+    int64_t rows, int64_t cols, int M, int64_t n_global, int64_t row0, u128 state, u128 inc,
+    double delta, double* __restrict__ norm_part) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t segs = (cols + kSeg - 1) / kSeg;
+  const int64_t tasks = (int64_t)M * rows * segs;
+  u128 m62, p62, m1, p1;
+  pcg_jump_coeffs(inc, 62, m62, p62);
+  m1 = pcg_mult();
+  p1 = inc;
+  double acc = 0.0;
+  for (int64_t task = warp; task < tasks; task += nwarps) {
+    const int64_t t = task / (rows * segs);
+    const int64_t rem = task - t * rows * segs;
+    const int64_t il = rem / segs;
+    const int64_t j0 = (rem - il * segs) * kSeg;
+    const int64_t j1 = min(cols, j0 + kSeg);
+    const int64_t e0 = ((int64_t)t * n_global + row0 + il) * n_global + j0 + 2 * lane;
+    u128 s = pcg_advance(state, inc, (uint64_t)e0);  // state before draw e0
+    const size_t rowoff = ((size_t)t * NR + il) * NC;
+    for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
+      s = add128(mul128(s, m1), p1);
+      const double u0 = pcg_out_double(s);
+      s = add128(mul128(s, m1), p1);
+      const double u1 = pcg_out_double(s);
+      const size_t off = rowoff + j;
+      const bool two = j + 1 < j1;
+      // j is even and NC % 128 == 0: a bf16x2 access stays inside the row
+      const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(Xh0 + off);
+      const __nv_bfloat162 l0 = *reinterpret_cast<const __nv_bfloat162*>(Xl0 + off);
+      double x0 = (double)join_bf16(h0.x, l0.x) * (1.0 + delta * (2.0 * u0 - 1.0));
+      double x1 = two ? (double)join_bf16(h0.y, l0.y) * (1.0 + delta * (2.0 * u1 - 1.0))
+                      : (double)join_bf16(h0.y, l0.y);
+      __nv_bfloat16 a0, b0, a1, b1;
+      split_bf16(x0, a0, b0);
+      split_bf16(x1, a1, b1);
+      __nv_bfloat162 ho, lo;
+      ho.x = a0; ho.y = a1;
+      lo.x = b0; lo.y = b1;
+      *reinterpret_cast<__nv_bfloat162*>(Xh + off) = ho;
+      *reinterpret_cast<__nv_bfloat162*>(Xl + off) = lo;
+      const double w0 = (double)join_bf16(a0, b0), w1 = (double)join_bf16(a1, b1);
+      acc += w0 * w0 + (two ? w1 * w1 : 0.0);
+      s = add128(mul128(s, m62), p62);  // skip the other lanes' 62 draws
+    }
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) norm_part[blockIdx.x] = acc;
+}
+
 // Raw draws (tests): out[i] = u_{offset+i}.
 __global__ void pcg64_draws(u128 state, u128 inc, uint64_t offset, int64_t count, double* out) {
   const int64_t per = 64;

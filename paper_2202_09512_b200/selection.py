@@ -114,7 +114,7 @@ def custom_cluster(ens: FactorEnsemble, ctx=None, max_iters: int = 100) -> Clust
     converged, sweeps = False, 0
     for _ in range(max_iters):
         sweeps += 1
-        sim = np.einsum("nc,nlq->clq", medoid, aligned_hat)
+        sim = (medoid.T @ aligned_hat.reshape(aligned_hat.shape[0], k * r)).reshape(k, k, r)
         perms = [lsa(sim[:, :, q], mode="maximize") for q in range(r)]
         if all(np.array_equal(p, ident) for p in perms):
             converged = True
@@ -150,13 +150,13 @@ def cluster_stability(ens: FactorEnsemble, ctx=None) -> SilhouetteStats:
         raise DataError(f"need r >= 2 solutions, got {ens.r}")
     k, r = ens.k, ens.r
     hat = _unit_columns(ens.A_stack)
-    inner = np.einsum("nca,ncb->abc", hat, hat)  # (r, r, k) within-cluster
+    inner = np.stack([hat[:, c, :].T @ hat[:, c, :] for c in range(k)], axis=2)  # (r, r, k)
     i_mat = (1.0 - inner).mean(axis=1)
     if k == 1:
         return SilhouetteStats(i_mat, np.ones((r, 1)), np.ones((r, 1)), 1.0, 1.0, True)
     j_mat = np.empty((r, k))
     for c in range(k):
-        cross = np.einsum("na,nob->abo", hat[:, c, :], hat)  # (r, r, k)
+        cross = (hat[:, c, :].T @ hat.reshape(hat.shape[0], k * r)).reshape(r, k, r).transpose(0, 2, 1)
         y = (1.0 - cross).mean(axis=1)
         y[:, c] = np.inf
         j_mat[:, c] = y.min(axis=1)
