@@ -90,7 +90,7 @@ def _rank_main(rank, world, port, n, m, k, iters, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 13), (4, 10)])
+@pytest.mark.parametrize("world,n", [(2, 13), (4, 10), (8, 21)])
 def test_grid_schedule_matches_serial_oracle(world, n):
     m, k, iters = 2, 3, 25
     ctx = mp.get_context("spawn")
