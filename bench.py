@@ -269,7 +269,10 @@ def run_reference(args, dist, rank, world):
             oracle.mu_iteration(x, a.copy(), r[:ms].copy(), 1e-16)
         dt = time.perf_counter() - t0
         t_full = dt / args.steps * (m / ms)
-        value = 1.0 / t_full
+        # same units as our arm: at N>1 (cfg2 weak scaling) one global iteration
+        # counts as N cfg2-sized block-iterations
+        blocks = world if (args.config == "cfg2" and world > 1) else 1
+        value = blocks / t_full
         sample = (f"each step: oracle.mu_iteration fp64 untracked on {ms} of {m} slices "
                   f"(n={n}, k={k}); time scaled x{m / ms:.2f} to the full tensor")
         line = {
