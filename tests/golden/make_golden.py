@@ -143,6 +143,25 @@ def main():
         **{f"core_k{e.k}": e.core for e in rep.entries},
     )
 
+    # 14. the planted inputs of the reference's own tests (synth.generate), so
+    #     the device test bodies run on identical data
+    planted = {
+        "p16_4_3_s1_ped": dict(n=16, m=4, k_true=3, seed=1, noise=0.0, pedestal=0.15),
+        "p16_2_2_s3_ped": dict(n=16, m=2, k_true=2, seed=3, noise=0.0, pedestal=0.15),
+        "p16_3_3_s7_ped": dict(n=16, m=3, k_true=3, seed=7, noise=0.0, pedestal=0.15),
+        "p8_2_2_s9": dict(n=8, m=2, k_true=2, seed=9, noise=0.01),
+        "p12_2_2_s10": dict(n=12, m=2, k_true=2, seed=10, noise=0.01),
+    }
+    pl = {}
+    for key, spec in planted.items():
+        xt, at, rt = rk.generate(rk.SynthSpec(**spec))
+        pl[f"{key}_X"] = xt.slices
+    rep7 = rk.rescalk(rk.RelTensor(pl["p16_3_3_s7_ped_X"]), 3, 3, r=2, cfg=rk.SolverConfig(max_iters=600, seed=8),
+                      pcfg=rk.PerturbConfig(delta=0.01, base_seed=8))
+    pl["p16_3_3_s7_ped_rescalk_s_min"] = np.array(rep7.entries[0].s_min)
+    pl["p16_3_3_s7_ped_rescalk_rel_error"] = np.array(rep7.entries[0].rel_error)
+    out["planted_inputs"] = pl
+
     import numpy, scipy
     meta = dict(numpy=numpy.__version__, scipy=scipy.__version__, reference=REF)
     for name, d in out.items():

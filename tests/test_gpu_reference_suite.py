@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from conftest import golden
 
 pytestmark = pytest.mark.gpu
 rk = pytest.importorskip("paper_2202_09512_b200")
@@ -164,6 +165,9 @@ class TestRescalK:  # test_model_select.py:237-291
                          pcfg=rk.PerturbConfig(delta=0.01, base_seed=8))
         entry = rep.entries[0]
         assert entry.s_min >= 0.98
+        g = golden("planted_inputs")
+        assert abs(entry.s_min - float(g["p16_3_3_s7_ped_rescalk_s_min"])) <= 1e-4
+        assert abs(entry.rel_error - float(g["p16_3_3_s7_ped_rescalk_rel_error"])) <= 1e-5
 
     def test_k_above_n_rejected(self):
         x, _, _ = oracle_planted(8, 2, 2, seed=9)
@@ -180,15 +184,9 @@ class TestRescalK:  # test_model_select.py:237-291
 
 
 def oracle_planted(n, m, k, seed, noise=0.0, pedestal=0.15):
-    """Planted tensor in the style of synth.generate (exactly factorisable
-    bumps + pedestal), built with numpy here (synth is out of scope)."""
-    rng = np.random.default_rng(seed)
-    centers = (np.arange(k) + 0.5) / k
-    grid = (np.arange(n) + 0.5) / n
-    a = np.exp(-((grid[:, None] - centers[None, :]) ** 2) / (2 * (0.2 / k) ** 2))
-    a = a + pedestal * a.max()
-    r = rng.exponential(1.0, (m, k, k))
-    x0 = np.einsum("nk,mkl,jl->mnj", a, r, a)
-    if noise > 0:
-        x0 = x0 * (1.0 + noise * (2.0 * rng.random(x0.shape) - 1.0))
-    return rk.RelTensor(x0), a, r
+    """The reference's planted tensor (synth.generate, conftest.py:21-23),
+    from the golden fixture produced by the reference itself."""
+    key = {(16, 4, 3, 1): "p16_4_3_s1_ped", (16, 2, 2, 3): "p16_2_2_s3_ped",
+           (16, 3, 3, 7): "p16_3_3_s7_ped", (8, 2, 2, 9): "p8_2_2_s9",
+           (12, 2, 2, 10): "p12_2_2_s10"}[(n, m, k, seed)]
+    return rk.RelTensor(golden("planted_inputs")[f"{key}_X"]), None, None
