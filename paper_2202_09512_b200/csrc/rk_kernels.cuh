@@ -257,14 +257,25 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
     return;
   }
   int bad = 0;
-  for (int e = threadIdx.x; e < M * KK; e += blockDim.x) {
-    double v = __ldcg(Rnext + e);
-    if (!isfinite(v)) bad = 1;
-    R[e] = v;
-    if (W32) {
-      const int q = e / KK, rem = e - q * KK, a = rem / K, b = rem - a * K;
-      W32[(size_t)q * 2 * KK + b * K + a] = (float)v;       // R_t^T
-      W32[(size_t)q * 2 * KK + KK + a * K + b] = (float)v;  // R_t
+  // batches of 4 independent loads per thread before the dependent stores
+  for (int e0 = threadIdx.x; e0 < M * KK; e0 += 4 * blockDim.x) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < M * KK ? __ldcg(Rnext + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= M * KK) break;
+      if (!isfinite(v[u])) bad = 1;
+      R[e] = v[u];
+      if (W32) {
+        const int q = e / KK, rem = e - q * KK, a = rem / K, b = rem - a * K;
+        W32[(size_t)q * 2 * KK + b * K + a] = (float)v[u];       // R_t^T
+        W32[(size_t)q * 2 * KK + KK + a * K + b] = (float)v[u];  // R_t
+      }
     }
   }
   bad = __syncthreads_or(bad);
@@ -276,9 +287,15 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
     return;
   }
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < M; ++q) s += __ldcg(Mt + (size_t)q * KK + e);
-    Mout[e] = s;
+    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int q = 0;
+    for (; q + 8 <= M; q += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s8[u] += __ldcg(Mt + (size_t)(q + u) * KK + e);
+    }
+    double tail = 0.0;
+    for (; q < M; ++q) tail += __ldcg(Mt + (size_t)q * KK + e);
+    Mout[e] = (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]))) + tail;
   }
   if (threadIdx.x == 0) ctl->iter += 1;
 }
