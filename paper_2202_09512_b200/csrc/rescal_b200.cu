@@ -589,13 +589,13 @@ void launch_k2b(rk_handle* h) {
     const int grid = h->num_sms * 8;
     const size_t wsm = (size_t)h->m * 2 * K * K * sizeof(float);
     if (K == 16) {
-      rk::sp::sp_csc_numer<16><<<grid, 256, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
+      rk::sp::sp_csc_numer<16><<<grid / 2, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
                                                                h->A32row, h->P, h->W32, h->numer,
                                                                (int)h->n, (int)h->NR, (int)h->m);
       rk::sp::sp_apply_a<16><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,
                                                                     h->Mm, (int)h->n, eps_m);
     } else {
-      rk::sp::sp_csc_numer<32><<<grid, 256, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
+      rk::sp::sp_csc_numer<32><<<grid / 2, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
                                                                h->A32row, h->P, h->W32, h->numer,
                                                                (int)h->n, (int)h->NR, (int)h->m);
       rk::sp::sp_apply_a<32><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,

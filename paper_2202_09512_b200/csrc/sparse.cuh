@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
 // p = P_t[j]; lane q of the group owns output columns 4q..4q+3 and needs the
 // full p, z vectors: exchanged with group-local shuffles.
 template <int K>
-__global__ void __launch_bounds__(256) sp_csc_numer(const Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(512) sp_csc_numer(const Ctl* __restrict__ ctl,
                                                     const int64_t* __restrict__ ptr,
                                                     const int* __restrict__ idx,
                                                     const float* __restrict__ val,
@@ -107,11 +107,22 @@ __global__ void __launch_bounds__(256) sp_csc_numer(const Ctl* __restrict__ ctl,
     const int64_t j = jw + lane / G;
     const bool active = j < n;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // software pipeline over slices: next slice's column bounds and P row are
+    // loaded while the current slice's gathers are in flight
+    int64_t nb = 0, ne = 0;
+    float4 npv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (active) {
+      nb = ptr[j];
+      ne = ptr[j + 1];
+      npv = __ldg(reinterpret_cast<const float4*>(P + (size_t)j * K) + q);
+    }
     for (int t = 0; t < M; ++t) {
-      int64_t b = 0, e = 0;
-      if (active) {
-        b = ptr[(int64_t)t * (n + 1) + j];
-        e = ptr[(int64_t)t * (n + 1) + j + 1];
+      const int64_t b = nb, e = ne;
+      const float4 pv = npv;
+      if (active && t + 1 < M) {
+        nb = ptr[(int64_t)(t + 1) * (n + 1) + j];
+        ne = ptr[(int64_t)(t + 1) * (n + 1) + j + 1];
+        npv = __ldg(reinterpret_cast<const float4*>(P + ((size_t)(t + 1) * Npad + j) * K) + q);
       }
       float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       int64_t p = b;
@@ -144,8 +155,6 @@ __global__ void __launch_bounds__(256) sp_csc_numer(const Ctl* __restrict__ ctl,
         z.z = fmaf(v, a.z, z.z);
         z.w = fmaf(v, a.w, z.w);
       }
-      const float4 pv = active ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)t * Npad + j) * K) + q)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
       const float* WrT = shw + (size_t)t * 2 * K * K;  // [d][c] = R_t[c][d]
       const float* Wr = WrT + K * K;                   // [d][c] = R_t[d][c]
       float s[4] = {0.f, 0.f, 0.f, 0.f};
