@@ -400,6 +400,10 @@ void alloc_factor_buffers(rk_handle* h) {
                                  (int)rk::k2b_fused_smem(K, (int)M)));
   RK_CUDA(cudaFuncSetAttribute(rk::k2a_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * K * 8));
   if (K == 16 || K == 32) {
+    if (K == 16)
+      RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    else
+      RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int rbu = 2 * (256 / K);
     const int tgu = rk::k2b_u4_tg(K, (int)M);
     const int smu = tgu * (K * K + rbu * K) * (int)sizeof(float);
@@ -509,23 +513,26 @@ void launch_k2a(rk_handle* h, int skip) {
   if (h->fast || (h->grid() && (K == 16 || K == 32))) {
     const double* aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
-    const bool tc = h->engine == RK_ENGINE_TC;
-    (void)tc;
-    const float* src = h->P;  // P/Q already reduced (k1_reduce / SIMT K1)
-    const int nparts = 1;
-    const size_t stride = 0;
-    float* pout = nullptr;
-    float* qout = nullptr;
-    const dim3 grid(rk::kCluster, (unsigned)(h->m + 1));
+    // P/Q already reduced (k1_reduce / SIMT K1 / sparse CSR pass)
+    const int ncta = h->NR >= (1 << 17) ? 16 : 8;  // cluster size: more CTAs for large n
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncta, (unsigned)(h->m + 1));
+    cfg.blockDim = dim3(K == 16 ? 512 : 256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (K == 16)
-      rk::k2a_v4<16><<<grid, 512, 0, h->stream>>>(h->ctl, h->Arow, aown, nown, src, nparts, stride, pout, h->Qpart,
-                                                  h->d_slot_first, h->d_slot_count, h->c * 128,
-                                                  h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
+      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<16>, (const Ctl*)h->ctl, (const double*)h->Arow, aown, nown,
+                                 (const float*)h->P, (int)h->NR, (int)h->m, h->red, skip));
     else
-      rk::k2a_v4<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->Arow, aown, nown, src, nparts, stride, pout, h->Qpart,
-                                                  h->d_slot_first, h->d_slot_count, h->c * 128,
-                                                  h->nstrips, qout, (int)h->NR, (int)h->m, h->red, skip);
-    RK_CUDA(cudaGetLastError());
+      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<32>, (const Ctl*)h->ctl, (const double*)h->Arow, aown, nown,
+                                 (const float*)h->P, (int)h->NR, (int)h->m, h->red, skip));
     h->launches += 1;
     return;
   }

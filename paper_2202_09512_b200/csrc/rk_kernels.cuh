@@ -418,14 +418,11 @@ inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
 constexpr int kCluster = 8;
 
 template <int K>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512 : 256)
+__global__ void __launch_bounds__(K == 16 ? 512 : 256)
     k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
-           const double* __restrict__ Aown, int Nown,
-           const float* __restrict__ Pparts, int nparts, size_t part_stride,
-           float* __restrict__ Pout, const float* __restrict__ Qpart,
-           const int* __restrict__ slot_first, const int* __restrict__ slot_count, int W,
-           int nstrips, float* __restrict__ Qout, int N, int M, double* __restrict__ gs,
-           int skip_if_stopped) {
+           const double* __restrict__ Aown, int Nown, const float* __restrict__ P, int N, int M,
+           double* __restrict__ gs, int skip_if_stopped) {
+  // launched with a runtime cluster of gridDim.x CTAs (8, or 16 for large N)
   static_assert(K == 16 || K == 32, "k2a_v4: K in {16, 32}");
   if (skip_if_stopped && ctl->stop) return;
   namespace cg = cooperative_groups;
@@ -434,19 +431,21 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
   constexpr int kWarps = K == 16 ? 16 : 8;
+  constexpr int NP = (8 * K4 + 31) / 32;       // float4 P items per lane per 8-row batch
+  constexpr int NA = (8 * (K / 2) + 31) / 32;  // double2 A items per lane per batch
   __shared__ __align__(16) double stage[kWarps][8][K];   // P rows, converted once to fp64
   __shared__ __align__(16) double astage[kWarps][8][K];
   __shared__ double bpart[KK];
-  const int rank = blockIdx.x;  // cluster rank (cluster spans gridDim.x)
+  const int ncta = gridDim.x;
+  const int rank = blockIdx.x;
   const int slot = blockIdx.y;
   const int t = slot - 1;
-  // slot 0 (G) runs over the rank's OWN piece of A (the whole A on one GPU)
-  if (slot == 0) {
+  if (slot == 0) {  // G runs over the rank's OWN piece of A (the whole A on one GPU)
     A = Aown;
     N = Nown;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RB = (((N + kCluster - 1) / kCluster) + 127) / 128 * 128;
+  const int RB = (((N + ncta - 1) / ncta) + 8 * kWarps - 1) / (8 * kWarps) * (8 * kWarps);
   const int WR = RB / kWarps;  // rows per warp (multiple of 8)
   const int r_begin = rank * RB + warp * WR;
   const int r_end = min(N, r_begin + WR);
@@ -455,67 +454,65 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   double acc[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
+  // register prefetch of the next 8-row batch (A as double2, P as float4)
+  double2 pa[NA];
+  float4 pp[NP];
+  auto fetch = [&](int b0) {
+    const int nrow = min(8, r_end - b0);
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int item = lane + 32 * u;
+      const int r8 = item / (K / 2), q = item - r8 * (K / 2);
+      pa[u] = (item < 8 * (K / 2) && r8 < nrow)
+                  ? __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q)
+                  : make_double2(0.0, 0.0);
+    }
+    if (slot > 0) {
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        const int item = lane + 32 * u;
+        const int r8 = item / K4, q = item - r8 * K4;
+        pp[u] = (item < 8 * K4 && r8 < nrow)
+                    ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)t * N + b0 + r8) * K) + q)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  if (r_begin < r_end) fetch(r_begin);
   for (int b0 = r_begin; b0 < r_end; b0 += 8) {
     const int nrow = min(8, r_end - b0);
-    {
-      constexpr int NA = 8 * (K / 2) / 32;  // double2 items per lane (2 or 4)
-      double2 v[NA];
 #pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const int item = lane + 32 * u;
+    for (int u = 0; u < NA; ++u) {
+      const int item = lane + 32 * u;
+      if (item < 8 * (K / 2)) {
         const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-        v[u] = r8 < nrow ? __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q)
-                         : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const int item = lane + 32 * u;
-        const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-        *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = v[u];
+        *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = pa[u];
       }
     }
     if (slot > 0) {
-      for (int item = lane; item < 8 * K4; item += 32) {
-        const int r8 = item / K4, q = item - r8 * K4;
-        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r8 < nrow) {
-          const int i = b0 + r8;
-          const size_t off = ((size_t)t * N + i) * K + (size_t)q * 4;
-          for (int s = 0; s < nparts; ++s) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(Pparts + s * part_stride + off));
-            v4.x += v.x; v4.y += v.y; v4.z += v.z; v4.w += v.w;
-          }
-          if (Pout) *reinterpret_cast<float4*>(Pout + off) = v4;
-          if (Qout) {
-            const int sq = i / W, jl = i - sq * W;
-            const int f = slot_first[t * nstrips + sq], ns = slot_count[t * nstrips + sq];
-            float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int u = 0; u < ns; ++u) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(Qpart + ((size_t)(f + u) * W + jl) * K) + q);
-              w4.x += v.x; w4.y += v.y; w4.z += v.z; w4.w += v.w;
-            }
-            *reinterpret_cast<float4*>(Qout + off) = w4;
-          }
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        const int item = lane + 32 * u;
+        if (item < 8 * K4) {
+          const int r8 = item / K4, q = item - r8 * K4;
+          double2* dst = reinterpret_cast<double2*>(&stage[warp][r8][q * 4]);
+          dst[0] = make_double2((double)pp[u].x, (double)pp[u].y);
+          dst[1] = make_double2((double)pp[u].z, (double)pp[u].w);
         }
-        double2* dst = reinterpret_cast<double2*>(&stage[warp][r8][q * 4]);
-        dst[0] = make_double2((double)v4.x, (double)v4.y);
-        dst[1] = make_double2((double)v4.z, (double)v4.w);
       }
-      __syncwarp();
-      for (int r8 = 0; r8 < nrow; ++r8) {
-        const double a = astage[warp][r8][c];
+    }
+    __syncwarp();
+    if (b0 + 8 < r_end) fetch(b0 + 8);  // in flight while this batch computes
+    for (int r8 = 0; r8 < nrow; ++r8) {
+      const double a = astage[warp][r8][c];
+      if (slot > 0) {
 #pragma unroll
         for (int q = 0; q < E; q += 2) {
           const double2 p2 = *reinterpret_cast<const double2*>(&stage[warp][r8][d0 + q]);
           acc[q] = fma(a, p2.x, acc[q]);
           acc[q + 1] = fma(a, p2.y, acc[q + 1]);
         }
-      }
-      __syncwarp();
-    } else {
-      __syncwarp();
-      for (int r8 = 0; r8 < nrow; ++r8) {
-        const double a = astage[warp][r8][c];
+      } else {
 #pragma unroll
         for (int q = 0; q < E; ++q) acc[q] = fma(a, astage[warp][r8][d0 + q], acc[q]);
       }
@@ -537,8 +534,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(K == 16 ? 512
   if (rank == 0) {
     for (int e = threadIdx.x; e < KK; e += blockDim.x) {
       double v = 0.0;
-#pragma unroll
-      for (int r = 0; r < kCluster; ++r) v += cluster.map_shared_rank(bpart, r)[e];
+      for (int r = 0; r < ncta; ++r) v += cluster.map_shared_rank(bpart, r)[e];
       gs[(size_t)slot * KK + e] = v;
     }
   }
