@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -514,7 +515,11 @@ void launch_k2a(rk_handle* h, int skip) {
     const double* aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
     // P/Q already reduced (k1_reduce / SIMT K1 / sparse CSR pass)
-    const int ncta = h->NR >= (1 << 17) ? 16 : 8;  // cluster size: more CTAs for large n
+    static const int env_cluster = [] {
+      const char* e = std::getenv("RK_K2A_CLUSTER");  // experiments only
+      return e ? std::atoi(e) : 0;
+    }();
+    const int ncta = env_cluster ? env_cluster : (h->NR >= (1 << 17) ? 16 : 8);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncta, (unsigned)(h->m + 1));
     cfg.blockDim = dim3(K == 16 ? 512 : 256);
