@@ -401,10 +401,15 @@ void alloc_factor_buffers(rk_handle* h) {
                                  (int)rk::k2b_fused_smem(K, (int)M)));
   RK_CUDA(cudaFuncSetAttribute(rk::k2a_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * K * 8));
   if (K == 16 || K == 32) {
-    if (K == 16)
+    if (K == 16) {
       RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    else
+      RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::k2a_v4_smem(16)));
+    } else {
       RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      RK_CUDA(cudaFuncSetAttribute(rk::k2a_v4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::k2a_v4_smem(32)));
+    }
     const int rbu = 2 * (256 / K);
     const int tgu = rk::k2b_u4_tg(K, (int)M);
     const int smu = tgu * (K * K + rbu * K) * (int)sizeof(float);
@@ -519,11 +524,11 @@ void launch_k2a(rk_handle* h, int skip) {
       const char* e = std::getenv("RK_K2A_CLUSTER");  // experiments only
       return e ? std::atoi(e) : 0;
     }();
-    const int ncta = env_cluster ? env_cluster : (h->NR >= (1 << 17) ? 16 : 8);
+    const int ncta = env_cluster ? env_cluster : 8;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncta, (unsigned)(h->m + 1));
     cfg.blockDim = dim3(K == 16 ? 512 : 256);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = rk::k2a_v4_smem(K);
     cfg.stream = h->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

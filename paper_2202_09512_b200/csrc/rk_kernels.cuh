@@ -417,6 +417,8 @@ inline int k2b_fused_rows(int K) { return (kThreads / K) * kRB; }
 // orders throughout: deterministic, no atomics, no global partials.
 constexpr int kCluster = 8;
 
+constexpr int kBatchRows = 16;
+
 template <int K>
 __global__ void __launch_bounds__(K == 16 ? 512 : 256)
     k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
@@ -431,10 +433,12 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
   constexpr int kWarps = K == 16 ? 16 : 8;
-  constexpr int NP = (8 * K4 + 31) / 32;       // float4 P items per lane per 8-row batch
-  constexpr int NA = (8 * (K / 2) + 31) / 32;  // double2 A items per lane per batch
-  __shared__ __align__(16) double stage[kWarps][8][K];   // P rows, converted once to fp64
-  __shared__ __align__(16) double astage[kWarps][8][K];
+  constexpr int BR = kBatchRows;                // rows per warp batch
+  constexpr int NP = (BR * K4 + 31) / 32;       // float4 P items per lane per batch
+  constexpr int NA = (BR * (K / 2) + 31) / 32;  // double2 A items per lane per batch
+  extern __shared__ __align__(16) double dyn[];
+  double (*stage)[BR][K] = reinterpret_cast<double (*)[BR][K]>(dyn);                 // P rows (fp64)
+  double (*astage)[BR][K] = reinterpret_cast<double (*)[BR][K]>(dyn + kWarps * BR * K);
   __shared__ double bpart[KK];
   const int ncta = gridDim.x;
   const int rank = blockIdx.x;
@@ -445,8 +449,8 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
     N = Nown;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RB = (((N + ncta - 1) / ncta) + 8 * kWarps - 1) / (8 * kWarps) * (8 * kWarps);
-  const int WR = RB / kWarps;  // rows per warp (multiple of 8)
+  const int RB = (((N + ncta - 1) / ncta) + BR * kWarps - 1) / (BR * kWarps) * (BR * kWarps);
+  const int WR = RB / kWarps;  // rows per warp (multiple of BR)
   const int r_begin = rank * RB + warp * WR;
   const int r_end = min(N, r_begin + WR);
   const int c = (lane * E) / K;
@@ -454,16 +458,16 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
   double acc[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
-  // register prefetch of the next 8-row batch (A as double2, P as float4)
+  // register prefetch of the next batch (A as double2, P as float4)
   double2 pa[NA];
   float4 pp[NP];
   auto fetch = [&](int b0) {
-    const int nrow = min(8, r_end - b0);
+    const int nrow = min(BR, r_end - b0);
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
       const int item = lane + 32 * u;
       const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-      pa[u] = (item < 8 * (K / 2) && r8 < nrow)
+      pa[u] = (item < BR * (K / 2) && r8 < nrow)
                   ? __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q)
                   : make_double2(0.0, 0.0);
     }
@@ -472,19 +476,19 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
       for (int u = 0; u < NP; ++u) {
         const int item = lane + 32 * u;
         const int r8 = item / K4, q = item - r8 * K4;
-        pp[u] = (item < 8 * K4 && r8 < nrow)
+        pp[u] = (item < BR * K4 && r8 < nrow)
                     ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)t * N + b0 + r8) * K) + q)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   };
   if (r_begin < r_end) fetch(r_begin);
-  for (int b0 = r_begin; b0 < r_end; b0 += 8) {
-    const int nrow = min(8, r_end - b0);
+  for (int b0 = r_begin; b0 < r_end; b0 += BR) {
+    const int nrow = min(BR, r_end - b0);
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
       const int item = lane + 32 * u;
-      if (item < 8 * (K / 2)) {
+      if (item < BR * (K / 2)) {
         const int r8 = item / (K / 2), q = item - r8 * (K / 2);
         *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = pa[u];
       }
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
 #pragma unroll
       for (int u = 0; u < NP; ++u) {
         const int item = lane + 32 * u;
-        if (item < 8 * K4) {
+        if (item < BR * K4) {
           const int r8 = item / K4, q = item - r8 * K4;
           double2* dst = reinterpret_cast<double2*>(&stage[warp][r8][q * 4]);
           dst[0] = make_double2((double)pp[u].x, (double)pp[u].y);
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
       }
     }
     __syncwarp();
-    if (b0 + 8 < r_end) fetch(b0 + 8);  // in flight while this batch computes
+    if (b0 + BR < r_end) fetch(b0 + BR);  // in flight while this batch computes
     for (int r8 = 0; r8 < nrow; ++r8) {
       const double a = astage[warp][r8][c];
       if (slot > 0) {
@@ -539,6 +543,11 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
     }
   }
   cluster.sync();
+}
+
+inline size_t k2a_v4_smem(int K) {
+  const int warps = K == 16 ? 16 : 8;
+  return (size_t)2 * warps * kBatchRows * K * sizeof(double);
 }
 
 // k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
