@@ -517,7 +517,7 @@ void launch_k5(rk_handle* h, int gate) {
 void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
   if (h->fast || (h->grid() && (K == 16 || K == 32))) {
-    const double* aown = h->grid() ? h->Arow + (size_t)h->gj * h->piece * K : h->Arow;
+    const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : h->A32row;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
     // P/Q already reduced (k1_reduce / SIMT K1 / sparse CSR pass)
     static const int env_cluster = [] {
@@ -538,10 +538,10 @@ void launch_k2a(rk_handle* h, int skip) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (K == 16)
-      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<16>, (const Ctl*)h->ctl, (const double*)h->Arow, aown, nown,
+      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<16>, (const Ctl*)h->ctl, (const float*)h->A32row, aown, nown,
                                  (const float*)h->P, (int)h->NR, (int)h->m, h->red, skip));
     else
-      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<32>, (const Ctl*)h->ctl, (const double*)h->Arow, aown, nown,
+      RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2a_v4<32>, (const Ctl*)h->ctl, (const float*)h->A32row, aown, nown,
                                  (const float*)h->P, (int)h->NR, (int)h->m, h->red, skip));
     h->launches += 1;
     return;

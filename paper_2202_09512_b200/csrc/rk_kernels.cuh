@@ -420,11 +420,13 @@ constexpr int kCluster = 8;
 constexpr int kBatchRows = 16;
 
 template <int K>
-__global__ void __launch_bounds__(K == 16 ? 512 : 256)
-    k2a_v4(const Ctl* __restrict__ ctl, const double* __restrict__ A,
-           const double* __restrict__ Aown, int Nown, const float* __restrict__ P, int N, int M,
+__global__ void __launch_bounds__(K == 16 ? 512 : 256, 2)
+    k2a_v4(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+           const float* __restrict__ A32own, int Nown, const float* __restrict__ P, int N, int M,
            double* __restrict__ gs, int skip_if_stopped) {
-  // launched with a runtime cluster of gridDim.x CTAs (8, or 16 for large N)
+  // launched with a runtime cluster of gridDim.x CTAs. Each lane forms the
+  // products of a BR-row batch in fp32 (short chains: <= 16 terms) and adds
+  // the batch partial into fp64 accumulators.
   static_assert(K == 16 || K == 32, "k2a_v4: K in {16, 32}");
   if (skip_if_stopped && ctl->stop) return;
   namespace cg = cooperative_groups;
@@ -433,24 +435,25 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
   constexpr int K4 = K / 4;
   constexpr int E = KK / 32;
   constexpr int kWarps = K == 16 ? 16 : 8;
-  constexpr int BR = kBatchRows;                // rows per warp batch
-  constexpr int NP = (BR * K4 + 31) / 32;       // float4 P items per lane per batch
-  constexpr int NA = (BR * (K / 2) + 31) / 32;  // double2 A items per lane per batch
-  extern __shared__ __align__(16) double dyn[];
-  double (*stage)[BR][K] = reinterpret_cast<double (*)[BR][K]>(dyn);                 // P rows (fp64)
-  double (*astage)[BR][K] = reinterpret_cast<double (*)[BR][K]>(dyn + kWarps * BR * K);
+  constexpr int BR = kBatchRows;
+  constexpr int NI = (BR * K4 + 31) / 32;  // float4 items per lane per batch (A or P)
+  extern __shared__ __align__(16) float dynf[];
+  float (*pst)[BR][K] = reinterpret_cast<float (*)[BR][K]>(dynf);                 // P rows
+  float (*ast)[BR][K] = reinterpret_cast<float (*)[BR][K]>(dynf + kWarps * BR * K);  // A rows
   __shared__ double bpart[KK];
   const int ncta = gridDim.x;
   const int rank = blockIdx.x;
   const int slot = blockIdx.y;
   const int t = slot - 1;
+  const float* A = A32;
   if (slot == 0) {  // G runs over the rank's OWN piece of A (the whole A on one GPU)
-    A = Aown;
+    A = A32own;
     N = Nown;
   }
+  const float* B = slot == 0 ? A : P + (size_t)(slot == 0 ? 0 : t) * N * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int RB = (((N + ncta - 1) / ncta) + BR * kWarps - 1) / (BR * kWarps) * (BR * kWarps);
-  const int WR = RB / kWarps;  // rows per warp (multiple of BR)
+  const int WR = RB / kWarps;
   const int r_begin = rank * RB + warp * WR;
   const int r_end = min(N, r_begin + WR);
   const int c = (lane * E) / K;
@@ -458,69 +461,50 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
   double acc[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) acc[q] = 0.0;
-  // register prefetch of the next batch (A as double2, P as float4)
-  double2 pa[NA];
-  float4 pp[NP];
+  float4 pa[NI], pb[NI];
   auto fetch = [&](int b0) {
     const int nrow = min(BR, r_end - b0);
 #pragma unroll
-    for (int u = 0; u < NA; ++u) {
+    for (int u = 0; u < NI; ++u) {
       const int item = lane + 32 * u;
-      const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-      pa[u] = (item < BR * (K / 2) && r8 < nrow)
-                  ? __ldg(reinterpret_cast<const double2*>(A + (size_t)(b0 + r8) * K) + q)
-                  : make_double2(0.0, 0.0);
-    }
-    if (slot > 0) {
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int item = lane + 32 * u;
-        const int r8 = item / K4, q = item - r8 * K4;
-        pp[u] = (item < BR * K4 && r8 < nrow)
-                    ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)t * N + b0 + r8) * K) + q)
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      const int r8 = item / K4, q = item - r8 * K4;
+      const bool ok = item < BR * K4 && r8 < nrow;
+      pa[u] = ok ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(b0 + r8) * K) + q)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      pb[u] = ok ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(b0 + r8) * K) + q)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   if (r_begin < r_end) fetch(r_begin);
   for (int b0 = r_begin; b0 < r_end; b0 += BR) {
     const int nrow = min(BR, r_end - b0);
 #pragma unroll
-    for (int u = 0; u < NA; ++u) {
+    for (int u = 0; u < NI; ++u) {
       const int item = lane + 32 * u;
-      if (item < BR * (K / 2)) {
-        const int r8 = item / (K / 2), q = item - r8 * (K / 2);
-        *reinterpret_cast<double2*>(&astage[warp][r8][2 * q]) = pa[u];
-      }
-    }
-    if (slot > 0) {
-#pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int item = lane + 32 * u;
-        if (item < BR * K4) {
-          const int r8 = item / K4, q = item - r8 * K4;
-          double2* dst = reinterpret_cast<double2*>(&stage[warp][r8][q * 4]);
-          dst[0] = make_double2((double)pp[u].x, (double)pp[u].y);
-          dst[1] = make_double2((double)pp[u].z, (double)pp[u].w);
-        }
+      if (item < BR * K4) {
+        const int r8 = item / K4, q = item - r8 * K4;
+        *reinterpret_cast<float4*>(&ast[warp][r8][q * 4]) = pa[u];
+        *reinterpret_cast<float4*>(&pst[warp][r8][q * 4]) = pb[u];
       }
     }
     __syncwarp();
     if (b0 + BR < r_end) fetch(b0 + BR);  // in flight while this batch computes
+    float part[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) part[q] = 0.f;
     for (int r8 = 0; r8 < nrow; ++r8) {
-      const double a = astage[warp][r8][c];
-      if (slot > 0) {
+      const float a = ast[warp][r8][c];
 #pragma unroll
-        for (int q = 0; q < E; q += 2) {
-          const double2 p2 = *reinterpret_cast<const double2*>(&stage[warp][r8][d0 + q]);
-          acc[q] = fma(a, p2.x, acc[q]);
-          acc[q + 1] = fma(a, p2.y, acc[q + 1]);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < E; ++q) acc[q] = fma(a, astage[warp][r8][d0 + q], acc[q]);
+      for (int q = 0; q < E; q += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(&pst[warp][r8][d0 + q]);
+        part[q] = fmaf(a, p4.x, part[q]);
+        part[q + 1] = fmaf(a, p4.y, part[q + 1]);
+        part[q + 2] = fmaf(a, p4.z, part[q + 2]);
+        part[q + 3] = fmaf(a, p4.w, part[q + 3]);
       }
     }
+#pragma unroll
+    for (int q = 0; q < E; ++q) acc[q] += (double)part[q];
     __syncwarp();
   }
   // CTA partial: warps add in warp order (fixed, deterministic)
@@ -547,7 +531,7 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256)
 
 inline size_t k2a_v4_smem(int K) {
   const int warps = K == 16 ? 16 : 8;
-  return (size_t)2 * warps * kBatchRows * K * sizeof(double);
+  return (size_t)2 * warps * kBatchRows * K * sizeof(float);
 }
 
 // k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
