@@ -420,7 +420,7 @@ constexpr int kCluster = 8;
 constexpr int kBatchRows = 16;
 
 template <int K>
-__global__ void __launch_bounds__(K == 16 ? 512 : 256, 2)
+__global__ void __launch_bounds__(K == 16 ? 512 : 256, K == 16 ? 2 : 1)
     k2a_v4(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
            const float* __restrict__ A32own, int Nown, const float* __restrict__ P, int N, int M,
            double* __restrict__ gs, int skip_if_stopped) {
