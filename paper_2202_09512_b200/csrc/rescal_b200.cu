@@ -157,6 +157,7 @@ struct rk_handle {
   int chunk_rows = 64;
   unsigned* counters = nullptr;  // last-block tickets (self-resetting)
   int k1_debug = 0;              // K1 experiment switches (bench/profiling only)
+  bool skip_comm = false;        // experiments only: skip the per-iteration NCCL calls
   bool fast = false;             // single GPU, K in {16, 32}: k2a_v4 / k2b_v4 path
   float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v4
   int *d_simt_first = nullptr, *d_simt_count = nullptr;
@@ -562,7 +563,8 @@ void grid_allreduce_parts(rk_handle* h, bool with_resid) {
   const int K = h->K;
   const int len = (int)((h->m + 1) * K * K);
   rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, with_resid ? h->nr : 0, h->red + len);
-  RK_NCCL(ncclAllReduce(h->red, h->red, (size_t)len + 1, ncclDouble, ncclSum, h->world, h->stream));
+  if (!h->skip_comm)
+    RK_NCCL(ncclAllReduce(h->red, h->red, (size_t)len + 1, ncclDouble, ncclSum, h->world, h->stream));
   h->launches += 1;
 }
 
@@ -593,6 +595,7 @@ void launch_emit(rk_handle* h) {
 // Grid: gather the owned pieces into the row / col operand sets.
 void grid_allgather_a(rk_handle* h) {
   const size_t cnt = (size_t)h->piece * h->K;
+  if (h->skip_comm) return;
   RK_NCCL(ncclGroupStart());
   RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Arow, cnt, ncclDouble, h->rowc, h->stream));
   RK_NCCL(ncclAllGather(h->Arow + (size_t)h->gj * cnt, h->Acol, cnt, ncclDouble, h->colc, h->stream));
@@ -682,12 +685,14 @@ void launch_k2b(rk_handle* h) {
   const size_t cnt = (size_t)h->piece * K;
   // reduce-scatter in place: the own piece's sum lands at its slot; the row
   // and col collectives are independent -> one NCCL group
+  if (!h->skip_comm) {
   RK_NCCL(ncclGroupStart());
   RK_NCCL(ncclReduceScatter(h->UI, h->UI + (size_t)h->gj * cnt, cnt, ncclDouble, ncclSum, h->rowc,
                             h->stream));
   RK_NCCL(ncclReduceScatter(h->UJ, h->UJ + (size_t)h->gi * cnt, cnt, ncclDouble, ncclSum, h->colc,
                             h->stream));
   RK_NCCL(ncclGroupEnd());
+  }
   rk::k2b_apply_own<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
       h->ctl, h->Arow + (size_t)h->gj * cnt, h->UI + (size_t)h->gj * cnt, h->UJ + (size_t)h->gi * cnt,
       h->Mm, (int)h->piece, K, eps_m);
@@ -1179,6 +1184,7 @@ int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     if (key == 1) h->profile = value != 0;
     else if (key == 3) h->k1_debug = (int)value;
+    else if (key == 4) h->skip_comm = value != 0;
     else if (key == 2) {
       h->use_graph = value != 0;
       if (!h->use_graph && h->graph) {

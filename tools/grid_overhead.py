@@ -1,0 +1,33 @@
+"""Grid-iteration cost split (experiment; results with skipped comm are not
+valid factorizations): device ms/iteration with and without the NCCL calls."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import math
+import torch.distributed as dist
+import paper_2202_09512_b200 as rk
+from paper_2202_09512_b200.multigpu import make_grid_engine
+
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+n = int(round(8192 * math.sqrt(world)))
+m, k = 16, 16
+eng, info = make_grid_engine(n, m, k)
+eng.fill_uniform(1)
+f0 = rk.random_init(n, k, m, 0)
+out = {}
+for skip in (0, 1):
+    eng.set_option(4, skip)
+    eng.set_factors(f0.A, f0.R)
+    eng.run(5, 1e-16, False)
+    dist.barrier()
+    eng.set_factors(f0.A, f0.R)
+    eng.run(30, 1e-16, False)
+    out["skip_comm" if skip else "full"] = eng.timing()["run_ms"] / 30
+eng.set_option(4, 0)
+allv = [None] * world
+dist.all_gather_object(allv, out)
+if rank == 0:
+    print(json.dumps({"world": world, "n": n, "per_rank_ms_per_iter": allv}))
+eng.close()
+dist.destroy_process_group()
