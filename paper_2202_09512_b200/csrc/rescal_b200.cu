@@ -190,6 +190,11 @@ struct rk_handle {
   bool profile = false;
   cudaEvent_t ev_run0 = nullptr, ev_run1 = nullptr;
   std::vector<cudaEvent_t> ev_k1;
+  // per-phase timing (profile mode): events at phase boundaries of each iteration
+  static constexpr int kPhases = 6;
+  std::vector<cudaEvent_t> ev_ph;
+  int ph_iters = 0;
+  double ph_ms[kPhases] = {0, 0, 0, 0, 0, 0};
   double last_ms = 0.0, k1_ms_sum = 0.0;
   int k1_count = 0, launches = 0, iter_launches = 0;
   double eps = 1e-16;
@@ -693,6 +698,7 @@ void launch_k2b(rk_handle* h) {
                             h->stream));
   RK_NCCL(ncclGroupEnd());
   }
+  phase_mark(h, h->profile, 5);
   rk::k2b_apply_own<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
       h->ctl, h->Arow + (size_t)h->gj * cnt, h->UI + (size_t)h->gj * cnt, h->UJ + (size_t)h->gi * cnt,
       h->Mm, (int)h->piece, K, eps_m);
@@ -702,13 +708,32 @@ void launch_k2b(rk_handle* h) {
   h->launches += 3;
 }
 
+void phase_mark(rk_handle* h, bool timed, int idx) {
+  if (!timed) return;
+  const size_t i = (size_t)h->ph_iters * (rk_handle::kPhases + 1) + idx;
+  while (h->ev_ph.size() <= i) {
+    cudaEvent_t e;
+    RK_CUDA(cudaEventCreate(&e));
+    h->ev_ph.push_back(e);
+  }
+  RK_CUDA(cudaEventRecord(h->ev_ph[i], h->stream));
+}
+
+// phases: 0 K1(+reduce) | 1 K5+K2a | 2 grid all-reduce | 3 K2f | 4 K2b/numerator (+RS) | 5 A update/gather
 void enqueue_iteration(rk_handle* h, bool timed) {
+  phase_mark(h, timed, 0);
   launch_k1(h, timed);
+  phase_mark(h, timed, 1);
   launch_k5(h, 1);
   launch_k2a(h, 1);
+  phase_mark(h, timed, 2);
   if (h->grid()) grid_allreduce_parts(h, true);
+  phase_mark(h, timed, 3);
   launch_k2f(h, 0);
+  phase_mark(h, timed, 4);
   launch_k2b(h);
+  phase_mark(h, timed, 6);
+  if (timed) h->ph_iters += 1;
 }
 
 void enqueue_tail(rk_handle* h) {
@@ -984,6 +1009,7 @@ void rk_destroy(rk_handle* h) {
   if (h->ctl_host) cudaFreeHost(h->ctl_host);
   if (h->stop_host) cudaFreeHost(h->stop_host);
   for (auto e : h->ev_k1) cudaEventDestroy(e);
+  for (auto e : h->ev_ph) cudaEventDestroy(e);
   if (h->ev_run0) cudaEventDestroy(h->ev_run0);
   if (h->ev_run1) cudaEventDestroy(h->ev_run1);
   if (h->rowc) ncclCommDestroy(h->rowc);
@@ -1359,6 +1385,7 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     reset_ctl(h, track_error ? 1 : 0, tol, iters);
     h->k1_count = 0;
     h->launches = 0;
+    h->ph_iters = 0;
     const bool timed = h->profile;
     const bool graph = h->use_graph && !timed && !h->grid();
     if (graph && !h->graph) {
@@ -1405,6 +1432,18 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     float ms = 0.f;
     RK_CUDA(cudaEventElapsedTime(&ms, h->ev_run0, h->ev_run1));
     h->last_ms = ms;
+    for (int p = 0; p < rk_handle::kPhases; ++p) h->ph_ms[p] = 0.0;
+    for (int it = 0; it < h->ph_iters; ++it) {
+      cudaEvent_t* e = &h->ev_ph[(size_t)it * (rk_handle::kPhases + 1)];
+      for (int p = 0; p < rk_handle::kPhases; ++p) {
+        // phase 5 exists only on grids; on one GPU phase 4 runs to the end mark
+        const int a = p, b = (p == 4 && !h->grid()) ? 6 : p + 1;
+        if (p == 5 && !h->grid()) continue;
+        float ms = 0.f;
+        RK_CUDA(cudaEventElapsedTime(&ms, e[a], e[b == 5 && !h->grid() ? 6 : b]));
+        h->ph_ms[p] += ms;
+      }
+    }
     h->k1_ms_sum = 0.0;
     for (int i = 0; i < h->k1_count; ++i) {
       float e = 0.f;
@@ -1648,6 +1687,13 @@ int rk_last_timing(rk_handle* h, double* out, int32_t n_out) {
     double v[4] = {h->last_ms, h->k1_count ? h->k1_ms_sum / h->k1_count : 0.0, (double)h->k1_count,
                    (double)h->launches};
     for (int i = 0; i < n_out && i < 4; ++i) out[i] = v[i];
+  });
+}
+
+int rk_phase_timing(rk_handle* h, double* out, int32_t n_out) {
+  return guarded([&] {
+    for (int p = 0; p < n_out && p < rk_handle::kPhases; ++p)
+      out[p] = h->ph_iters ? h->ph_ms[p] / h->ph_iters : 0.0;
   });
 }
 
