@@ -71,6 +71,7 @@ SIGNATURES = {
     "rk_time_k1": (ctypes.c_int, [_vp, _i32, _pd]),
     "rk_trace_len": (ctypes.c_int, [_vp, _pi32]),
     "rk_restore": (ctypes.c_int, [_vp]),
+    "rk_phase_timing": (ctypes.c_int, [_vp, _pd, _i32]),
     "rk_block_uniform": (ctypes.c_int, [_vp, _u64, _pf]),
     "rk_csc_copy": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _pf]),
     "rk_csr_copy": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _pf]),
@@ -303,6 +304,14 @@ class Engine:
         out = np.zeros(4, dtype=np.float64)
         check(self._lib.rk_last_timing(self._h, _dp(out), 4))
         return {"run_ms": out[0], "k1_ms": out[1], "k1_launches": int(out[2]), "launches": int(out[3])}
+
+    def phase_timing(self):
+        """ms per iteration of each phase of the last profiled rk_run:
+        K1, K5+K2a, grid all-reduce, K2f, K2b/numerator(+RS), A update/gather."""
+        out = np.zeros(6, dtype=np.float64)
+        check(self._lib.rk_phase_timing(self._h, _dp(out), 6))
+        names = ["k1", "k2a", "allreduce", "k2f", "numer_rs", "apply_gather"]
+        return dict(zip(names, out.tolist()))
 
     def time_k1(self, reps=10):
         ms = _f64(0.0)

@@ -607,6 +607,8 @@ void grid_allgather_a(rk_handle* h) {
   RK_NCCL(ncclGroupEnd());
 }
 
+void phase_mark(rk_handle* h, bool timed, int idx);
+
 void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;

@@ -16,18 +16,21 @@ eng, info = make_grid_engine(n, m, k)
 eng.fill_uniform(1)
 f0 = rk.random_init(n, k, m, 0)
 out = {}
-for skip in (0, 1):
-    eng.set_option(4, skip)
-    eng.set_factors(f0.A, f0.R)
-    eng.run(5, 1e-16, False)
-    dist.barrier()
-    eng.set_factors(f0.A, f0.R)
-    eng.run(30, 1e-16, False)
-    out["skip_comm" if skip else "full"] = eng.timing()["run_ms"] / 30
-eng.set_option(4, 0)
+eng.set_factors(f0.A, f0.R)
+eng.run(5, 1e-16, False)
+dist.barrier()
+eng.set_factors(f0.A, f0.R)
+eng.set_option(1, 1)
+eng.run(30, 1e-16, False)
+out["profiled_ms_per_iter"] = eng.timing()["run_ms"] / 30
+out["phases"] = eng.phase_timing()
+eng.set_option(1, 0)
+eng.set_factors(f0.A, f0.R)
+eng.run(30, 1e-16, False)
+out["graph_or_direct_ms_per_iter"] = eng.timing()["run_ms"] / 30
 allv = [None] * world
 dist.all_gather_object(allv, out)
 if rank == 0:
-    print(json.dumps({"world": world, "n": n, "per_rank_ms_per_iter": allv}))
+    print(json.dumps({"world": world, "n": n, "per_rank": allv}))
 eng.close()
 dist.destroy_process_group()
