@@ -1389,7 +1389,8 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     h->launches = 0;
     h->ph_iters = 0;
     const bool timed = h->profile;
-    const bool graph = h->use_graph && !timed && !h->grid();
+    // NCCL collectives are stream-capturable: the grid iteration is a graph too
+    const bool graph = h->use_graph && !timed;
     if (graph && !h->graph) {
       cudaGraph_t g;
       RK_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
