@@ -308,10 +308,8 @@ def run_ours(args, dist, rank, world, local_rank):
     # untracked; the tracked rate (per-iteration relative error + one trace-only
     # tail pass per solve, rescal.py:218-222) is reported beside it.
     track = False
-    if sparse and world > 1:
-        raise SystemExit("cfg4 multi-GPU is not implemented (sparse path is single-GPU in round 1)")
     if world > 1:
-        eng, info = make_grid_engine(n, m, k, cfg=cfg)
+        eng, info = make_grid_engine(n, m, k, cfg=cfg, sparse=sparse)
         grid = (info["pr"], info["pc"])
     else:
         eng, info, grid = _lib.Engine(n, m, k, device=local_rank, sparse=sparse), None, (1, 1)
@@ -359,7 +357,7 @@ def run_ours(args, dist, rank, world, local_rank):
 
     # roofline of the dominant kernel (K1): algorithmic bytes = the local
     # block's X planes read once (hi+lo bf16 = 4 B per element)
-    if info is not None:
+    if info is not None and not sparse:
         elems = m * info["rows"] * info["cols"]
     else:
         elems = m * n * n
@@ -410,6 +408,8 @@ def run_ours(args, dist, rank, world, local_rank):
     if not args.no_e2e:
         try:
             phases = {}
+            if sparse and world > 1:
+                raise RuntimeError("sparse e2e at N>1 not measured (device-generated blocks only)")
             if sparse:
                 import scipy.sparse as sps
 

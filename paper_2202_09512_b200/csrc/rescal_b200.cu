@@ -456,11 +456,11 @@ void launch_k1(rk_handle* h, bool timed) {
   if (h->sparse) {
     const int grid = h->num_sms * 16;
     if (K == 16)
-      rk::sp::sp_csr_pass<16><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32row,
-                                                  h->P, (int)h->n, (int)h->NR, M, 1);
+      rk::sp::sp_csr_pass<16><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32col,
+                                                  h->P, (int)h->rows_valid, (int)h->NR, M, 1);
     else
-      rk::sp::sp_csr_pass<32><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32row,
-                                                  h->P, (int)h->n, (int)h->NR, M, 1);
+      rk::sp::sp_csr_pass<32><<<grid, 256, 0, s>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, h->A32col,
+                                                  h->P, (int)h->rows_valid, (int)h->NR, M, 1);
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
@@ -612,7 +612,7 @@ void phase_mark(rk_handle* h, bool timed, int idx);
 void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
-  if (h->sparse) {
+  if (h->sparse && !h->grid()) {
     const int grid = h->num_sms * 8;
     const size_t wsm = (size_t)h->m * 2 * K * K * sizeof(float);
     if (K == 16) {
@@ -670,7 +670,25 @@ void launch_k2b(rk_handle* h) {
     return;
   }
   const int rpb = 256 / K;
-  if (h->W32) {
+  if (h->sparse) {
+    // U_I = sum_t P_t R_t^T over the row set (dense P); U_J = sum_t z_t R_t with
+    // z_t = X_t^T A_row streamed from the block's CSC (no P part: P_t lives on
+    // the row set)
+    const int rb = 2 * (256 / K);
+    const int tg = rk::k2b_u4_tg(K, (int)h->m);
+    const size_t smem = (size_t)tg * (K * K + rb * K) * sizeof(float);
+    const size_t wsm = (size_t)h->m * 2 * K * K * sizeof(float);
+    const int grid = h->num_sms * 4;
+    if (K == 16) {
+      rk::k2b_u4<16><<<(unsigned)((h->NR + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->P, h->W32, 0, (int)h->NR, (int)h->m, tg, h->UI);
+      rk::sp::sp_csc_numer<16><<<grid, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
+                                                              nullptr, h->W32, h->UJ, (int)h->cols_valid, (int)h->NC, (int)h->m);
+    } else {
+      rk::k2b_u4<32><<<(unsigned)((h->NR + rb - 1) / rb), 256, smem, h->stream>>>(h->ctl, h->P, h->W32, 0, (int)h->NR, (int)h->m, tg, h->UI);
+      rk::sp::sp_csc_numer<32><<<grid, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
+                                                              nullptr, h->W32, h->UJ, (int)h->cols_valid, (int)h->NC, (int)h->m);
+    }
+  } else if (h->W32) {
     const int rb = 2 * (256 / K);
     const int tg = rk::k2b_u4_tg(K, (int)h->m);
     const size_t smem = (size_t)tg * (K * K + rb * K) * sizeof(float);
@@ -890,32 +908,33 @@ void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iter
 }  // namespace
 
 namespace {
-// Shared tail of the CSR uploads: build the CSC copy on the device.
+// Shared tail of the CSR uploads: build the CSC copy on the device. The
+// block has `rows` CSR rows and `cols` columns per slice.
 void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
-  const int64_t n = h->n, M = h->m;
+  const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
   int64_t max_nnz = 0;
   for (int64_t t = 0; t < M; ++t)
-    max_nnz = std::max(max_nnz, indptr_host[t * (n + 1) + n] - indptr_host[t * (n + 1)]);
+    max_nnz = std::max(max_nnz, indptr_host[t * (rows + 1) + rows] - indptr_host[t * (rows + 1)]);
   uint64_t* keys = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
   uint64_t* keys2 = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
-  int* counts = dalloc<int>((size_t)n);
+  int* counts = dalloc<int>((size_t)cols);
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, h->csr_val, h->csc_val,
                                   (int)std::max<int64_t>(1, max_nnz), 0, 64, h->stream);
   void* tmp = dalloc<uint8_t>(tmp_bytes + 16);
   for (int64_t t = 0; t < M; ++t) {
-    const int64_t base = indptr_host[t * (n + 1)], cnt = indptr_host[t * (n + 1) + n] - base;
-    RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * n, h->stream));
+    const int64_t base = indptr_host[t * (rows + 1)], cnt = indptr_host[t * (rows + 1) + rows] - base;
+    RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * cols, h->stream));
     if (cnt > 0) {
-      rk::sp::sp_make_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(h->csr_ptr + t * (n + 1), h->csr_idx,
-                                                                   (int)n, base, cnt, keys);
-      const int bits = 32 + (int)std::ceil(std::log2((double)std::max<int64_t>(2, n)));
+      rk::sp::sp_make_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(h->csr_ptr + t * (rows + 1), h->csr_idx,
+                                                                   (int)rows, base, cnt, keys);
+      const int bits = 32 + (int)std::ceil(std::log2((double)std::max<int64_t>(2, cols)));
       RK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, h->csr_val + base,
                                               h->csc_val + base, (int)cnt, 0, std::min(64, bits),
                                               h->stream));
       rk::sp::sp_split_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(keys2, cnt, h->csc_idx + base, counts);
     }
-    rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)n, base, h->csc_ptr + t * (n + 1));
+    rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)cols, base, h->csc_ptr + t * (cols + 1));
     RK_CUDA(cudaGetLastError());
   }
   RK_CUDA(cudaStreamSynchronize(h->stream));
@@ -923,6 +942,17 @@ void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
   dfree(keys2);
   dfree(counts);
   dfree(tmp);
+}
+
+// ||X||^2 over all ranks (the trace denominator is global)
+double global_sum(rk_handle* h, double v) {
+  if (!h->grid()) return v;
+  double* d = h->red;
+  RK_CUDA(cudaMemcpy(d, &v, sizeof(double), cudaMemcpyHostToDevice));
+  RK_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclSum, h->world, h->stream));
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  RK_CUDA(cudaMemcpy(&v, d, sizeof(double), cudaMemcpyDeviceToHost));
+  return v;
 }
 }  // namespace
 
@@ -1072,15 +1102,16 @@ int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, c
     RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "rk_upload_csr needs a sparse handle");
     RK_REQUIRE(indptr && (nnz == 0 || (indices && data)), RK_ERR_DATA, "null argument");
     RK_CUDA(cudaSetDevice(h->dev));
-    const int64_t n = h->n, M = h->m;
-    RK_REQUIRE(indptr[0] == 0 && indptr[M * (n + 1) - 1] == nnz, RK_ERR_DATA, "inconsistent indptr");
+    // the handle's (local) block: rows_valid CSR rows, cols_valid columns
+    const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
+    RK_REQUIRE(indptr[0] == 0 && indptr[M * (rows + 1) - 1] == nnz, RK_ERR_DATA, "inconsistent indptr");
     void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
                    h->csc_val0};
     for (void* p : old) dfree(p);
     h->csr_val0 = h->csc_val0 = nullptr;
     h->nnz = nnz;
-    h->csr_ptr = dalloc<int64_t>((size_t)M * (n + 1));
-    h->csc_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    h->csr_ptr = dalloc<int64_t>((size_t)M * (rows + 1));
+    h->csc_ptr = dalloc<int64_t>((size_t)M * (cols + 1));
     h->csr_idx = dalloc<int>((size_t)nnz);
     h->csc_idx = dalloc<int>((size_t)nnz);
     h->csr_val = dalloc<float>((size_t)nnz);
@@ -1092,62 +1123,76 @@ int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, c
       const double v = dtype == RK_F32 ? (double)static_cast<const float*>(data)[e]
                                        : static_cast<const double*>(data)[e];
       RK_REQUIRE(v >= 0.0, RK_ERR_DATA, "negative value in tensor");
+      RK_REQUIRE(indices[e] >= 0 && indices[e] < cols, RK_ERR_DATA, "column index out of range");
       s2 += v * v;
       v32[e] = (float)v;
     }
-    RK_CUDA(cudaMemcpy(h->csr_ptr, indptr, sizeof(int64_t) * M * (n + 1), cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(h->csr_ptr, indptr, sizeof(int64_t) * M * (rows + 1), cudaMemcpyHostToDevice));
     RK_CUDA(cudaMemcpy(h->csr_idx, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
     RK_CUDA(cudaMemcpy(h->csr_val, v32.data(), sizeof(float) * nnz, cudaMemcpyHostToDevice));
-    build_csc(h, std::vector<int64_t>(indptr, indptr + M * (n + 1)));
-    h->norm2 = h->norm2_dev = h->norm2_orig = s2;
+    build_csc(h, std::vector<int64_t>(indptr, indptr + M * (rows + 1)));
+    h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
     h->have_x = true;
     h->perturbed = false;
   });
 }
-
 
 int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_slice) {
   return guarded([&] {
     RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
     RK_CUDA(cudaSetDevice(h->dev));
     const int64_t n = h->n, M = h->m, cnt = nnz_target_per_slice;
+    const int64_t rows = h->rows_valid, cols = h->cols_valid;
+    const int64_t row0 = h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0;
     void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
                    h->csc_val0};
     for (void* p : old) dfree(p);
     h->csr_val0 = h->csc_val0 = nullptr;
-    const size_t cap = (size_t)M * cnt;
-    h->csr_ptr = dalloc<int64_t>((size_t)M * (n + 1));
-    h->csc_ptr = dalloc<int64_t>((size_t)M * (n + 1));
+    // a block holds ~ rows*cols/n^2 of the entries; leave slack
+    const double frac = h->grid() ? std::min(1.0, 1.25 * (double)rows * cols / ((double)n * n) + 0.01) : 1.0;
+    const size_t cap = (size_t)std::ceil((double)M * cnt * frac) + 1024;
+    h->csr_ptr = dalloc<int64_t>((size_t)M * (rows + 1));
+    h->csc_ptr = dalloc<int64_t>((size_t)M * (cols + 1));
     h->csr_idx = dalloc<int>(cap);
     h->csc_idx = dalloc<int>(cap);
     h->csr_val = dalloc<float>(cap);
     h->csc_val = dalloc<float>(cap);
+    int* col_local = nullptr;
+    if (h->grid()) {
+      std::vector<int> cl((size_t)n, -1);
+      for (size_t jl = 0; jl < h->colmap.size(); ++jl)
+        if (h->colmap[jl] < n) cl[h->colmap[jl]] = (int)jl;
+      col_local = dalloc<int>((size_t)n);
+      RK_CUDA(cudaMemcpy(col_local, cl.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    }
     uint64_t* keys = dalloc<uint64_t>(cnt);
     uint64_t* keys2 = dalloc<uint64_t>(cnt);
     int* flag = dalloc<int>(cnt);
     int* pos = dalloc<int>(cnt);
-    int* counts = dalloc<int>(n);
+    int* counts = dalloc<int>(rows);
     size_t t1 = 0, t2 = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, keys2, (int)cnt, 0, 64, h->stream);
     cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, pos, (int)cnt, h->stream);
     void* tmp = dalloc<uint8_t>(std::max(t1, t2) + 16);
     size_t tmp_bytes = std::max(t1, t2);
-    std::vector<int64_t> ptr_host((size_t)M * (n + 1));
+    std::vector<int64_t> ptr_host((size_t)M * (rows + 1));
     int64_t base = 0;
     for (int64_t t = 0; t < M; ++t) {
       rk::sp::sp_gen_keys<<<h->num_sms * 8, 256, 0, h->stream>>>(seed, (int)t, cnt, (int)n, keys);
       RK_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys2, (int)cnt, 0, 64, h->stream));
-      rk::sp::sp_mark_unique<<<h->num_sms * 8, 256, 0, h->stream>>>(keys2, cnt, flag);
+      rk::sp::sp_mark_unique_block<<<h->num_sms * 8, 256, 0, h->stream>>>(keys2, cnt, row0, rows, col_local, flag);
       RK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, pos, (int)cnt, h->stream));
-      RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * n, h->stream));
+      RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * rows, h->stream));
       rk::sp::sp_scatter_unique<<<h->num_sms * 8, 256, 0, h->stream>>>(keys2, flag, pos, cnt, base, h->csr_idx,
-                                                                        h->csr_val, counts, seed, (int)t);
-      rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)n, base, h->csr_ptr + t * (n + 1));
+                                                                        h->csr_val, counts, seed, (int)t,
+                                                                        row0, col_local);
+      rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)rows, base, h->csr_ptr + t * (rows + 1));
       RK_CUDA(cudaGetLastError());
-      RK_CUDA(cudaMemcpyAsync(&ptr_host[t * (n + 1)], h->csr_ptr + t * (n + 1), sizeof(int64_t) * (n + 1),
-                              cudaMemcpyDeviceToHost, h->stream));
+      RK_CUDA(cudaMemcpyAsync(&ptr_host[t * (rows + 1)], h->csr_ptr + t * (rows + 1),
+                              sizeof(int64_t) * (rows + 1), cudaMemcpyDeviceToHost, h->stream));
       RK_CUDA(cudaStreamSynchronize(h->stream));
-      base = ptr_host[t * (n + 1) + n];
+      base = ptr_host[t * (rows + 1) + rows];
+      RK_REQUIRE((size_t)base <= cap, RK_ERR_DEVICE, "sparse generator: block capacity exceeded");
     }
     h->nnz = base;
     dfree(keys);
@@ -1156,6 +1201,7 @@ int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_s
     dfree(pos);
     dfree(counts);
     dfree(tmp);
+    dfree(col_local);
     build_csc(h, ptr_host);
     rk::sp::sp_sq_norm<<<h->nnp, 256, 0, h->stream>>>(h->csr_val, h->nnz, h->npart);
     RK_CUDA(cudaStreamSynchronize(h->stream));
@@ -1163,7 +1209,7 @@ int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_s
     RK_CUDA(cudaMemcpy(p.data(), h->npart, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
     double s2 = 0.0;
     for (double v : p) s2 += v;
-    h->norm2 = h->norm2_dev = h->norm2_orig = s2;
+    h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
     h->have_x = true;
     h->perturbed = false;
   });
@@ -1173,7 +1219,7 @@ int rk_csr_copy(rk_handle* h, int64_t* indptr, int32_t* indices, float* data) {
   return guarded([&] {
     RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
     RK_CUDA(cudaSetDevice(h->dev));
-    RK_CUDA(cudaMemcpy(indptr, h->csr_ptr, sizeof(int64_t) * h->m * (h->n + 1), cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(indptr, h->csr_ptr, sizeof(int64_t) * h->m * (h->rows_valid + 1), cudaMemcpyDeviceToHost));
     RK_CUDA(cudaMemcpy(indices, h->csr_idx, sizeof(int) * h->nnz, cudaMemcpyDeviceToHost));
     RK_CUDA(cudaMemcpy(data, h->csr_val, sizeof(float) * h->nnz, cudaMemcpyDeviceToHost));
   });
@@ -1187,7 +1233,7 @@ int rk_csc_copy(rk_handle* h, int64_t* indptr, int32_t* indices, float* data) {
   return guarded([&] {
     RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "needs a sparse handle");
     RK_CUDA(cudaSetDevice(h->dev));
-    RK_CUDA(cudaMemcpy(indptr, h->csc_ptr, sizeof(int64_t) * h->m * (h->n + 1), cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(indptr, h->csc_ptr, sizeof(int64_t) * h->m * (h->cols_valid + 1), cudaMemcpyDeviceToHost));
     RK_CUDA(cudaMemcpy(indices, h->csc_idx, sizeof(int) * h->nnz, cudaMemcpyDeviceToHost));
     RK_CUDA(cudaMemcpy(data, h->csc_val, sizeof(float) * h->nnz, cudaMemcpyDeviceToHost));
   });
@@ -1503,6 +1549,7 @@ int rk_residual(rk_handle* h, double* sq_residual, double* sq_norm) {
       // ||X - A R A^T||^2 = ||X||^2 - 2 sum <R_t, A^T X_t A> + sum <R_t, G R_t G>
       launch_k1(h, false);
       launch_k2a(h, 0);
+      if (h->grid()) grid_allreduce_parts(h, false);
       launch_k2f(h, 1);
       RK_CUDA(cudaStreamSynchronize(h->stream));
       std::vector<double> tt(2 * h->m);
@@ -1547,10 +1594,13 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
         h->norm2_orig = h->norm2;
       }
       rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+      const int64_t prow0 = h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0;
       rk::sp::sp_perturb<<<h->num_sms * 8, 256, 0, h->stream>>>(h->csr_ptr, h->csr_idx, h->csr_val0, h->csr_val,
-                                                                 (int)h->n, (int)h->m, 0, st, inc, delta, h->nnz);
+                                                                 (int)h->rows_valid, (int)h->m, 0, st, inc, delta,
+                                                                 h->n, prow0, h->d_colmap);
       rk::sp::sp_perturb<<<h->num_sms * 8, 256, 0, h->stream>>>(h->csc_ptr, h->csc_idx, h->csc_val0, h->csc_val,
-                                                                 (int)h->n, (int)h->m, 1, st, inc, delta, h->nnz);
+                                                                 (int)h->cols_valid, (int)h->m, 1, st, inc, delta,
+                                                                 h->n, prow0, h->d_colmap);
       RK_CUDA(cudaGetLastError());
       rk::sp::sp_sq_norm<<<h->nnp, 256, 0, h->stream>>>(h->csr_val, h->nnz, h->npart);
       RK_CUDA(cudaStreamSynchronize(h->stream));
@@ -1558,7 +1608,7 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
       RK_CUDA(cudaMemcpy(p.data(), h->npart, sizeof(double) * h->nnp, cudaMemcpyDeviceToHost));
       double s2 = 0.0;
       for (double v : p) s2 += v;
-      h->norm2 = h->norm2_dev = s2;
+      h->norm2 = h->norm2_dev = global_sum(h, s2);
       h->perturbed = true;
       return;
     }

@@ -24,6 +24,8 @@
 namespace rk {
 namespace sp {
 
+// n = CSR rows of the (local) block; A32 = the gathered factor rows (the
+// block's column set); P row stride Npad.
 template <int K>
 __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
                                                    const int64_t* __restrict__ ptr,
@@ -80,7 +82,9 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
 // CSC pass fused with the A numerator. W32 = [R_t^T ; R_t] for all slices in
 // shared memory (fp32). Per (column j, slice t): z = X_t[:, j]^T A (gathered),
 // p = P_t[j]; lane q of the group owns output columns 4q..4q+3 and needs the
-// full p, z vectors: exchanged with group-local shuffles.
+// full p, z vectors: exchanged with group-local shuffles. With P == nullptr
+// (grid blocks, where the P and Q sides live on different row sets) only the
+// z R_t part is formed: U_J = sum_t z_t R_t. n = CSC columns of the block.
 template <int K>
 __global__ void __launch_bounds__(512) sp_csc_numer(const Ctl* __restrict__ ctl,
                                                     const int64_t* __restrict__ ptr,
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(512) sp_csc_numer(const Ctl* __restrict__ ctl,
     if (active) {
       nb = ptr[j];
       ne = ptr[j + 1];
-      npv = __ldg(reinterpret_cast<const float4*>(P + (size_t)j * K) + q);
+      if (P) npv = __ldg(reinterpret_cast<const float4*>(P + (size_t)j * K) + q);
     }
     for (int t = 0; t < M; ++t) {
       const int64_t b = nb, e = ne;
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(512) sp_csc_numer(const Ctl* __restrict__ ctl,
       if (active && t + 1 < M) {
         nb = ptr[(int64_t)(t + 1) * (n + 1) + j];
         ne = ptr[(int64_t)(t + 1) * (n + 1) + j + 1];
-        npv = __ldg(reinterpret_cast<const float4*>(P + ((size_t)(t + 1) * Npad + j) * K) + q);
+        if (P) npv = __ldg(reinterpret_cast<const float4*>(P + ((size_t)(t + 1) * Npad + j) * K) + q);
       }
       float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       int64_t p = b;
@@ -236,19 +240,22 @@ __global__ void __launch_bounds__(256) sp_apply_a(Ctl* __restrict__ ctl, double*
 __global__ void __launch_bounds__(256) sp_perturb(const int64_t* __restrict__ ptr,
                                                   const int* __restrict__ idx,
                                                   const float* __restrict__ val0,
-                                                  float* __restrict__ val, int n, int M,
+                                                  float* __restrict__ val, int nmajor, int M,
                                                   int col_major, u128 state, u128 inc,
-                                                  double delta, int64_t nnz_total) {
-  // one thread per (t, major index); entries of a major index are contiguous
-  const int64_t total = (int64_t)M * n;
+                                                  double delta, int64_t n_global, int64_t row0,
+                                                  const int64_t* __restrict__ colmap) {
+  // one thread per (t, major index); entries of a major index are contiguous.
+  // Local (row, col) -> global (row0 + row, colmap[col]) for grid blocks.
+  const int64_t total = (int64_t)M * nmajor;
   for (int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; task < total;
        task += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(task / n), a = (int)(task - (int64_t)t * n);
-    const int64_t b = ptr[(int64_t)t * (n + 1) + a], e = ptr[(int64_t)t * (n + 1) + a + 1];
+    const int t = (int)(task / nmajor), a = (int)(task - (int64_t)t * nmajor);
+    const int64_t b = ptr[(int64_t)t * (nmajor + 1) + a], e = ptr[(int64_t)t * (nmajor + 1) + a + 1];
     for (int64_t p = b; p < e; ++p) {
       const int o = idx[p];
-      const int64_t i = col_major ? o : a, j = col_major ? a : o;
-      const uint64_t el = (uint64_t)(((int64_t)t * n + i) * n + j);
+      const int64_t il = col_major ? o : a, jl = col_major ? a : o;
+      const int64_t i = row0 + il, j = colmap ? colmap[jl] : jl;
+      const uint64_t el = (uint64_t)(((int64_t)t * n_global + i) * n_global + j);
       u128 s = pcg_advance(state, inc, el);
       const double u = pcg_next_double(s, inc);
       const double f = 1.0 + delta * (2.0 * u - 1.0);
@@ -358,20 +365,37 @@ __global__ void sp_mark_unique(const uint64_t* __restrict__ keys, int64_t count,
 
 // flag -> exclusive positions (scan done with cub), scatter unique keys into
 // (indices, row counts) and draw the value of each unique entry.
+// flag[e] = 1 for the first copy of a key that lies in the (grid) block:
+// rows [row0, row0 + rows) and columns with col_local[j] >= 0 (all columns on
+// one GPU: col_local == nullptr).
+__global__ void sp_mark_unique_block(const uint64_t* __restrict__ keys, int64_t count, int64_t row0,
+                                     int64_t rows, const int* __restrict__ col_local,
+                                     int* __restrict__ flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    const int64_t i = (int64_t)(k >> 32), j = (int64_t)(k & 0xffffffffu);
+    const bool first = e == 0 || k != keys[e - 1];
+    const bool in = i >= row0 && i < row0 + rows && (!col_local || col_local[j] >= 0);
+    flag[e] = (first && in) ? 1 : 0;
+  }
+}
+
 __global__ void sp_scatter_unique(const uint64_t* __restrict__ keys, const int* __restrict__ flag,
                                   const int* __restrict__ pos, int64_t count, int64_t base,
                                   int* __restrict__ idx, float* __restrict__ val,
-                                  int* __restrict__ row_counts, uint64_t seed, int t) {
+                                  int* __restrict__ row_counts, uint64_t seed, int t, int64_t row0,
+                                  const int* __restrict__ col_local) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[e]) continue;
     const uint64_t k = keys[e];
     const int i = (int)(k >> 32), j = (int)(k & 0xffffffffu);
     const int64_t p = base + pos[e];
-    idx[p] = j;
+    idx[p] = col_local ? col_local[j] : j;
     const uint64_t r = splitmix64(seed ^ (k * 0xD1B54A32D192ED03ull) ^ ((uint64_t)t << 56));
     val[p] = 1.0f - (float)(r >> 40) * (1.0f / 16777216.0f);  // (0, 1]
-    atomicAdd(row_counts + i, 1);
+    atomicAdd(row_counts + (i - row0), 1);
   }
 }
 

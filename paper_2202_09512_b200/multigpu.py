@@ -23,7 +23,7 @@ import math
 import numpy as np
 
 from . import _lib
-from .containers import dense_slices, tensor_dtype
+from .containers import dense_slices, is_sparse, tensor_dtype
 from .exceptions import DataError, GridError
 from .solver import RescalFactors, SolverConfig, random_init
 
@@ -50,6 +50,26 @@ def block_of(x_dense: np.ndarray, n: int, info: dict) -> np.ndarray:
     return out
 
 
+def csr_block_of(slices, n: int, info: dict):
+    """This rank's CSR block of canonical CSR slices: rows row0 + [0, rows),
+    columns colmap (local column ids), canonical (sorted, no duplicates)."""
+    import scipy.sparse as sp
+
+    rows = np.arange(info["row0"], info["row0"] + info["rows"])
+    cols = np.asarray(info["colmap"])
+    rv = rows[rows < n]
+    cmask = cols < n
+    local_of = np.nonzero(cmask)[0]
+    out = []
+    for s in slices:
+        sub = sp.csr_matrix(s)[rv][:, cols[cmask]].tocoo()
+        blk = sp.csr_matrix((sub.data, (sub.row, local_of[sub.col])), shape=(info["rows"], info["cols"]))
+        blk.sum_duplicates()
+        blk.sort_indices()
+        out.append(blk)
+    return out
+
+
 def piece_layout(n: int, pr: int, pc: int, gi: int, gj: int) -> dict:
     """Host restatement of rk_grid_init's block geometry (for tests/tools)."""
     p = pr * pc
@@ -72,8 +92,9 @@ def _broadcast_id(dist, rank):
     return obj[0]
 
 
-def make_grid_engine(n, m, k, grid=None, cfg: SolverConfig | None = None):
-    """Create this rank's engine and join the NCCL grid."""
+def make_grid_engine(n, m, k, grid=None, cfg: SolverConfig | None = None, sparse=False):
+    """Create this rank's engine (dense, or the CSR/CSC engine) and join the
+    NCCL grid."""
     import torch.distributed as dist
 
     if not dist.is_initialized():
@@ -83,7 +104,7 @@ def make_grid_engine(n, m, k, grid=None, cfg: SolverConfig | None = None):
     pr, pc = grid if grid is not None else grid_shape(size)
     if pr * pc != size:
         raise GridError(f"{pr}x{pc} grid needs {pr * pc} ranks, have {size}")
-    eng = _lib.Engine(n, m, k, device=cfg.device, engine=cfg.engine)
+    eng = _lib.Engine(n, m, k, device=cfg.device, engine=cfg.engine, sparse=sparse)
     nid = _broadcast_id(dist, rank)
     eng.grid_init(pr, pc, rank, nid)
     return eng, eng.grid_block()
@@ -106,11 +127,15 @@ def solve_on_grid(x, k: int, cfg: SolverConfig | None = None, p: int | None = No
     f0 = initial.copy() if initial is not None else random_init(x.n, k, x.m, cfg.seed, dtype=dt)
     if f0.A.shape != (x.n, k) or f0.R.shape != (x.m, k, k):
         raise DataError("initial factors do not match tensor/k")
-    eng, info = make_grid_engine(x.n, x.m, k, grid, cfg)
+    sparse = is_sparse(x) and k <= 32
+    eng, info = make_grid_engine(x.n, x.m, k, grid, cfg, sparse=sparse)
     try:
-        xd = dense_slices(x)
-        sq = float(np.sum(np.asarray(xd, dtype=np.float64) ** 2))
-        eng.upload_block(block_of(xd, x.n, info), sq)
+        if sparse:
+            eng.upload_csr(csr_block_of(list(x.slices), x.n, info))
+        else:
+            xd = dense_slices(x)
+            sq = float(np.sum(np.asarray(xd, dtype=np.float64) ** 2))
+            eng.upload_block(block_of(xd, x.n, info), sq)
         eng.set_factors(f0.A.astype(dt).astype(np.float64), f0.R.astype(dt).astype(np.float64))
         _, trace = eng.run(cfg.max_iters, float(dt.type(cfg.epsilon)), cfg.track_error, cfg.tolerance)
         a, r = eng.get_factors()

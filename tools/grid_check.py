@@ -35,6 +35,30 @@ for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "aut
         ok = ok and good
         results.append(dict(n=n, m=m, k=k, iters=iters, engine=engine, grid=[info["pr"], info["pc"]],
                             relA=rel_a, relR=rel_r, dErr=derr, R_replicated=same_r, ok=good))
+# sparse CSR/CSC grid engine
+import scipy.sparse as sp
+for (n, m, k, dens, iters) in [(600, 2, 8, 0.02, 20), (1000, 3, 16, 0.01, 15), (555, 2, 32, 0.03, 10)]:
+    rng = np.random.default_rng(n + 7)
+    slices = []
+    for _ in range(m):
+        nnz = int(dens * n * n)
+        slices.append(sp.coo_matrix((rng.random(nnz) + 0.01, (rng.integers(0, n, nnz), rng.integers(0, n, nnz))),
+                                    shape=(n, n)))
+    xs = rk.SparseRelTensor(slices)
+    f0 = rk.random_init(n, k, m, 2)
+    f, tr, info = rk.solve_on_grid(xs, k, rk.SolverConfig(max_iters=iters), initial=f0)
+    rb = [None] * world
+    dist.all_gather_object(rb, f.R.tobytes())
+    if rank == 0:
+        ao, ro, tro = oracle.solve(list(xs.slices), k, oracle.OracleConfig(max_iters=iters), initial=(f0.A, f0.R))
+        rel_a = float(np.linalg.norm(f.A - ao) / np.linalg.norm(ao))
+        rel_r = float(np.linalg.norm(f.R - ro) / np.linalg.norm(ro))
+        derr = float(np.max(np.abs(tr - tro)))
+        same_r = len(set(rb)) == 1
+        good = rel_a <= 1e-4 and rel_r <= 1e-4 and derr <= 1e-5 and same_r and len(tr) == iters
+        ok = ok and good
+        results.append(dict(n=n, m=m, k=k, iters=iters, engine="sparse", grid=[info["pr"], info["pc"]],
+                            relA=rel_a, relR=rel_r, dErr=derr, R_replicated=same_r, ok=good))
 if rank == 0:
     print(json.dumps({"world": world, "ok": ok, "cases": results}))
 dist.destroy_process_group()
