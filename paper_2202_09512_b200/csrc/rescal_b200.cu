@@ -205,7 +205,10 @@ struct rk_handle {
   int64_t *csr_ptr = nullptr, *csc_ptr = nullptr;
   int *csr_idx = nullptr, *csc_idx = nullptr;
   float *csr_val = nullptr, *csc_val = nullptr, *csr_val0 = nullptr, *csc_val0 = nullptr;
-  double* numer = nullptr;  // [n][K] A numerator (sparse path)
+  double* numer = nullptr;  // [n][K] A numerator (sparse path, grid)
+  double* gpart = nullptr;  // sp_gram chunk partials [(M+1)][nchunk][K*K]
+  float4* wfrag = nullptr;  // per-lane TF32 hi/lo B fragments of [R_t^T ; R_t] (sparse, K = 16)
+  int gchunks = 0;
 
   bool grid() const { return pr * pc > 1; }
 };
@@ -224,6 +227,10 @@ void free_factor_buffers(rk_handle* h) {
   }
   dfree(h->numer);
   h->numer = nullptr;
+  dfree(h->gpart);
+  h->gpart = nullptr;
+  dfree(h->wfrag);
+  h->wfrag = nullptr;
   void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
                   h->part, h->red, h->gscratch, h->counters, h->W32, h->d_simt_first,
                   h->d_simt_count, h->UI, h->UJ, h->regS, h->regG, h->regT,
@@ -362,12 +369,32 @@ void alloc_factor_buffers(rk_handle* h) {
   if (grid_fast) h->W32 = dalloc<float>((size_t)M * 2 * KK);
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
+    h->gchunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (h->rows_valid + 2047) / 2048));
+    h->gpart = dalloc<double>((size_t)(M + 1) * h->gchunks * KK);
+    if (K == 16) {
+      h->wfrag = dalloc<float4>((size_t)M * 256);
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpNumTc::smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramCfg<16>::smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpNumCfg<16>::smem));
+    } else {
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramCfg<32>::smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpNumCfg<32>::smem));
+    }
     const size_t wsm = (size_t)M * 2 * KK * sizeof(float);
-    RK_REQUIRE(wsm <= 200 * 1024, RK_ERR_DATA, "sparse engine: m*k_pad^2 too large for the staged cores");
-    if (K == 16)
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-    else
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    // grid blocks keep the fused z-only CSC numerator (all W_t staged at once)
+    RK_REQUIRE(!h->grid() || wsm <= 200 * 1024, RK_ERR_DATA,
+               "sparse grid engine: m*k_pad^2 too large for the staged cores");
+    if (h->grid()) {
+      if (K == 16)
+        RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+      else
+        RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_csc_numer<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    }
   }
   if (h->fast) {
     h->W32 = dalloc<float>((size_t)M * 2 * KK);
@@ -522,6 +549,21 @@ void launch_k5(rk_handle* h, int gate) {
 
 void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
+  if (h->sparse && !h->grid()) {
+    // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram)
+    const int grid = h->num_sms * 3;
+    if (K == 16)
+      rk::sp::sp_gram<16><<<grid, 256, rk::sp::SpGramCfg<16>::smem, h->stream>>>(
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    else
+      rk::sp::sp_gram<32><<<grid, 256, rk::sp::SpGramCfg<32>::smem, h->stream>>>(
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
+                                                                        h->red, skip);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 2;
+    return;
+  }
   if (h->fast || (h->grid() && (K == 16 || K == 32))) {
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : h->A32row;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
@@ -613,20 +655,31 @@ void launch_k2b(rk_handle* h) {
   const int K = h->K;
   const double eps_m = h->eps * (double)h->m;
   if (h->sparse && !h->grid()) {
-    const int grid = h->num_sms * 8;
-    const size_t wsm = (size_t)h->m * 2 * K * K * sizeof(float);
+    // Q_t = X_t^T A from the CSC arrays (same gather kernel as the CSR pass),
+    // then the fused numerator + A update over the stored P and Q
+    const int grid = h->num_sms * 16;
+    const unsigned nb = (unsigned)h->num_sms * 2;  // persistent: two CTAs per SM
     if (K == 16) {
-      rk::sp::sp_csc_numer<16><<<grid / 2, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
-                                                               h->A32row, h->P, h->W32, h->numer,
-                                                               (int)h->n, (int)h->NR, (int)h->m);
-      rk::sp::sp_apply_a<16><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,
-                                                                    h->Mm, (int)h->n, eps_m);
+      rk::sp::sp_csr_pass<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
+                                                          h->Q, (int)h->cols_valid, (int)h->NC, (int)h->m, 1);
+      static const bool simt_numer = std::getenv("RK_SP_NUMER_SIMT") != nullptr;  // experiments only
+      if (simt_numer) {
+        rk::sp::sp_numer_apply<16><<<nb, 256, rk::sp::SpNumCfg<16>::smem, h->stream>>>(
+            h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->W32, h->Mm, (int)h->n, (int)h->m,
+            eps_m);
+      } else {
+        rk::sp::sp_wfrag<<<(unsigned)h->m, 256, 0, h->stream>>>(h->ctl, h->W32, h->wfrag, (int)h->m);
+        rk::sp::sp_numer_tc<<<(unsigned)h->num_sms, 256, rk::sp::SpNumTc::smem, h->stream>>>(
+            h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->wfrag, h->Mm, (int)h->n,
+            (int)h->m, eps_m);
+        h->launches += 1;
+      }
     } else {
-      rk::sp::sp_csc_numer<32><<<grid / 2, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
-                                                               h->A32row, h->P, h->W32, h->numer,
-                                                               (int)h->n, (int)h->NR, (int)h->m);
-      rk::sp::sp_apply_a<32><<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->Arow, h->A32row, h->numer,
-                                                                    h->Mm, (int)h->n, eps_m);
+      rk::sp::sp_csr_pass<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
+                                                          h->Q, (int)h->cols_valid, (int)h->NC, (int)h->m, 1);
+      rk::sp::sp_numer_apply<32><<<nb, 256, rk::sp::SpNumCfg<32>::smem, h->stream>>>(
+          h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->W32, h->Mm, (int)h->n, (int)h->m,
+          eps_m);
     }
     RK_CUDA(cudaGetLastError());
     h->launches += 2;

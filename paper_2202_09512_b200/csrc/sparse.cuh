@@ -19,15 +19,33 @@
 // chunk per lane (a coalesced K*4-byte A row per group).
 #pragma once
 
+#include "k1_tc.cuh"
 #include "rk_common.cuh"
 
 namespace rk {
 namespace sp {
 
-// n = CSR rows of the (local) block; A32 = the gathered factor rows (the
-// block's column set); P row stride Npad.
+RK_DEV uint32_t sp_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+RK_DEV void sp_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp_smem_u32(dst)), "l"(src) : "memory");
+}
+RK_DEV void sp_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+RK_DEV void sp_cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// SpMM pass Y_t = X_t B over the M slices of a CSR (or CSC) array set: one
+// lane group of G = K/4 lanes per row, K accumulators as one float4 per lane,
+// each stored entry gathers one K*4-byte row of B (coalesced across the group,
+// L2-resident). Used for P_t = X_t A (CSR, rows) and Q_t = X_t^T A (CSC,
+// columns). n = major dimension (rows of the block), ldy = row stride of Y.
+// The (slice, row) task index advances incrementally (no 64-bit division per
+// row); the gather loop keeps 4 independent loads in flight per lane.
 template <int K>
-__global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ctl,
                                                    const int64_t* __restrict__ ptr,
                                                    const int* __restrict__ idx,
                                                    const float* __restrict__ val,
@@ -39,12 +57,12 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
   const int lane = threadIdx.x & 31;
   const int q = lane % G;
   const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
-  const int64_t total = (int64_t)M * n;
-  for (int64_t task = group; task < total; task += ngroups) {
-    const int t = (int)(task / n);
-    const int i = (int)(task - (int64_t)t * n);
-    const int64_t b = ptr[(int64_t)t * (n + 1) + i], e = ptr[(int64_t)t * (n + 1) + i + 1];
+  const int ngroups = (int)(((int64_t)gridDim.x * blockDim.x) / G);
+  if (n <= 0) return;
+  int t = (int)(group / n), i = (int)(group - (int64_t)t * n);
+  for (; t < M;) {
+    const int64_t* pt = ptr + (size_t)t * (n + 1);
+    const int64_t b = pt[i], e = pt[i + 1];
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t p = b;
     for (; p + 4 <= e; p += 4) {
@@ -76,6 +94,508 @@ __global__ void __launch_bounds__(256) sp_csr_pass(const Ctl* __restrict__ ctl,
       y.w = fmaf(v, a.w, y.w);
     }
     reinterpret_cast<float4*>(P + ((size_t)t * Npad + i) * K)[q] = y;
+    i += ngroups;
+    while (i >= n) {
+      i -= n;
+      ++t;
+    }
+  }
+}
+
+// S_t = A^T P_t (slots 1..M) and G = A^T A (slot 0) for tall P (sparse path,
+// n up to 2^20+): a persistent grid walks (slot, row-chunk) items; each item
+// streams its chunk's A and P_t rows through a 4-stage cp.async ring in shared
+// memory; thread (c-block, d-block, row lane) forms a 4x4 block of the k x k
+// outer-product sum in fp32 over <= 16 rows, then adds into fp64. The row
+// lanes are summed in fixed order and each item writes one fp64 partial;
+// sp_gram_reduce sums the chunk partials in chunk order (deterministic, no
+// atomics). Replaces K2a (rk_kernels.cuh k2a_v4) on the sparse path, where
+// the cluster-per-slot layout cannot stream 2 GB of P at HBM rate.
+template <int K>
+struct SpGramCfg {
+  static constexpr int KB = K / 4;
+  static constexpr int NB = KB * KB;     // 4x4 blocks
+  static constexpr int RL = 256 / NB;    // row lanes
+  static constexpr int SR = K == 16 ? 128 : 64;  // rows per stage
+  static constexpr int RPT = SR / RL;            // rows per thread per stage (8 | 16)
+  static constexpr int NS = 4;           // stages
+  static constexpr size_t smem = (size_t)NS * SR * K * 2 * sizeof(float);
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) sp_gram(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+                                               const float* __restrict__ P, int n, int ldp, int M,
+                                               int nchunk, double* __restrict__ part,
+                                               int skip_if_stopped) {
+  using C = SpGramCfg<K>;
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ __align__(16) float gsm[];
+  float* As = gsm;
+  float* Bs = gsm + C::NS * C::SR * K;
+  const int tid = threadIdx.x;
+  const int sub = tid % C::NB, rl = tid / C::NB;
+  const int cb = sub / C::KB, db = sub % C::KB;
+  const int rows_per_chunk = (n + nchunk - 1) / nchunk;
+  const int nitems = (M + 1) * nchunk;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int slot = item / nchunk, chunk = item - slot * nchunk;
+    const float* B = slot == 0 ? A32 : P + (size_t)(slot - 1) * ldp * K;
+    const int r0 = chunk * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+    const int nst = r1 > r0 ? (r1 - r0 + C::SR - 1) / C::SR : 0;
+    auto issue = [&](int s) {
+      const int base = r0 + s * C::SR, nr = min(C::SR, r1 - base);
+      float* as = As + (s % C::NS) * C::SR * K;
+      float* bs = Bs + (s % C::NS) * C::SR * K;
+      for (int e = tid; e < nr * (K / 4); e += 256) {
+        sp_cp16(as + 4 * e, A32 + (size_t)base * K + 4 * e);
+        sp_cp16(bs + 4 * e, B + (size_t)base * K + 4 * e);
+      }
+    };
+    __syncthreads();  // previous item's buffers fully consumed
+#pragma unroll
+    for (int s = 0; s < C::NS - 1; ++s) {
+      if (s < nst) issue(s);
+      sp_cp_commit();
+    }
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+    float pacc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) pacc[u] = 0.f;
+    for (int s = 0; s < nst; ++s) {
+      if (s + C::NS - 1 < nst) issue(s + C::NS - 1);
+      sp_cp_commit();
+      sp_cp_wait<C::NS - 1>();
+      __syncthreads();
+      const int nr = min(C::SR, r1 - (r0 + s * C::SR));
+      const float* as = As + (s % C::NS) * C::SR * K;
+      const float* bs = Bs + (s % C::NS) * C::SR * K;
+      auto row = [&](int r) {
+        const float4 a = *reinterpret_cast<const float4*>(as + r * K + 4 * cb);
+        const float4 b = *reinterpret_cast<const float4*>(bs + r * K + 4 * db);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) pacc[x * 4 + y] = fmaf(av[x], bv[y], pacc[x * 4 + y]);
+      };
+      if (nr == C::SR) {
+#pragma unroll
+        for (int u = 0; u < C::RPT; ++u) row(rl + u * C::RL);
+      } else {
+        for (int r = rl; r < nr; r += C::RL) row(r);
+      }
+      // fp32 chains of <= 16 rows, then fp64
+      if (C::RPT >= 16 || (s & 1) || s == nst - 1) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          acc[u] += (double)pacc[u];
+          pacc[u] = 0.f;
+        }
+      }
+      __syncthreads();  // buffer s % NS is refilled by the next iteration
+    }
+    // row-lane reduction in fixed order through shared memory (reuses the ring)
+    double* red = reinterpret_cast<double*>(gsm);
+    sp_cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) red[(size_t)rl * (C::NB * 16) + sub * 16 + u] = acc[u];
+    __syncthreads();
+    for (int o = tid; o < K * K; o += 256) {
+      double v = 0.0;
+      for (int l = 0; l < C::RL; ++l) v += red[(size_t)l * (C::NB * 16) + o];
+      const int sb = o / 16, u = o % 16;
+      const int c = (sb / C::KB) * 4 + u / 4, d = (sb % C::KB) * 4 + u % 4;
+      part[((size_t)slot * nchunk + chunk) * K * K + c * K + d] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sp_gram_reduce(const Ctl* __restrict__ ctl,
+                                                      const double* __restrict__ part, int nchunk,
+                                                      int KK, double* __restrict__ gs,
+                                                      int skip_if_stopped) {
+  if (skip_if_stopped && ctl->stop) return;
+  const int slot = blockIdx.x;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < nchunk; ++c) v += part[((size_t)slot * nchunk + c) * KK + e];
+    gs[(size_t)slot * KK + e] = v;
+  }
+}
+
+// A update from the stored P_t = X_t A and Q_t = X_t^T A (sparse path):
+//   num_i = sum_t P_t[i] R_t^T + Q_t[i] R_t      (rescal.py:133-143)
+//   A_i <- A_i * num_i / (A_i M + m eps)         (rescal.py:144-145)
+// Persistent: one CTA per SM walks its row blocks; the flat sequence of
+// (row block, slice t) stages — the block's P_t / Q_t rows plus W_t =
+// [R_t^T ; R_t] (fp32, written by the K2f commit) — streams through a
+// cp.async ring in shared memory without draining between row blocks (P/Q
+// row stride padded to K+4 floats: conflict-free LDS.128). Thread = NRT rows
+// x 4 output columns; per slice the 2K-term products are formed in fp32 and
+// accumulated across slices in fp64 (as k2b_v4). A row block's update is
+// applied after its last slice; each CTA owns its rows, so the in-place A
+// update is race-free.
+template <int K>
+struct SpNumCfg {
+  static constexpr int NRT = 2;         // rows per thread
+  static constexpr int CB = K / 4;
+  static constexpr int RQ = 256 / CB;   // row lanes
+  static constexpr int RB = NRT * RQ;   // rows per block
+  static constexpr int LD = K + 4;      // padded smem row (floats)
+  static constexpr int NS = 4;          // ring stages
+  static constexpr int STAGE = 2 * RB * LD + 2 * K * K;  // floats per stage
+  static constexpr size_t smem = (size_t)NS * STAGE * sizeof(float) + (size_t)K * K * sizeof(double);
+};
+
+template <int K>
+__global__ void __launch_bounds__(256, 2) sp_numer_apply(Ctl* __restrict__ ctl, double* __restrict__ A64,
+                                                         float* __restrict__ A32,
+                                                         const float* __restrict__ P,
+                                                         const float* __restrict__ Q, int ldp, int ldq,
+                                                         const float* __restrict__ W32,
+                                                         const double* __restrict__ Mm, int n, int M,
+                                                         double eps_m) {
+  using C = SpNumCfg<K>;
+  if (ctl->stop) return;
+  extern __shared__ __align__(16) float nsm[];
+  double* Ms = reinterpret_cast<double*>(nsm + (size_t)C::NS * C::STAGE);
+  const int tid = threadIdx.x;
+  const int cb = tid % C::CB, rq = tid / C::CB;
+  const int nrb = (n + C::RB - 1) / C::RB;
+  const int my_rb = nrb > (int)blockIdx.x ? (nrb - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nstage = my_rb * M;
+  if (nstage == 0) return;
+  for (int e = tid; e < K * K; e += 256) Ms[e] = Mm[e];
+  auto issue = [&](int f) {
+    const int t = f % M, row0 = ((int)blockIdx.x + (f / M) * (int)gridDim.x) * C::RB;
+    const int nr = min(C::RB, n - row0);
+    float* ps = nsm + (size_t)(f % C::NS) * C::STAGE;
+    float* qs = ps + C::RB * C::LD;
+    float* ws = qs + C::RB * C::LD;
+    const float* pg = P + ((size_t)t * ldp + row0) * K;
+    const float* qg = Q + ((size_t)t * ldq + row0) * K;
+    for (int e = tid; e < nr * (K / 4); e += 256) {
+      const int r = e / (K / 4), c4 = e % (K / 4);
+      sp_cp16(ps + r * C::LD + 4 * c4, pg + (size_t)r * K + 4 * c4);
+      sp_cp16(qs + r * C::LD + 4 * c4, qg + (size_t)r * K + 4 * c4);
+    }
+    for (int e = tid; e < 2 * K * K / 4; e += 256) sp_cp16(ws + 4 * e, W32 + (size_t)t * 2 * K * K + 4 * e);
+  };
+#pragma unroll
+  for (int s = 0; s < C::NS - 1; ++s) {
+    if (s < nstage) issue(s);
+    sp_cp_commit();
+  }
+  double acc[C::NRT][4];
+  bool bad = false;
+  for (int f = 0; f < nstage; ++f) {
+    const int t = f % M;
+    const int row0 = ((int)blockIdx.x + (f / M) * (int)gridDim.x) * C::RB;
+    const int nr = min(C::RB, n - row0);
+    if (f + C::NS - 1 < nstage) issue(f + C::NS - 1);
+    sp_cp_commit();
+    sp_cp_wait<C::NS - 1>();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int u = 0; u < C::NRT; ++u)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[u][x] = 0.0;
+    }
+    const float* ps = nsm + (size_t)(f % C::NS) * C::STAGE;
+    const float* qs = ps + C::RB * C::LD;
+    const float* WrT = qs + C::RB * C::LD;  // [d][c] = R_t[c][d]
+    const float* Wr = WrT + K * K;          // [d][c] = R_t[d][c]
+    float s[C::NRT][4];
+#pragma unroll
+    for (int u = 0; u < C::NRT; ++u)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) s[u][x] = 0.f;
+#pragma unroll
+    for (int d4 = 0; d4 < K / 4; ++d4) {
+      float4 pr[C::NRT], qr[C::NRT];
+#pragma unroll
+      for (int u = 0; u < C::NRT; ++u) {
+        const int r = rq + u * C::RQ;
+        pr[u] = *reinterpret_cast<const float4*>(ps + r * C::LD + 4 * d4);
+        qr[u] = *reinterpret_cast<const float4*>(qs + r * C::LD + 4 * d4);
+      }
+#pragma unroll
+      for (int dd = 0; dd < 4; ++dd) {
+        const int d = 4 * d4 + dd;
+        const float4 wp = *reinterpret_cast<const float4*>(WrT + d * K + 4 * cb);
+        const float4 wq = *reinterpret_cast<const float4*>(Wr + d * K + 4 * cb);
+#pragma unroll
+        for (int u = 0; u < C::NRT; ++u) {
+          const float pv = dd == 0 ? pr[u].x : dd == 1 ? pr[u].y : dd == 2 ? pr[u].z : pr[u].w;
+          const float qv = dd == 0 ? qr[u].x : dd == 1 ? qr[u].y : dd == 2 ? qr[u].z : qr[u].w;
+          s[u][0] = fmaf(pv, wp.x, fmaf(qv, wq.x, s[u][0]));
+          s[u][1] = fmaf(pv, wp.y, fmaf(qv, wq.y, s[u][1]));
+          s[u][2] = fmaf(pv, wp.z, fmaf(qv, wq.z, s[u][2]));
+          s[u][3] = fmaf(pv, wp.w, fmaf(qv, wq.w, s[u][3]));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < C::NRT; ++u)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[u][x] += (double)s[u][x];
+    if (t == M - 1) {
+      // A update of this row block: read the old rows, sync, write
+      double an[C::NRT][4];
+#pragma unroll
+      for (int u = 0; u < C::NRT; ++u) {
+        const int r = rq + u * C::RQ;
+        if (r < nr) {
+          const double* Ai = A64 + (size_t)(row0 + r) * K;
+          double deno[4] = {eps_m, eps_m, eps_m, eps_m};
+          for (int d = 0; d < K; ++d) {
+            const double a = Ai[d];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) deno[x] = fma(a, Ms[d * K + 4 * cb + x], deno[x]);
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            an[u][x] = Ai[4 * cb + x] * acc[u][x] / deno[x];
+            bad |= !isfinite(an[u][x]);
+          }
+        }
+      }
+      __syncthreads();  // every thread has read its whole A rows before any write
+#pragma unroll
+      for (int u = 0; u < C::NRT; ++u) {
+        const int r = rq + u * C::RQ;
+        if (r < nr) {
+          double* Ai = A64 + (size_t)(row0 + r) * K + 4 * cb;
+          float* Af = A32 + (size_t)(row0 + r) * K + 4 * cb;
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            Ai[x] = an[u][x];
+            Af[x] = (float)an[u][x];
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage f % NS is refilled next iteration
+  }
+  if (bad) {
+    ctl->nonfinite = 1;
+    ctl->stop = 1;
+  }
+}
+
+// ---- tensor-core numerator (K = 16): num = [P_1..P_m Q_1..Q_m] . [R_t^T ; R_t]
+// is an (n x 32m) by (32m x 16) GEMM. mma.sync m16n8k8 TF32 with the 3-pass
+// split (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32-level products); a warp owns
+// 32 rows (two m-tiles) x 16 columns. The K order inside a slice is permuted so
+// that each lane's A fragment is one LDS.128 of a contiguous smem row (lane
+// (g, tq) holds d = 4tq..4tq+3 of rows g and g+8: k-step s uses d = 4tq+2s and
+// 4tq+2s+1), which is conflict-free on unpadded 64-byte rows. The matching B
+// fragments (hi/lo, per slice) are laid out per lane by sp_wfrag.
+RK_DEV uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+RK_DEV void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+RK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// Wf[t][pq][s][nt][lane] = {b0_hi, b1_hi, b0_lo, b1_lo} with lane = 4g + tq,
+// b0 = W[4tq+2s][8nt+g], b1 = W[4tq+2s+1][8nt+g], W = R_t^T (pq 0) | R_t (pq 1)
+// taken from W32 = [R_t^T ; R_t] (K = 16).
+__global__ void __launch_bounds__(256) sp_wfrag(const Ctl* __restrict__ ctl, const float* __restrict__ W32,
+                                                float4* __restrict__ Wf, int M) {
+  if (ctl->stop) return;
+  const int t = blockIdx.x;
+  const int lane = threadIdx.x & 31, combo = threadIdx.x >> 5;  // combo = pq*4 + s*2 + nt
+  const int pq = combo >> 2, s = (combo >> 1) & 1, nt = combo & 1;
+  const int g = lane >> 2, tq = lane & 3;
+  const float* W = W32 + ((size_t)t * 2 + pq) * 256;
+  const float b0 = W[(4 * tq + 2 * s) * 16 + 8 * nt + g], b1 = W[(4 * tq + 2 * s + 1) * 16 + 8 * nt + g];
+  const uint32_t h0 = tf32_rna(b0), h1 = tf32_rna(b1);
+  const uint32_t l0 = tf32_rna(b0 - __uint_as_float(h0)), l1 = tf32_rna(b1 - __uint_as_float(h1));
+  Wf[((size_t)t * 8 + combo) * 32 + lane] =
+      make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(l0), __uint_as_float(l1));
+}
+
+struct SpNumTc {
+  static constexpr int K = 16;
+  static constexpr int RB = 256;  // rows per row block (8 warps x 32)
+  static constexpr int NS = 4;
+  static constexpr int PQ_BYTES = RB * K * 4;         // one of P_t / Q_t
+  static constexpr int WF_BYTES = 8 * 32 * 16;        // Wf_t
+  static constexpr int STAGE = 2 * PQ_BYTES + WF_BYTES;
+  static constexpr size_t smem = (size_t)NS * STAGE + K * K * sizeof(double) + NS * 8 + 128;
+};
+
+__global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, double* __restrict__ A64,
+                                                      float* __restrict__ A32, const float* __restrict__ P,
+                                                      const float* __restrict__ Q, int ldp, int ldq,
+                                                      const float4* __restrict__ Wf,
+                                                      const double* __restrict__ Mm, int n, int M,
+                                                      double eps_m) {
+  using C = SpNumTc;
+  constexpr int K = 16;
+  if (ctl->stop) return;
+  extern __shared__ __align__(128) uint8_t tsm[];
+  uint8_t* ring = tsm;
+  double* Ms = reinterpret_cast<double*>(tsm + (size_t)C::NS * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ms + K * K);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int nrb = (n + C::RB - 1) / C::RB;
+  const int my_rb = nrb > (int)blockIdx.x ? (nrb - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nstage = my_rb * M;
+  if (nstage == 0) return;
+  for (int e = tid; e < K * K; e += 256) Ms[e] = Mm[e];
+  if (tid == 0) {
+    for (int i = 0; i < C::NS; ++i) tc::mbar_init(tc::smem_u32(&full[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int f) {  // thread 0 only
+    const int t = f % M, row0 = ((int)blockIdx.x + (f / M) * (int)gridDim.x) * C::RB;
+    const int nr = min(C::RB, n - row0);
+    uint8_t* st = ring + (size_t)(f % C::NS) * C::STAGE;
+    const uint32_t bar = tc::smem_u32(&full[f % C::NS]);
+    const uint32_t bytes = (uint32_t)nr * K * 4;
+    tc::mbar_expect_tx(bar, 2 * bytes + C::WF_BYTES);
+    bulk_g2s(tc::smem_u32(st), P + ((size_t)t * ldp + row0) * K, bytes, bar);
+    bulk_g2s(tc::smem_u32(st + C::PQ_BYTES), Q + ((size_t)t * ldq + row0) * K, bytes, bar);
+    bulk_g2s(tc::smem_u32(st + 2 * C::PQ_BYTES), Wf + (size_t)t * 256, C::WF_BYTES, bar);
+  };
+  if (tid == 0)
+    for (int f = 0; f < C::NS - 1 && f < nstage; ++f) issue(f);
+  double acc[2][2][4];
+  bool bad = false;
+  for (int f = 0; f < nstage; ++f) {
+    const int t = f % M;
+    const int row0 = ((int)blockIdx.x + (f / M) * (int)gridDim.x) * C::RB;
+    const int nr = min(C::RB, n - row0);
+    if (tid == 0 && f + C::NS - 1 < nstage) issue(f + C::NS - 1);
+    tc::mbar_wait(tc::smem_u32(&full[f % C::NS]), (uint32_t)((f / C::NS) & 1));
+    if (t == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) acc[mt][nt][x] = 0.0;
+    }
+    const uint8_t* st = ring + (size_t)(f % C::NS) * C::STAGE;
+    const float4* wf = reinterpret_cast<const float4*>(st + 2 * C::PQ_BYTES);
+    float c[2][2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) c[mt][nt][x] = 0.f;
+#pragma unroll
+    for (int pq = 0; pq < 2; ++pq) {
+      const float* S = reinterpret_cast<const float*>(st + pq * C::PQ_BYTES);
+      float4 bw[2][2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bw[s][nt] = wf[(pq * 4 + s * 2 + nt) * 32 + lane];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = warp * 32 + mt * 16 + g;
+        const float4 x0 = *reinterpret_cast<const float4*>(S + r * K + 4 * tq);
+        const float4 x1 = *reinterpret_cast<const float4*>(S + (r + 8) * K + 4 * tq);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const float v[4] = {s ? x0.z : x0.x, s ? x1.z : x1.x, s ? x0.w : x0.y, s ? x1.w : x1.y};
+          uint32_t ah[4], al[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ah[q] = tf32_rna(v[q]);
+            al[q] = tf32_rna(v[q] - __uint_as_float(ah[q]));
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const uint32_t bh0 = __float_as_uint(bw[s][nt].x), bh1 = __float_as_uint(bw[s][nt].y);
+            const uint32_t bl0 = __float_as_uint(bw[s][nt].z), bl1 = __float_as_uint(bw[s][nt].w);
+            mma_tf32(c[mt][nt], al, bh0, bh1);
+            mma_tf32(c[mt][nt], ah, bl0, bl1);
+            mma_tf32(c[mt][nt], ah, bh0, bh1);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)c[mt][nt][x];
+    if (t == M - 1) {
+      // A update of this row block. Lane (g, tq) holds rows r (c0, c1) and
+      // r + 8 (c2, c3) at columns 8nt + 2tq + {0, 1} of each m-tile.
+      double an[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = warp * 32 + mt * 16 + g + 8 * h;
+          if (r < nr) {
+            const double* Ai = A64 + (size_t)(row0 + r) * K;
+            double a[K];
+#pragma unroll
+            for (int d = 0; d < K; ++d) a[d] = Ai[d];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int col = 8 * nt + 2 * tq + e;
+                double deno = eps_m;
+#pragma unroll
+                for (int d = 0; d < K; ++d) deno = fma(a[d], Ms[d * K + col], deno);
+                const double v = Ai[col] * acc[mt][nt][2 * h + e] / deno;
+                an[mt][nt][2 * h + e] = v;
+                bad |= !isfinite(v);
+              }
+          }
+        }
+      __syncthreads();  // all rows of the block read before any write
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = warp * 32 + mt * 16 + g + 8 * h;
+          if (r < nr) {
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const int col = 8 * nt + 2 * tq;
+              const double v0 = an[mt][nt][2 * h], v1 = an[mt][nt][2 * h + 1];
+              *reinterpret_cast<double2*>(A64 + (size_t)(row0 + r) * K + col) = make_double2(v0, v1);
+              *reinterpret_cast<float2*>(A32 + (size_t)(row0 + r) * K + col) = make_float2((float)v0, (float)v1);
+            }
+          }
+        }
+    }
+    __syncthreads();  // stage f % NS is refilled next iteration
+  }
+  if (bad) {
+    ctl->nonfinite = 1;
+    ctl->stop = 1;
   }
 }
 
