@@ -551,7 +551,7 @@ void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
   if (h->sparse && !h->grid()) {
     // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram)
-    const int grid = h->num_sms * 3;
+    const int grid = h->num_sms * 2;
     if (K == 16)
       rk::sp::sp_gram<16><<<grid, 256, rk::sp::SpGramCfg<16>::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);

@@ -37,23 +37,62 @@ RK_DEV void sp_cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// L2 cache-policy helpers (createpolicy + .L2::cache_hint): the index/value
+// streams and the output rows are touched once per pass (evict_first), the
+// gathered factor rows are re-read ~10x per pass from L2 (evict_last, and not
+// allocated in L1 where a random 64 B row is never reused).
+RK_DEV uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+RK_DEV uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+RK_DEV int ld_stream(const int* a, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+RK_DEV float ld_stream(const float* a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+RK_DEV float4 ld_gather(const float* a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+RK_DEV void st_stream(float* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
 // SpMM pass Y_t = X_t B over the M slices of a CSR (or CSC) array set: one
 // lane group of G = K/4 lanes per row, K accumulators as one float4 per lane,
 // each stored entry gathers one K*4-byte row of B (coalesced across the group,
 // L2-resident). Used for P_t = X_t A (CSR, rows) and Q_t = X_t^T A (CSC,
-// columns). n = major dimension (rows of the block), ldy = row stride of Y.
+// columns). n = major dimension (rows of the block), Npad = row stride of Y.
 // The (slice, row) task index advances incrementally (no 64-bit division per
-// row); the gather loop keeps 4 independent loads in flight per lane.
+// row); the gather loop keeps 4 independent loads in flight per lane; 32
+// registers -> 64 resident warps per SM (the pass is L1/L2-latency bound).
 template <int K>
 __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ctl,
-                                                   const int64_t* __restrict__ ptr,
-                                                   const int* __restrict__ idx,
-                                                   const float* __restrict__ val,
-                                                   const float* __restrict__ A32,
-                                                   float* __restrict__ P, int n, int Npad, int M,
-                                                   int skip_if_stopped) {
+                                                      const int64_t* __restrict__ ptr,
+                                                      const int* __restrict__ idx,
+                                                      const float* __restrict__ val,
+                                                      const float* __restrict__ A32,
+                                                      float* __restrict__ P, int n, int Npad, int M,
+                                                      int skip_if_stopped) {
   if (skip_if_stopped && ctl->stop) return;
   constexpr int G = K / 4;
+  const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
   const int lane = threadIdx.x & 31;
   const int q = lane % G;
   const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -71,11 +110,11 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
       float4 a[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        j[u] = __ldg(idx + p + u);
-        v[u] = __ldg(val + p + u);
+        j[u] = ld_stream(idx + p + u, pf);
+        v[u] = ld_stream(val + p + u, pf);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j[u] * K) + q);
+      for (int u = 0; u < 4; ++u) a[u] = ld_gather(A32 + (size_t)j[u] * K + 4 * q, pl);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         y.x = fmaf(v[u], a[u].x, y.x);
@@ -85,15 +124,15 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
       }
     }
     for (; p < e; ++p) {
-      const int j = __ldg(idx + p);
-      const float v = __ldg(val + p);
-      const float4 a = __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j * K) + q);
+      const int j = ld_stream(idx + p, pf);
+      const float v = ld_stream(val + p, pf);
+      const float4 a = ld_gather(A32 + (size_t)j * K + 4 * q, pl);
       y.x = fmaf(v, a.x, y.x);
       y.y = fmaf(v, a.y, y.y);
       y.z = fmaf(v, a.z, y.z);
       y.w = fmaf(v, a.w, y.w);
     }
-    reinterpret_cast<float4*>(P + ((size_t)t * Npad + i) * K)[q] = y;
+    st_stream(P + ((size_t)t * Npad + i) * K + 4 * q, y, pf);
     i += ngroups;
     while (i >= n) {
       i -= n;
@@ -118,7 +157,7 @@ struct SpGramCfg {
   static constexpr int RL = 256 / NB;    // row lanes
   static constexpr int SR = K == 16 ? 128 : 64;  // rows per stage
   static constexpr int RPT = SR / RL;            // rows per thread per stage (8 | 16)
-  static constexpr int NS = 4;           // stages
+  static constexpr int NS = 6;           // stages (2 CTAs/SM: ~160 KB in flight)
   static constexpr size_t smem = (size_t)NS * SR * K * 2 * sizeof(float);
 };
 
@@ -437,7 +476,7 @@ __global__ void __launch_bounds__(256) sp_wfrag(const Ctl* __restrict__ ctl, con
 struct SpNumTc {
   static constexpr int K = 16;
   static constexpr int RB = 256;  // rows per row block (8 warps x 32)
-  static constexpr int NS = 4;
+  static constexpr int NS = 6;    // ~180 KB in flight per SM (HBM latency under load)
   static constexpr int PQ_BYTES = RB * K * 4;         // one of P_t / Q_t
   static constexpr int WF_BYTES = 8 * 32 * 16;        // Wf_t
   static constexpr int STAGE = 2 * PQ_BYTES + WF_BYTES;
@@ -483,6 +522,7 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
   if (tid == 0)
     for (int f = 0; f < C::NS - 1 && f < nstage; ++f) issue(f);
   double acc[2][2][4];
+  float c[2][2][2][4];  // [pq][mt][nt][frag]
   bool bad = false;
   for (int f = 0; f < nstage; ++f) {
     const int t = f % M;
@@ -500,13 +540,19 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
     }
     const uint8_t* st = ring + (size_t)(f % C::NS) * C::STAGE;
     const float4* wf = reinterpret_cast<const float4*>(st + 2 * C::PQ_BYTES);
-    float c[2][2][4];
+    // independent accumulators per (pq, mt, nt): 8 MMA chains per warp; the
+    // three split passes are issued pass-major so consecutive MMAs never
+    // depend on each other
+    if ((t & 1) == 0) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+      for (int pq = 0; pq < 2; ++pq)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int x = 0; x < 4; ++x) c[mt][nt][x] = 0.f;
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int x = 0; x < 4; ++x) c[pq][mt][nt][x] = 0.f;
+    }
 #pragma unroll
     for (int pq = 0; pq < 2; ++pq) {
       const float* S = reinterpret_cast<const float*>(st + pq * C::PQ_BYTES);
@@ -515,6 +561,7 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
       for (int s = 0; s < 2; ++s)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) bw[s][nt] = wf[(pq * 4 + s * 2 + nt) * 32 + lane];
+      uint32_t ah[2][2][4], al[2][2][4];  // [mt][s][q]
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int r = warp * 32 + mt * 16 + g;
@@ -523,29 +570,38 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const float v[4] = {s ? x0.z : x0.x, s ? x1.z : x1.x, s ? x0.w : x0.y, s ? x1.w : x1.y};
-          uint32_t ah[4], al[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ah[q] = tf32_rna(v[q]);
-            al[q] = tf32_rna(v[q] - __uint_as_float(ah[q]));
-          }
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const uint32_t bh0 = __float_as_uint(bw[s][nt].x), bh1 = __float_as_uint(bw[s][nt].y);
-            const uint32_t bl0 = __float_as_uint(bw[s][nt].z), bl1 = __float_as_uint(bw[s][nt].w);
-            mma_tf32(c[mt][nt], al, bh0, bh1);
-            mma_tf32(c[mt][nt], ah, bl0, bl1);
-            mma_tf32(c[mt][nt], ah, bh0, bh1);
+          for (int q = 0; q < 4; ++q) {  // hi = truncation to tf32 (one LOP), lo exact
+            ah[mt][s][q] = __float_as_uint(v[q]) & 0xffffe000u;
+            al[mt][s][q] = __float_as_uint(v[q] - __uint_as_float(ah[mt][s][q]));
           }
         }
       }
+#pragma unroll
+      for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const float4 b = bw[s][nt];
+              if (pass == 0)
+                mma_tf32(c[pq][mt][nt], al[mt][s], __float_as_uint(b.x), __float_as_uint(b.y));
+              else if (pass == 1)
+                mma_tf32(c[pq][mt][nt], ah[mt][s], __float_as_uint(b.z), __float_as_uint(b.w));
+              else
+                mma_tf32(c[pq][mt][nt], ah[mt][s], __float_as_uint(b.x), __float_as_uint(b.y));
+            }
     }
+    if ((t & 1) || t == M - 1) {  // fp32 over <= 2 slices (64 products), then fp64
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)c[mt][nt][x];
+          for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)(c[0][mt][nt][x] + c[1][mt][nt][x]);
+    }
     if (t == M - 1) {
       // A update of this row block. Lane (g, tq) holds rows r (c0, c1) and
       // r + 8 (c2, c3) at columns 8nt + 2tq + {0, 1} of each m-tile.

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) csr_v1(const int64_t* __restrict__ ptr, c
         j[u] &= mask;
       }
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) a[u] = HINT == 4 ? ld_gather_l1(A32 + (size_t)j[u] * K + 4 * q, pl) : HINT == 2 ? ld_gather(A32 + (size_t)j[u] * K + 4 * q, pl) : __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j[u] * K) + q);
+      for (int u = 0; u < UNR; ++u) a[u] = HINT == 5 ? ld_gather_plain(A32 + (size_t)j[u] * K + 4 * q) : HINT == 6 ? ld_gather(A32 + (size_t)j[u] * K + 4 * q, pl) : HINT == 4 ? ld_gather_l1(A32 + (size_t)j[u] * K + 4 * q, pl) : HINT == 2 ? ld_gather(A32 + (size_t)j[u] * K + 4 * q, pl) : __ldg(reinterpret_cast<const float4*>(A32 + (size_t)j[u] * K) + q);
 #pragma unroll
       for (int u = 0; u < UNR; ++u) { y.x = fmaf(v[u], a[u].x, y.x); y.y = fmaf(v[u], a[u].y, y.y); y.z = fmaf(v[u], a[u].z, y.z); y.w = fmaf(v[u], a[u].w, y.w); }
     }
@@ -345,6 +345,49 @@ __global__ void __launch_bounds__(256) csr_v11(const int64_t* __restrict__ ptr, 
     }
     const int t = (int)(task / n), i = (int)(task - (int64_t)t * n);
     *reinterpret_cast<float4*>(P + ((size_t)t * n + i) * K + 4 * q) = y;
+  }
+}
+
+// V12: library kernel (hints, incremental task) + group-cooperative idx/val loads
+template <int K>
+__global__ void __launch_bounds__(256, 8) csr_v12(const int64_t* __restrict__ ptr, const int* __restrict__ idx,
+                                                  const float* __restrict__ val, const float* __restrict__ A32,
+                                                  float* __restrict__ P, int n, int Npad, int M) {
+  constexpr int G = K / 4;
+  const uint64_t pf = rk::sp::l2_evict_first(), pl = rk::sp::l2_evict_last();
+  const int lane = threadIdx.x & 31;
+  const int q = lane % G, gb = lane - q;
+  const unsigned gmask = ((1u << G) - 1u) << gb;
+  const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int ngroups = (int)(((int64_t)gridDim.x * blockDim.x) / G);
+  int t = (int)(group / n), i = (int)(group - (int64_t)t * n);
+  for (; t < M;) {
+    const int64_t* pt = ptr + (size_t)t * (n + 1);
+    const int64_t b = pt[i], e = pt[i + 1];
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t p = b; p < e; p += G) {
+      const bool ok = p + q < e;
+      const int jq = ok ? rk::sp::ld_stream(idx + p + q, pf) : 0;
+      const float vq = ok ? rk::sp::ld_stream(val + p + q, pf) : 0.f;
+      float4 a[G];
+      float v[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int j = __shfl_sync(gmask, jq, gb + u);
+        v[u] = __shfl_sync(gmask, vq, gb + u);
+        a[u] = p + u < e ? rk::sp::ld_gather(A32 + (size_t)j * K + 4 * q, pl) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        y.x = fmaf(v[u], a[u].x, y.x);
+        y.y = fmaf(v[u], a[u].y, y.y);
+        y.z = fmaf(v[u], a[u].z, y.z);
+        y.w = fmaf(v[u], a[u].w, y.w);
+      }
+    }
+    rk::sp::st_stream(P + ((size_t)t * Npad + i) * K + 4 * q, y, pf);
+    i += ngroups;
+    while (i >= n) { i -= n; ++t; }
   }
 }
 
@@ -625,6 +668,16 @@ int main(int argc, char** argv) {
   if (on("mask")) for (int lg : {16, 18, 19, 20}) {
     char nm[64]; snprintf(nm, 64, "V1 unr4 cols masked to 2^%d", lg);
     report(nm, timeit([&] { csr_v1<4, 0><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M, (1 << lg) - 1); }));
+  }
+  if (on("coop2")) {
+    report("V0 (hinted library)", timeit([&] { sp::sp_csr_pass<16><<<sms * 16, 256>>>(ctl, ptr2, idx, val, A, P, n, n, M, 0); }));
+    report("V12 coop", timeit([&] { csr_v12<16><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, n, M); })); check("v12");
+  }
+  if (on("hint2")) {
+    report("V1 unr4 hint0", timeit([&] { csr_v1<4, 0><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M); })); check("v1");
+    report("V1 unr4 hint3 (stream L1+evict_first)", timeit([&] { csr_v1<4, 3><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M); })); check("v1");
+    report("V1 unr4 hint5 (+gather L1 no_alloc)", timeit([&] { csr_v1<4, 5><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M); })); check("v1");
+    report("V1 unr4 hint6 (+gather no_alloc evict_last)", timeit([&] { csr_v1<4, 6><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M); })); check("v1");
   }
   if (on("hint")) {
     report("V1 unr4 hint3 (stream L1+evict_first)", timeit([&] { csr_v1<4, 3><<<sms * 16, 256>>>(ptr2, idx, val, A, P, n, M); })); check("v1");
