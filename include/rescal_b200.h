@@ -76,6 +76,16 @@ int rk_create_sparse(int device, int64_t n, int64_t m, int32_t k, rk_handle** ou
 int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, const void* data,
                   int32_t dtype, int64_t nnz);
 
+/* Per-slice form (no host-side concatenation): for t < m, indptrs[t] is the
+ * slice's own (n+1) int64 indptr starting at 0, indices[t] / data[t] its
+ * nnz_per_slice[t] column ids and values — i.e. the arrays of each canonical
+ * scipy csr_matrix in SparseRelTensor.slices (tensor.py:86-104). Pageable
+ * buffers stream through a pinned ring; validation (non-negative values,
+ * column range: tensor.py:102-103) and ||X||^2 (rescal.py:160-165) run on
+ * the device. */
+int rk_upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_t* const* indices,
+                         const void* const* data, const int64_t* nnz_per_slice, int32_t dtype);
+
 /* Host tensor -> device. x is (m, n, n) C-contiguous in `dtype`. Replaces the
  * dense RelTensor.slice_ops() operand view (tensor.py:67-69). Also records
  * ||X||^2 in fp64 from the host values (rescal.py:160-165). */

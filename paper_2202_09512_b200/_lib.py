@@ -47,6 +47,7 @@ SIGNATURES = {
     "rk_upload_block": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _f64]),
     "rk_create_sparse": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i32, ctypes.POINTER(_vp)]),
     "rk_upload_csr": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _vp, _i32, _i64]),
+    "rk_upload_csr_slices": (ctypes.c_int, [_vp, _vp, _vp, _vp, _pi64, _i32]),
     "rk_fill_uniform": (ctypes.c_int, [_vp, _u64]),
     "rk_set_factors": (ctypes.c_int, [_vp, _pd, _pd]),
     "rk_get_factors": (ctypes.c_int, [_vp, _pd, _pd]),
@@ -165,20 +166,31 @@ class Engine:
         check(self._lib.rk_upload_dense(self._h, x.ctypes.data_as(_vp), RK_F32 if x.dtype == np.float32 else RK_F64))
 
     def upload_csr(self, slices):
-        """Canonical CSR slices (scipy) -> device CSR + device-built CSC."""
+        """Canonical CSR slices (scipy) -> device CSR + device-built CSC.
+
+        The per-slice arrays are handed over as they are (no concatenation);
+        the library streams them through a pinned ring and validates them on
+        the device."""
         if len(slices) != self.m:
             raise DataError(f"expected {self.m} slices, got {len(slices)}")
-        nnz = np.array([s.nnz for s in slices], dtype=np.int64)
-        base = np.concatenate([[0], np.cumsum(nnz)[:-1]])
-        indptr = np.concatenate([s.indptr.astype(np.int64) + b for s, b in zip(slices, base)])
-        indices = np.ascontiguousarray(np.concatenate([s.indices for s in slices]).astype(np.int32))
-        data = np.concatenate([s.data for s in slices])
-        data = np.ascontiguousarray(data if data.dtype in (np.float32, np.float64) else data.astype(np.float64))
-        indptr = np.ascontiguousarray(indptr)
-        check(self._lib.rk_upload_csr(self._h, indptr.ctypes.data_as(_pi64),
-                                      indices.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                      data.ctypes.data_as(_vp), RK_F32 if data.dtype == np.float32 else RK_F64,
-                                      int(nnz.sum())))
+        keep = []
+        dts = {s.data.dtype for s in slices}
+        dt = np.float32 if dts == {np.dtype(np.float32)} else np.float64
+        ip = (ctypes.c_void_p * self.m)()
+        ix = (ctypes.c_void_p * self.m)()
+        dv = (ctypes.c_void_p * self.m)()
+        nnz = np.empty(self.m, dtype=np.int64)
+        for t, sl in enumerate(slices):
+            a = np.ascontiguousarray(sl.indptr, dtype=np.int64)
+            b = np.ascontiguousarray(sl.indices, dtype=np.int32)
+            c = np.ascontiguousarray(sl.data, dtype=dt)
+            keep += [a, b, c]
+            ip[t], ix[t], dv[t] = a.ctypes.data, b.ctypes.data, c.ctypes.data
+            nnz[t] = sl.nnz
+        check(self._lib.rk_upload_csr_slices(self._h, ctypes.cast(ip, _vp), ctypes.cast(ix, _vp),
+                                             ctypes.cast(dv, _vp), nnz.ctypes.data_as(_pi64),
+                                             RK_F32 if dt == np.float32 else RK_F64))
+        del keep
 
     def fill_sparse_uniform(self, seed, nnz_per_slice):
         """Synthetic uniform-random sparse slices generated on the device."""

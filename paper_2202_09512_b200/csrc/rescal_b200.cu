@@ -18,11 +18,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/rescal_b200.h"
@@ -975,6 +977,13 @@ void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, h->csr_val, h->csc_val,
                                   (int)std::max<int64_t>(1, max_nnz), 0, 64, h->stream);
   void* tmp = dalloc<uint8_t>(tmp_bytes + 16);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, scan_bytes, counts, h->csc_ptr, cub::Sum(), (int64_t)0, (int)cols,
+                                 h->stream);
+  void* scan_tmp = dalloc<uint8_t>(scan_bytes + 16);
+  // the last offset of each slice comes from host memory that outlives the
+  // asynchronous copies (filled before each copy is enqueued)
+  std::vector<int64_t> ends((size_t)M);
   for (int64_t t = 0; t < M; ++t) {
     const int64_t base = indptr_host[t * (rows + 1)], cnt = indptr_host[t * (rows + 1) + rows] - base;
     RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * cols, h->stream));
@@ -987,7 +996,11 @@ void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
                                               h->stream));
       rk::sp::sp_split_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(keys2, cnt, h->csc_idx + base, counts);
     }
-    rk::sp::sp_offsets<<<1, 1024, 0, h->stream>>>(counts, (int)cols, base, h->csc_ptr + t * (cols + 1));
+    RK_CUDA(cub::DeviceScan::ExclusiveScan(scan_tmp, scan_bytes, counts, h->csc_ptr + t * (cols + 1),
+                                           cub::Sum(), (int64_t)base, (int)cols, h->stream));
+    ends[t] = base + cnt;
+    RK_CUDA(cudaMemcpyAsync(h->csc_ptr + t * (cols + 1) + cols, &ends[t], sizeof(int64_t),
+                            cudaMemcpyHostToDevice, h->stream));
     RK_CUDA(cudaGetLastError());
   }
   RK_CUDA(cudaStreamSynchronize(h->stream));
@@ -995,6 +1008,7 @@ void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
   dfree(keys2);
   dfree(counts);
   dfree(tmp);
+  dfree(scan_tmp);
 }
 
 // ||X||^2 over all ranks (the trace denominator is global)
@@ -1010,6 +1024,187 @@ double global_sum(rk_handle* h, double v) {
 }  // namespace
 
 // =============================== C ABI ======================================
+
+namespace {
+// Host -> device streaming through a pinned two-slot ring: pageable sources
+// are copied into the pinned slot by several host threads while the other
+// slot's DMA and post-processing kernel run (pinned sources are DMA'd
+// directly). `post(dev_chunk, offset, bytes)` runs on the stream after each
+// chunk has landed in `dev_dst + offset` (or in a device staging slot when
+// dev_dst is null).
+class Uploader {
+ public:
+  static constexpr size_t kChunk = 64ull << 20;
+  explicit Uploader(rk_handle* h) : h_(h) {
+    for (int i = 0; i < 2; ++i) {
+      RK_CUDA(cudaMallocHost(&host_[i], kChunk));
+      dev_[i] = dalloc<uint8_t>(kChunk);
+      RK_CUDA(cudaEventCreateWithFlags(&done_[i], cudaEventDisableTiming));
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    threads_ = (int)std::max(1u, std::min(8u, hw ? hw : 1u));
+  }
+  ~Uploader() {
+    cudaStreamSynchronize(h_->stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaFreeHost(host_[i]);
+      dfree(dev_[i]);
+      cudaEventDestroy(done_[i]);
+    }
+  }
+  double wait_ms = 0.0, memcpy_ms = 0.0;  // diagnostics
+  template <typename Post>
+  void copy(const void* src, size_t bytes, void* dev_dst, Post post) {
+    cudaPointerAttributes attr;
+    const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    for (size_t off = 0; off < bytes; off += kChunk) {
+      const size_t nb = std::min(kChunk, bytes - off);
+      auto t0 = std::chrono::steady_clock::now();
+      if (used_[slot_]) RK_CUDA(cudaEventSynchronize(done_[slot_]));
+      auto t1 = std::chrono::steady_clock::now();
+      const uint8_t* from = static_cast<const uint8_t*>(src) + off;
+      if (!pinned) {
+        par_memcpy(host_[slot_], from, nb);
+        from = host_[slot_];
+      }
+      auto t2 = std::chrono::steady_clock::now();
+      wait_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+      memcpy_ms += std::chrono::duration<double, std::milli>(t2 - t1).count();
+      uint8_t* to = dev_dst ? static_cast<uint8_t*>(dev_dst) + off : dev_[slot_];
+      RK_CUDA(cudaMemcpyAsync(to, from, nb, cudaMemcpyHostToDevice, h_->stream));
+      post(to, off, nb);
+      RK_CUDA(cudaGetLastError());
+      RK_CUDA(cudaEventRecord(done_[slot_], h_->stream));
+      used_[slot_] = true;
+      slot_ ^= 1;
+    }
+  }
+
+ private:
+  void par_memcpy(void* dst, const void* src, size_t nb) {
+    const size_t min_part = 4ull << 20;
+    const int nt = (int)std::min<size_t>(threads_, std::max<size_t>(1, nb / min_part));
+    if (nt <= 1) {
+      std::memcpy(dst, src, nb);
+      return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (nb + nt - 1) / nt;
+    for (int i = 0; i < nt; ++i) {
+      const size_t o = (size_t)i * part;
+      if (o >= nb) break;
+      th.emplace_back([=] {
+        std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, std::min(part, nb - o));
+      });
+    }
+    for (auto& t : th) t.join();
+  }
+  rk_handle* h_;
+  uint8_t* host_[2] = {nullptr, nullptr};
+  uint8_t* dev_[2] = {nullptr, nullptr};
+  cudaEvent_t done_[2];
+  bool used_[2] = {false, false};
+  int slot_ = 0;
+  int threads_ = 1;
+};
+
+// Shared body of the CSR uploads: per-slice host arrays (local indptr,
+// indices, values) -> device CSR with global offsets, validated and
+// converted on the device, then the device-built CSC.
+void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_t* const* indices,
+                       const void* const* data, const int64_t* nnz_t, int32_t dtype) {
+  static const bool timing = std::getenv("RK_UPLOAD_TIMING") != nullptr;  // diagnostics only
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t_start = now();
+  auto ms_since = [&](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(now() - a).count();
+  };
+  const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
+  RK_REQUIRE(dtype == RK_F32 || dtype == RK_F64, RK_ERR_DATA, "unsupported dtype");
+  std::vector<int64_t> ptr_host((size_t)M * (rows + 1));
+  int64_t nnz = 0;
+  for (int64_t t = 0; t < M; ++t) {
+    RK_REQUIRE(indptrs[t] != nullptr, RK_ERR_DATA, "null indptr");
+    RK_REQUIRE(nnz_t[t] >= 0 && indptrs[t][0] == 0 && indptrs[t][rows] == nnz_t[t], RK_ERR_DATA,
+               "inconsistent indptr");
+    RK_REQUIRE(nnz_t[t] == 0 || (indices[t] && data[t]), RK_ERR_DATA, "null argument");
+    nnz += nnz_t[t];
+  }
+  void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
+                 h->csc_val0};
+  for (void* p : old) dfree(p);
+  h->csr_val0 = h->csc_val0 = nullptr;
+  h->nnz = nnz;
+  h->csr_ptr = dalloc<int64_t>((size_t)M * (rows + 1));
+  h->csc_ptr = dalloc<int64_t>((size_t)M * (cols + 1));
+  h->csr_idx = dalloc<int>((size_t)std::max<int64_t>(1, nnz));
+  h->csc_idx = dalloc<int>((size_t)std::max<int64_t>(1, nnz));
+  h->csr_val = dalloc<float>((size_t)std::max<int64_t>(1, nnz));
+  h->csc_val = dalloc<float>((size_t)std::max<int64_t>(1, nnz));
+  const size_t vsize = dtype == RK_F32 ? 4 : 8;
+  const size_t nchunks = (size_t)(nnz * vsize / Uploader::kChunk) + (size_t)M + 2;
+  const int pblocks = h->num_sms * 2;
+  double* part = dalloc<double>(nchunks * pblocks);
+  int* flag = dalloc<int>(1);
+  RK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * nchunks * pblocks, h->stream));
+  RK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  size_t chunk_id = 0;
+  const double t_setup = ms_since(t_start);
+  {
+    Uploader up(h);
+    int64_t base = 0;
+    for (int64_t t = 0; t < M; ++t) {
+      int64_t* dptr = h->csr_ptr + t * (rows + 1);
+      up.copy(indptrs[t], sizeof(int64_t) * (rows + 1), nullptr, [&](void* d, size_t off, size_t nb) {
+        rk::sp::sp_rebase_ptr<<<h->num_sms * 2, 256, 0, h->stream>>>(
+            static_cast<const int64_t*>(d), (int64_t)(nb / 8), base, dptr + off / 8);
+      });
+      for (int64_t e = 0; e <= rows; ++e) ptr_host[(size_t)t * (rows + 1) + e] = indptrs[t][e] + base;
+      if (nnz_t[t] > 0) {
+        up.copy(indices[t], sizeof(int32_t) * nnz_t[t], h->csr_idx + base, [&](void* d, size_t, size_t nb) {
+          rk::sp::sp_check_idx<<<h->num_sms * 2, 256, 0, h->stream>>>(static_cast<const int*>(d),
+                                                                      (int64_t)(nb / 4), (int)cols, flag);
+        });
+        float* vdst = h->csr_val + base;
+        up.copy(data[t], vsize * nnz_t[t], dtype == RK_F32 ? (void*)vdst : nullptr,
+                [&](void* d, size_t off, size_t nb) {
+                  double* pp = part + (chunk_id++) * pblocks;
+                  if (dtype == RK_F32)
+                    rk::sp::sp_take_vals<float><<<pblocks, 256, 0, h->stream>>>(
+                        static_cast<const float*>(d), (int64_t)(nb / 4), vdst + off / 4, pp, flag);
+                  else
+                    rk::sp::sp_take_vals<double><<<pblocks, 256, 0, h->stream>>>(
+                        static_cast<const double*>(d), (int64_t)(nb / 8), vdst + off / 8, pp, flag);
+                });
+      }
+      base += nnz_t[t];
+    }
+    if (timing)
+      std::fprintf(stderr, "[rk]   ring: host memcpy %.1f ms, slot waits %.1f ms, setup %.1f ms\n", up.memcpy_ms,
+                   up.wait_ms, t_setup);
+  }
+  int fl = 0;
+  RK_CUDA(cudaMemcpy(&fl, flag, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<double> ph(chunk_id * pblocks);
+  if (!ph.empty()) RK_CUDA(cudaMemcpy(ph.data(), part, sizeof(double) * ph.size(), cudaMemcpyDeviceToHost));
+  dfree(part);
+  dfree(flag);
+  RK_REQUIRE(!(fl & 1), RK_ERR_DATA, "negative value in tensor");
+  RK_REQUIRE(!(fl & 2), RK_ERR_DATA, "column index out of range");
+  double s2 = 0.0;
+  for (double v : ph) s2 += v;
+  const double t_copy = ms_since(t_start);
+  auto t_csc = now();
+  build_csc(h, ptr_host);
+  h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
+  h->have_x = true;
+  h->perturbed = false;
+  if (timing)
+    std::fprintf(stderr, "[rk] upload_csr_slices: copy+validate %.1f ms, csc build %.1f ms (nnz %lld)\n", t_copy,
+                 ms_since(t_csc), (long long)nnz);
+}
+}  // namespace
 
 extern "C" {
 
@@ -1149,44 +1344,41 @@ int rk_create_sparse(int device, int64_t n, int64_t m, int32_t k, rk_handle** ou
   });
 }
 
+int rk_upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_t* const* indices,
+                         const void* const* data, const int64_t* nnz_per_slice, int32_t dtype) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "rk_upload_csr_slices needs a sparse handle");
+    RK_REQUIRE(indptrs && indices && data && nnz_per_slice, RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(h->dev));
+    upload_csr_slices(h, indptrs, indices, data, nnz_per_slice, dtype);
+  });
+}
+
 int rk_upload_csr(rk_handle* h, const int64_t* indptr, const int32_t* indices, const void* data,
                   int32_t dtype, int64_t nnz) {
   return guarded([&] {
     RK_REQUIRE(h && h->sparse, RK_ERR_DATA, "rk_upload_csr needs a sparse handle");
     RK_REQUIRE(indptr && (nnz == 0 || (indices && data)), RK_ERR_DATA, "null argument");
     RK_CUDA(cudaSetDevice(h->dev));
-    // the handle's (local) block: rows_valid CSR rows, cols_valid columns
-    const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
+    const int64_t rows = h->rows_valid, M = h->m;
     RK_REQUIRE(indptr[0] == 0 && indptr[M * (rows + 1) - 1] == nnz, RK_ERR_DATA, "inconsistent indptr");
-    void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
-                   h->csc_val0};
-    for (void* p : old) dfree(p);
-    h->csr_val0 = h->csc_val0 = nullptr;
-    h->nnz = nnz;
-    h->csr_ptr = dalloc<int64_t>((size_t)M * (rows + 1));
-    h->csc_ptr = dalloc<int64_t>((size_t)M * (cols + 1));
-    h->csr_idx = dalloc<int>((size_t)nnz);
-    h->csc_idx = dalloc<int>((size_t)nnz);
-    h->csr_val = dalloc<float>((size_t)nnz);
-    h->csc_val = dalloc<float>((size_t)nnz);
-    // values -> fp32, ||X||^2 in fp64 from the host values (rescal.py:160-165)
-    std::vector<float> v32((size_t)nnz);
-    double s2 = 0.0;
-    for (int64_t e = 0; e < nnz; ++e) {
-      const double v = dtype == RK_F32 ? (double)static_cast<const float*>(data)[e]
-                                       : static_cast<const double*>(data)[e];
-      RK_REQUIRE(v >= 0.0, RK_ERR_DATA, "negative value in tensor");
-      RK_REQUIRE(indices[e] >= 0 && indices[e] < cols, RK_ERR_DATA, "column index out of range");
-      s2 += v * v;
-      v32[e] = (float)v;
+    const size_t vsize = dtype == RK_F64 ? 8 : 4;
+    std::vector<std::vector<int64_t>> local((size_t)M);
+    std::vector<const int64_t*> ip((size_t)M);
+    std::vector<const int32_t*> ix((size_t)M);
+    std::vector<const void*> dv((size_t)M);
+    std::vector<int64_t> cnt((size_t)M);
+    for (int64_t t = 0; t < M; ++t) {
+      const int64_t* g = indptr + t * (rows + 1);
+      const int64_t b0 = g[0];
+      local[t].resize((size_t)rows + 1);
+      for (int64_t e = 0; e <= rows; ++e) local[t][e] = g[e] - b0;
+      ip[t] = local[t].data();
+      ix[t] = indices ? indices + b0 : nullptr;
+      dv[t] = data ? static_cast<const uint8_t*>(data) + (size_t)b0 * vsize : nullptr;
+      cnt[t] = g[rows] - b0;
     }
-    RK_CUDA(cudaMemcpy(h->csr_ptr, indptr, sizeof(int64_t) * M * (rows + 1), cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(h->csr_idx, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(h->csr_val, v32.data(), sizeof(float) * nnz, cudaMemcpyHostToDevice));
-    build_csc(h, std::vector<int64_t>(indptr, indptr + M * (rows + 1)));
-    h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
-    h->have_x = true;
-    h->perturbed = false;
+    upload_csr_slices(h, ip.data(), ix.data(), dv.data(), cnt.data(), dtype);
   });
 }
 

@@ -861,6 +861,53 @@ __global__ void __launch_bounds__(256) sp_sq_norm(const float* __restrict__ val,
   }
 }
 
+// Upload helpers (host CSR -> device, validated on the device): rebase a
+// slice's local indptr to global offsets; check column ids; check values
+// (non-negative, tensor.py:102-103), convert to fp32 and form per-block fp64
+// sums of squares (||X||^2, rescal.py:160-165) in a fixed order.
+__global__ void sp_rebase_ptr(const int64_t* __restrict__ src, int64_t count, int64_t base,
+                              int64_t* __restrict__ dst) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e] + base;
+}
+
+__global__ void sp_check_idx(const int* __restrict__ idx, int64_t count, int cols, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = idx[e];
+    bad |= j < 0 || j >= cols;
+  }
+  if (bad) atomicOr(flag, 2);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) sp_take_vals(const T* __restrict__ src, int64_t count,
+                                                    float* __restrict__ dst, double* __restrict__ part,
+                                                    int* __restrict__ flag) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)src[e];
+    bad |= !(v >= 0.0);
+    acc += v * v;
+    dst[e] = (float)v;
+  }
+  if (bad) atomicOr(flag, 1);
+  acc = warp_sum(acc);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    part[blockIdx.x] = s;
+  }
+}
+
 // CSC construction helpers: keys = (col << 32) | row per stored entry of
 // slice t, then a stable radix sort; counts per column -> exclusive scan.
 __global__ void sp_make_keys(const int64_t* __restrict__ ptr, const int* __restrict__ idx, int n,
