@@ -137,6 +137,25 @@ int rk_perturb(rk_handle* h, uint64_t state_hi, uint64_t state_lo, uint64_t inc_
                uint64_t inc_lo, double delta, int64_t n_global, int64_t row0, int64_t col0,
                const int64_t* col_map);
 
+/* Host-format resampling, the reference's perturb() / perturbation_field()
+ * (dist_rescal.py:164-171,205-215): `values` (dtype, host, in/out) are the
+ * elements e0 .. e0+count-1 of the C-ordered (m, n, n) tensor; each becomes
+ * value * (dtype)(1 + delta (2u_e - 1)), or the multiplier itself when
+ * field_only, with u_e the e-th draw of numpy PCG64 seeded as (state, inc).
+ * Bit-exact with the reference (fp64 field, cast, product in dtype). */
+int rk_perturb_values(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      double delta, int32_t dtype, void* values, int64_t count, uint64_t e0, int32_t field_only);
+
+/* Sparse perturb(): the stored values of CSR slice t (indptr starting at 0,
+ * n rows) are resampled at their elements (t*n + i)*n + j. */
+int rk_perturb_csr_values(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                          double delta, int32_t dtype, int64_t t, int64_t n, const int64_t* indptr,
+                          const int32_t* indices, void* values, int64_t nnz);
+
+/* Raw PCG64 draws u_{offset} .. u_{offset+count-1} (tests of the generator). */
+int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
+                   int64_t count, double* out);
+
 /* Multi-GPU p_r x p_c grid (dist_rescal.py:113-161 generalised to non-square
  * grids). nccl_id is a 128-byte ncclUniqueId broadcast by the caller. The
  * handle then holds the (m, n/p_r, n/p_c) block of rank (i, j); A pieces of

@@ -33,6 +33,8 @@ from .selection import (
     custom_cluster,
     lsa,
     pearson_correlation,
+    perturb,
+    perturbation_field,
     rescalk,
     select_k,
 )

@@ -67,6 +67,9 @@ SIGNATURES = {
     "rk_set_option": (ctypes.c_int, [_vp, _i32, _i64]),
     "rk_uniform_values": (ctypes.c_int, [_u64, _i64, _i64, _pf]),
     "rk_pcg64_draws": (ctypes.c_int, [_u64, _u64, _u64, _u64, _u64, _i64, _pd]),
+    "rk_perturb_values": (ctypes.c_int, [_i32, _u64, _u64, _u64, _u64, _f64, _i32, _vp, _i64, _u64, _i32]),
+    "rk_perturb_csr_values": (ctypes.c_int, [_i32, _u64, _u64, _u64, _u64, _f64, _i32, _i64, _i64, _pi64,
+                                             ctypes.POINTER(ctypes.c_int32), _vp, _i64]),
     "rk_grid_block": (ctypes.c_int, [_vp, _pi64, _i32]),
     "rk_grid_colmap": (ctypes.c_int, [_vp, _pi64]),
     "rk_time_k1": (ctypes.c_int, [_vp, _i32, _pd]),
@@ -353,6 +356,30 @@ def pcg64_draws(entropy, offset, count):
     out = np.empty(count, dtype=np.float64)
     check(load().rk_pcg64_draws(sh, sl, ih, il, int(offset), int(count), _dp(out)))
     return out
+
+
+def perturb_values(entropy, delta, values: np.ndarray, e0: int = 0, field_only: bool = False, device: int = 0):
+    """In place: values (contiguous f32/f64, the C-ordered elements e0..) times
+    the PCG64 multiplier field of `entropy` (or the field itself)."""
+    if values.dtype not in (np.float32, np.float64) or not values.flags.c_contiguous:
+        raise DataError("perturb_values needs a C-contiguous float32/float64 array")
+    sh, sl, ih, il = pcg64_seed_state(entropy)
+    check(load().rk_perturb_values(int(device), sh, sl, ih, il, float(delta),
+                                   RK_F32 if values.dtype == np.float32 else RK_F64,
+                                   values.ctypes.data, int(values.size), int(e0), int(bool(field_only))))
+
+
+def perturb_csr_values(entropy, delta, t: int, n: int, indptr, indices, values: np.ndarray, device: int = 0):
+    """In place: stored values of CSR slice t resampled at (t*n + i)*n + j."""
+    if values.dtype not in (np.float32, np.float64) or not values.flags.c_contiguous:
+        raise DataError("perturb_csr_values needs a C-contiguous float32/float64 array")
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    sh, sl, ih, il = pcg64_seed_state(entropy)
+    check(load().rk_perturb_csr_values(int(device), sh, sl, ih, il, float(delta),
+                                       RK_F32 if values.dtype == np.float32 else RK_F64, int(t), int(n),
+                                       ip.ctypes.data_as(_pi64), ix.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       values.ctypes.data, int(values.size)))
 
 
 def nccl_unique_id() -> bytes:

@@ -1921,6 +1921,68 @@ int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64
   });
 }
 
+int rk_perturb_values(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      double delta, int32_t dtype, void* values, int64_t count, uint64_t e0, int32_t field_only) {
+  return guarded([&] {
+    RK_REQUIRE(dtype == RK_F32 || dtype == RK_F64, RK_ERR_DATA, "unsupported dtype");
+    RK_REQUIRE(count >= 0 && (count == 0 || values), RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(device));
+    if (count == 0) return;
+    const rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+    const size_t esz = dtype == RK_F32 ? 4 : 8;
+    // chunks of whole 2048-element segments so every chunk restarts cleanly
+    const int64_t chunk = (int64_t)((256ull << 20) / esz);
+    uint8_t* d = dalloc<uint8_t>((size_t)std::min<int64_t>(count, chunk) * esz);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    for (int64_t o = 0; o < count; o += chunk) {
+      const int64_t c = std::min(chunk, count - o);
+      uint8_t* hv = static_cast<uint8_t*>(values) + (size_t)o * esz;
+      if (!field_only) RK_CUDA(cudaMemcpy(d, hv, (size_t)c * esz, cudaMemcpyHostToDevice));
+      if (dtype == RK_F32)
+        rk::perturb_flat<float><<<sms * 8, 256>>>(reinterpret_cast<float*>(d), c, e0 + (uint64_t)o, st, inc, delta,
+                                                  field_only);
+      else
+        rk::perturb_flat<double><<<sms * 8, 256>>>(reinterpret_cast<double*>(d), c, e0 + (uint64_t)o, st, inc,
+                                                   delta, field_only);
+      RK_CUDA(cudaGetLastError());
+      RK_CUDA(cudaMemcpy(hv, d, (size_t)c * esz, cudaMemcpyDeviceToHost));
+    }
+    dfree(d);
+  });
+}
+
+int rk_perturb_csr_values(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                          double delta, int32_t dtype, int64_t t, int64_t n, const int64_t* indptr,
+                          const int32_t* indices, void* values, int64_t nnz) {
+  return guarded([&] {
+    RK_REQUIRE(dtype == RK_F32 || dtype == RK_F64, RK_ERR_DATA, "unsupported dtype");
+    RK_REQUIRE(indptr && (nnz == 0 || (indices && values)), RK_ERR_DATA, "null argument");
+    RK_REQUIRE(indptr[0] == 0 && indptr[n] == nnz, RK_ERR_DATA, "inconsistent indptr");
+    RK_CUDA(cudaSetDevice(device));
+    if (nnz == 0) return;
+    const rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+    const size_t esz = dtype == RK_F32 ? 4 : 8;
+    int64_t* dp = dalloc<int64_t>((size_t)n + 1);
+    int* di = dalloc<int>((size_t)nnz);
+    uint8_t* dv = dalloc<uint8_t>((size_t)nnz * esz);
+    RK_CUDA(cudaMemcpy(dp, indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(di, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(dv, values, esz * nnz, cudaMemcpyHostToDevice));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (dtype == RK_F32)
+      rk::perturb_csr_vals<float><<<sms * 8, 256>>>(reinterpret_cast<float*>(dv), dp, di, n, t, n, st, inc, delta);
+    else
+      rk::perturb_csr_vals<double><<<sms * 8, 256>>>(reinterpret_cast<double*>(dv), dp, di, n, t, n, st, inc, delta);
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(values, dv, esz * nnz, cudaMemcpyDeviceToHost));
+    dfree(dp);
+    dfree(di);
+    dfree(dv);
+  });
+}
+
 int rk_nccl_unique_id(void* out128) {
   return guarded([&] {
     ncclUniqueId id;

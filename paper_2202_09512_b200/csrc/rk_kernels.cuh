@@ -1334,6 +1334,12 @@ RK_DEV double pcg_out_double(u128 state) {
   return (double)(out >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// The multiplier 1 + delta (2u - 1) with every operation rounded separately,
+// as numpy evaluates it (no FMA contraction): bit-exact fields.
+RK_DEV double pcg_field(double u, double delta) {
+  return __dadd_rn(1.0, __dmul_rn(delta, __dsub_rn(__dmul_rn(2.0, u), 1.0)));
+}
+
 // Coalesced resampling for whole-row tensors (single GPU): a warp owns a
 // 2048-element segment of one row; lane l draws elements base+64c+2l and +1.
 // Each lane jumps once per segment (log-time), then per 64-element chunk uses
@@ -1377,8 +1383,8 @@ __global__ void __launch_bounds__(256) perturb_rows(
       // j is even and NC % 128 == 0: a bf16x2 access stays inside the row
       const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(Xh0 + off);
       const __nv_bfloat162 l0 = *reinterpret_cast<const __nv_bfloat162*>(Xl0 + off);
-      double x0 = (double)join_bf16(h0.x, l0.x) * (1.0 + delta * (2.0 * u0 - 1.0));
-      double x1 = two ? (double)join_bf16(h0.y, l0.y) * (1.0 + delta * (2.0 * u1 - 1.0))
+      double x0 = (double)join_bf16(h0.x, l0.x) * pcg_field(u0, delta);
+      double x1 = two ? (double)join_bf16(h0.y, l0.y) * pcg_field(u1, delta)
                       : (double)join_bf16(h0.y, l0.y);
       __nv_bfloat16 a0, b0, a1, b1;
       split_bf16(x0, a0, b0);
@@ -1405,6 +1411,57 @@ __global__ void pcg64_draws(u128 state, u128 inc, uint64_t offset, int64_t count
   u128 s = pcg_advance(state, inc, offset + (uint64_t)start);
   int64_t end = min(count, start + per);
   for (int64_t e = start; e < end; ++e) out[e] = pcg_next_double(s, inc);
+}
+
+// Host-format resampling (the reference's perturb() / perturbation_field(),
+// dist_rescal.py:164-171,205-215) over a chunk of `count` consecutive
+// elements starting at global element e0: v[i] <- v[i] * (T)f(e0+i), or
+// v[i] <- (T)f(e0+i) when field_only, f = 1 + delta (2u - 1) in fp64 and the
+// product formed in T (x * field.astype(x.dtype)). Warp segments of kSeg
+// elements: lane l draws 2l, 2l+1 of every 64-element chunk after one
+// log-time jump per segment, then the fixed 62-step skip (as perturb_rows).
+template <typename T>
+__global__ void __launch_bounds__(256) perturb_flat(T* __restrict__ v, int64_t count, uint64_t e0, u128 state,
+                                                    u128 inc, double delta, int field_only) {
+  constexpr int kFlatSeg = 2048;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t segs = (count + kFlatSeg - 1) / kFlatSeg;
+  u128 m62, p62;
+  pcg_jump_coeffs(inc, 62, m62, p62);
+  const u128 m1 = pcg_mult(), p1 = inc;
+  for (int64_t sg = warp; sg < segs; sg += nwarps) {
+    const int64_t j0 = sg * kFlatSeg, j1 = min(count, j0 + kFlatSeg);
+    u128 s = pcg_advance(state, inc, e0 + (uint64_t)(j0 + 2 * lane));
+    for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
+      s = add128(mul128(s, m1), p1);
+      const double u0 = pcg_out_double(s);
+      s = add128(mul128(s, m1), p1);
+      const double u1 = pcg_out_double(s);
+      const T f0 = (T)pcg_field(u0, delta), f1 = (T)pcg_field(u1, delta);
+      v[j] = field_only ? f0 : v[j] * f0;
+      if (j + 1 < j1) v[j + 1] = field_only ? f1 : v[j + 1] * f1;
+      s = add128(mul128(s, m62), p62);
+    }
+  }
+}
+
+// Same for the stored values of one CSR slice t (sparse perturb(): only the
+// stored entries are resampled, dist_rescal.py:208-213); one thread per row,
+// one jump per stored entry to e = (t*n + i)*n + j.
+template <typename T>
+__global__ void __launch_bounds__(256) perturb_csr_vals(T* __restrict__ val, const int64_t* __restrict__ indptr,
+                                                        const int* __restrict__ indices, int64_t rows, int64_t t,
+                                                        int64_t n, u128 state, u128 inc, double delta) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+      const uint64_t el = (uint64_t)((t * n + i) * n + indices[p]);
+      u128 s = pcg_advance(state, inc, el);
+      const double u = pcg_next_double(s, inc);
+      val[p] = val[p] * (T)pcg_field(u, delta);
+    }
+  }
 }
 
 // Perturb the device tensor: X'[t][il][jl] = X0[t][il][jl] * f(e), with
@@ -1439,7 +1496,7 @@ __global__ void __launch_bounds__(kThreads) perturb_planes(
       if (e != next_e) s = pcg_advance(state, inc, (uint64_t)e);
       double u = pcg_next_double(s, inc);
       next_e = e + 1;
-      double f = 1.0 + delta * (2.0 * u - 1.0);
+      double f = pcg_field(u, delta);
       size_t off = ((size_t)t * NR + il) * NC + jl;
       double x = (double)join_bf16(Xh0[off], Xl0[off]);
       double v = dtype_f32 ? (double)((float)x * (float)f) : x * f;

@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(256) sp_perturb(const int64_t* __restrict__ pt
       const uint64_t el = (uint64_t)(((int64_t)t * n_global + i) * n_global + j);
       u128 s = pcg_advance(state, inc, el);
       const double u = pcg_next_double(s, inc);
-      const double f = 1.0 + delta * (2.0 * u - 1.0);
+      const double f = pcg_field(u, delta);
       val[p] = (float)((double)val0[p] * f);
     }
   }

@@ -43,6 +43,39 @@ class PerturbConfig:
             raise DataError(f"delta must be > 0, got {self.delta}")
 
 
+def perturbation_field(n: int, m: int, pcfg: PerturbConfig, q, dtype=np.float64, device: int = 0) -> np.ndarray:
+    """The full (m, n, n) multiplier field for perturbation q
+    (dist_rescal.py:164-171), drawn on the device, bit-exact with numpy."""
+    out = np.empty((m, n, n), dtype=np.dtype(dtype))
+    if out.dtype not in (np.float32, np.float64):
+        raise DataError(f"unsupported field dtype {out.dtype}")
+    _lib.perturb_values((pcfg.base_seed, _SEED_TAG_PERTURB, q), pcfg.delta, out, 0, True, device)
+    return out
+
+
+def perturb(x, pcfg: PerturbConfig, q, device: int = 0):
+    """Whole-tensor resampling with the reference's multiplier field
+    (dist_rescal.py:205-215): dense x * field.astype(x.dtype); sparse tensors
+    keep their pattern and only the stored values are resampled. Computed on
+    the device (no (m, n, n) fp64 field on the host)."""
+    from .containers import RelTensor, SparseRelTensor, is_sparse
+    import scipy.sparse as sps
+
+    key = (pcfg.base_seed, _SEED_TAG_PERTURB, q)
+    if is_sparse(x):
+        slices = []
+        for t, s in enumerate(x.slices):
+            data = np.array(s.data, dtype=s.dtype if s.dtype in (np.float32, np.float64) else np.float64)
+            _lib.perturb_csr_values(key, pcfg.delta, t, x.n, s.indptr, s.indices, data, device)
+            slices.append(sps.csr_matrix((data, s.indices.copy(), s.indptr.copy()), shape=s.shape))
+        return SparseRelTensor(slices, n=x.n)
+    xs = np.array(x.slices, order="C", copy=True)
+    if xs.dtype not in (np.float32, np.float64):
+        xs = xs.astype(np.float64)
+    _lib.perturb_values(key, pcfg.delta, xs, 0, False, device)
+    return RelTensor(xs)
+
+
 # ---------------------------------------------------------------------------
 # host-side k x k math
 
