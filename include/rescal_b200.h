@@ -152,6 +152,20 @@ int rk_perturb_csr_values(int32_t device, uint64_t state_hi, uint64_t state_lo, 
                           double delta, int32_t dtype, int64_t t, int64_t n, const int64_t* indptr,
                           const int32_t* indices, void* values, int64_t nnz);
 
+/* NNDSVD support (nndsvd_init, rescal.py:327-372): products with the
+ * unfolding M = [X_1 .. X_m | X_1^T .. X_m^T] (n x 2nm) of the handle's
+ * tensor, for a device subspace iteration in place of the reference's
+ * LAPACK SVD / ARPACK svds of M (rescal.py:341-352). V, U, Y are n x b
+ * row-major fp64; b <= 256 (dense) or b in {16, 32} (sparse).
+ *   rk_gram_apply:        Y = M M^T V = sum_t X_t (X_t^T V) + X_t^T (X_t V)
+ *   rk_unfold_sign_norms: per column c of M^T U, the squared norms of its
+ *                         positive and negative parts (the yp / ym norms of
+ *                         rescal.py:357-360 before the 1/s scaling)
+ *   rk_positive_mean:     mean of the positive stored entries (rescal.py:375-383) */
+int rk_gram_apply(rk_handle* h, const double* V, int32_t b, double* Y);
+int rk_unfold_sign_norms(rk_handle* h, const double* U, int32_t b, double* pos2, double* neg2);
+int rk_positive_mean(rk_handle* h, double* mean);
+
 /* Raw PCG64 draws u_{offset} .. u_{offset+count-1} (tests of the generator). */
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
                    int64_t count, double* out);

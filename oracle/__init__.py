@@ -21,6 +21,7 @@ from .mu_oracle import (  # noqa: F401
     canonical_csr,
     finalize_normalize,
     mu_iteration,
+    nndsvd_init,
     perturbation_field,
     perturb_dense,
     perturb_sparse,

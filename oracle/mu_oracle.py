@@ -200,6 +200,59 @@ def regress_r(xs, a, eps=1e-16, max_iters=500, tol=1e-8):
 
 
 # --------------------------------------------------------------------------
+# NNDSVD start
+
+
+def nndsvd_init(xs, k, r_update_iters=20, eps=1e-16):
+    """rescal.py:327-372 — A from the non-negative parts of the leading
+    singular triplets of [X_1 .. X_m | X_1^T .. X_m^T] (LAPACK SVD for dense
+    slices, ARPACK svds for sparse ones with k < n, :341-352), zeros filled
+    with 1e-2 x the mean positive entry (:366-368, :375-383), then
+    `r_update_iters` Jacobi R sweeps from all-ones with tol None (:370)."""
+    import scipy.sparse.linalg as spla
+
+    n = xs[0].shape[0]
+    sparse_input = sp.issparse(xs[0])
+    if sparse_input:
+        mm = sp.hstack([*(o.tocsr() for o in xs), *(o.T.tocsr() for o in xs)], format="csr")
+    else:
+        mm = np.concatenate([*xs, *(o.T for o in xs)], axis=1)
+    if sparse_input and k < n:
+        u, s, vt = spla.svds(mm.astype(np.float64), k=k)
+        order = np.argsort(s)[::-1]
+        u, s, vt = u[:, order], s[order], vt[order]
+    else:
+        dense = mm.toarray() if sparse_input else np.asarray(mm, dtype=np.float64)
+        u, s, vt = np.linalg.svd(dense, full_matrices=False)
+        u, s, vt = u[:, :k], s[:k], vt[:k]
+    a = np.zeros((n, k))
+    lead = u[:, 0] if u[:, 0].sum() >= 0 else -u[:, 0]
+    a[:, 0] = np.sqrt(s[0]) * np.maximum(lead, 0.0)
+    for j in range(1, k):
+        xu, yv = u[:, j], vt[j]
+        xp, xm = np.maximum(xu, 0.0), np.maximum(-xu, 0.0)
+        yp, ym = np.maximum(yv, 0.0), np.maximum(-yv, 0.0)
+        mu_p = np.linalg.norm(xp) * np.linalg.norm(yp)
+        mu_m = np.linalg.norm(xm) * np.linalg.norm(ym)
+        if max(mu_p, mu_m) <= 0 or s[j] <= 0:
+            continue
+        part, norm = (xp, np.linalg.norm(xp)) if mu_p >= mu_m else (xm, np.linalg.norm(xm))
+        a[:, j] = np.sqrt(s[j] * max(mu_p, mu_m)) * part / norm
+    total, count = 0.0, 0
+    for o in xs:
+        vals = np.asarray(o.data) if sp.issparse(o) else np.asarray(o).ravel()
+        vals = vals[vals > 0]
+        total += float(vals.sum())
+        count += vals.size
+    positives = total / count if count else 0.0
+    a[a == 0] = 1e-2 * positives if positives > 0 else 1e-2
+    dt = xs[0].dtype
+    a = a.astype(dt)
+    r = regress_r(xs, a, eps=eps, max_iters=r_update_iters, tol=None)
+    return a, r
+
+
+# --------------------------------------------------------------------------
 # perturbation (RESCALk resampling)
 
 

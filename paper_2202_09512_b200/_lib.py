@@ -67,6 +67,9 @@ SIGNATURES = {
     "rk_set_option": (ctypes.c_int, [_vp, _i32, _i64]),
     "rk_uniform_values": (ctypes.c_int, [_u64, _i64, _i64, _pf]),
     "rk_pcg64_draws": (ctypes.c_int, [_u64, _u64, _u64, _u64, _u64, _i64, _pd]),
+    "rk_gram_apply": (ctypes.c_int, [_vp, _pd, _i32, _pd]),
+    "rk_unfold_sign_norms": (ctypes.c_int, [_vp, _pd, _i32, _pd, _pd]),
+    "rk_positive_mean": (ctypes.c_int, [_vp, _pd]),
     "rk_perturb_values": (ctypes.c_int, [_i32, _u64, _u64, _u64, _u64, _f64, _i32, _vp, _i64, _u64, _i32]),
     "rk_perturb_csr_values": (ctypes.c_int, [_i32, _u64, _u64, _u64, _u64, _f64, _i32, _i64, _i64, _pi64,
                                              ctypes.POINTER(ctypes.c_int32), _vp, _i64]),
@@ -194,6 +197,27 @@ class Engine:
                                              ctypes.cast(dv, _vp), nnz.ctypes.data_as(_pi64),
                                              RK_F32 if dt == np.float32 else RK_F64))
         del keep
+
+    # ---- NNDSVD support (products with the unfolding M = [X_t | X_t^T]) ----
+    def gram_apply(self, v: np.ndarray) -> np.ndarray:
+        """Y = M M^T V for an (n, b) block V (fp64 result)."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        y = np.empty_like(v)
+        check(self._lib.rk_gram_apply(self._h, _dp(v), int(v.shape[1]), _dp(y)))
+        return y
+
+    def unfold_sign_norms(self, u: np.ndarray):
+        """Squared norms of the positive / negative parts of each column of M^T U."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        pos = np.empty(u.shape[1])
+        neg = np.empty(u.shape[1])
+        check(self._lib.rk_unfold_sign_norms(self._h, _dp(u), int(u.shape[1]), _dp(pos), _dp(neg)))
+        return pos, neg
+
+    def positive_mean(self) -> float:
+        out = _f64(0.0)
+        check(self._lib.rk_positive_mean(self._h, ctypes.byref(out)))
+        return float(out.value)
 
     def fill_sparse_uniform(self, seed, nnz_per_slice):
         """Synthetic uniform-random sparse slices generated on the device."""

@@ -1983,6 +1983,148 @@ int rk_perturb_csr_values(int32_t device, uint64_t state_hi, uint64_t state_lo, 
   });
 }
 
+// ---- NNDSVD support (rescal.py:327-372): products with the unfolding
+// M = [X_1 .. X_m | X_1^T .. X_m^T] for the device subspace iteration.
+namespace {
+struct UnfoldBufs {
+  float *V = nullptr, *P1 = nullptr, *Q1 = nullptr;
+  ~UnfoldBufs() {
+    dfree(V);
+    dfree(P1);
+    dfree(Q1);
+  }
+};
+
+void check_unfold(rk_handle* h, int b) {
+  RK_REQUIRE(h != nullptr, RK_ERR_DATA, "null handle");
+  RK_REQUIRE(h->have_x, RK_ERR_DATA, "no tensor uploaded");
+  RK_REQUIRE(!h->grid(), RK_ERR_GRID, "unfolding products run on a single-GPU handle");
+  if (h->sparse)
+    RK_REQUIRE(b == 16 || b == 32, RK_ERR_DATA, "sparse unfolding products need a block width of 16 or 32");
+  else
+    RK_REQUIRE(b >= 1 && b <= 256, RK_ERR_DATA, "dense unfolding products need 1 <= block width <= 256");
+  RK_CUDA(cudaSetDevice(h->dev));
+}
+
+// out_p[t] = X_t B(t), out_q[t] = X_t^T B'(t); B(t) = V + t*sv, B'(t) = W + t*sw
+void unfold_products(rk_handle* h, int b, const float* V, int64_t sv, const float* W, int64_t sw, float* out_p,
+                     float* out_q) {
+  const int M = (int)h->m;
+  if (h->sparse) {
+    const int grid = h->num_sms * 16;
+    if (b == 16) {
+      rk::sp::sp_csr_pass<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, V, out_p,
+                                                          (int)h->rows_valid, (int)h->NR, M, 0, sv);
+      rk::sp::sp_csr_pass<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, W, out_q,
+                                                          (int)h->cols_valid, (int)h->NC, M, 0, sw);
+    } else {
+      rk::sp::sp_csr_pass<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->csr_ptr, h->csr_idx, h->csr_val, V, out_p,
+                                                          (int)h->rows_valid, (int)h->NR, M, 0, sv);
+      rk::sp::sp_csr_pass<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, W, out_q,
+                                                          (int)h->cols_valid, (int)h->NC, M, 0, sw);
+    }
+  } else {
+    const size_t smem = (size_t)(64 * 33 + 64 * b) * sizeof(float);
+    RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rk::k1_simt_p<<<dim3((unsigned)(h->NR / 32), M), rk::kThreads, smem, h->stream>>>(
+        h->ctl, h->Xh, h->Xl, V, out_p, (int)h->NR, (int)h->NC, b, 0, sv);
+    rk::k1_simt_q<<<dim3((unsigned)(h->NC / 32), M), rk::kThreads, smem, h->stream>>>(
+        h->ctl, h->Xh, h->Xl, W, out_q, (int)h->NR, (int)h->NC, b, 0, sw);
+  }
+  RK_CUDA(cudaGetLastError());
+}
+
+float* upload_block_cols(rk_handle* h, const double* V, int b) {
+  const int64_t n = h->n, ld = std::max(h->NR, h->NC);
+  std::vector<float> v32((size_t)ld * b, 0.f);
+  for (int64_t e = 0; e < n * b; ++e) v32[e] = (float)V[e];
+  float* d = dalloc<float>(v32.size());
+  RK_CUDA(cudaMemcpy(d, v32.data(), sizeof(float) * v32.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+}  // namespace
+
+int rk_gram_apply(rk_handle* h, const double* V, int32_t b, double* Y) {
+  return guarded([&] {
+    check_unfold(h, b);
+    RK_REQUIRE(V && Y, RK_ERR_DATA, "null argument");
+    const int64_t M = h->m, n = h->n, ld = std::max(h->NR, h->NC);
+    UnfoldBufs u;
+    u.V = upload_block_cols(h, V, b);
+    u.P1 = dalloc<float>((size_t)M * ld * b);
+    u.Q1 = dalloc<float>((size_t)M * ld * b);
+    float* P2 = dalloc<float>((size_t)M * ld * b);
+    float* Q2 = dalloc<float>((size_t)M * ld * b);
+    double* Yd = dalloc<double>((size_t)n * b);
+    unfold_products(h, b, u.V, 0, u.V, 0, u.P1, u.Q1);                      // X_t V, X_t^T V
+    unfold_products(h, b, u.Q1, ld * b, u.P1, ld * b, P2, Q2);             // X_t (X_t^T V), X_t^T (X_t V)
+    rk::sum_slices<<<h->num_sms * 4, 256, 0, h->stream>>>(P2, Q2, (int)M, n, ld, b, Yd);
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    RK_CUDA(cudaMemcpy(Y, Yd, sizeof(double) * n * b, cudaMemcpyDeviceToHost));
+    dfree(P2);
+    dfree(Q2);
+    dfree(Yd);
+  });
+}
+
+int rk_unfold_sign_norms(rk_handle* h, const double* U, int32_t b, double* pos2, double* neg2) {
+  return guarded([&] {
+    check_unfold(h, b);
+    RK_REQUIRE(U && pos2 && neg2, RK_ERR_DATA, "null argument");
+    const int64_t M = h->m, n = h->n, ld = std::max(h->NR, h->NC);
+    UnfoldBufs u;
+    u.V = upload_block_cols(h, U, b);
+    u.P1 = dalloc<float>((size_t)M * ld * b);
+    u.Q1 = dalloc<float>((size_t)M * ld * b);
+    unfold_products(h, b, u.V, 0, u.V, 0, u.P1, u.Q1);
+    const int nblk = h->num_sms;
+    double* part = dalloc<double>((size_t)nblk * 2 * b);
+    rk::sign_norms<<<dim3(nblk, b), 256, 256 * 2 * sizeof(double), h->stream>>>(u.P1, u.Q1, (int)M, n, ld, b, part);
+    RK_CUDA(cudaGetLastError());
+    std::vector<double> ph((size_t)nblk * 2 * b);
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    RK_CUDA(cudaMemcpy(ph.data(), part, sizeof(double) * ph.size(), cudaMemcpyDeviceToHost));
+    dfree(part);
+    for (int c = 0; c < b; ++c) {
+      double a = 0.0, z = 0.0;
+      for (int k = 0; k < nblk; ++k) {
+        a += ph[(size_t)k * 2 * b + c];
+        z += ph[(size_t)k * 2 * b + b + c];
+      }
+      pos2[c] = a;
+      neg2[c] = z;
+    }
+  });
+}
+
+int rk_positive_mean(rk_handle* h, double* mean) {
+  return guarded([&] {
+    RK_REQUIRE(h && mean, RK_ERR_DATA, "null argument");
+    RK_REQUIRE(h->have_x, RK_ERR_DATA, "no tensor uploaded");
+    RK_CUDA(cudaSetDevice(h->dev));
+    const int nblk = h->num_sms * 2;
+    double* part = dalloc<double>((size_t)nblk * 2);
+    if (h->sparse)
+      rk::positive_sum_flat<<<nblk, 256, 0, h->stream>>>(h->csr_val, h->nnz, part);
+    else
+      rk::positive_sum<<<nblk, 256, 0, h->stream>>>(h->Xh, h->Xl, (int)h->m, h->NR, h->NC, h->rows_valid,
+                                                     h->cols_valid, part);
+    RK_CUDA(cudaGetLastError());
+    std::vector<double> ph((size_t)nblk * 2);
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    RK_CUDA(cudaMemcpy(ph.data(), part, sizeof(double) * ph.size(), cudaMemcpyDeviceToHost));
+    dfree(part);
+    double s = 0.0, c = 0.0;
+    for (int k = 0; k < nblk; ++k) {
+      s += ph[2 * k];
+      c += ph[2 * k + 1];
+    }
+    *mean = c > 0 ? s / c : 0.0;
+  });
+}
+
 int rk_nccl_unique_id(void* out128) {
   return guarded([&] {
     ncclUniqueId id;

@@ -949,10 +949,14 @@ __global__ void __launch_bounds__(kThreads) k1_simt_p(const Ctl* __restrict__ ct
                                                       const __nv_bfloat16* __restrict__ Xl,
                                                       const float* __restrict__ A32col,
                                                       float* __restrict__ P, int NR, int NC,
-                                                      int K, int skip_if_stopped) {
+                                                      int K, int skip_if_stopped,
+                                                      int64_t a_stride = 0) {
+  // a_stride > 0: slice t multiplies its own operand A32col + t * a_stride
+  // (the NNDSVD Gram products sum_t X_t B_t, rk_gram_apply)
   if (skip_if_stopped && ctl->stop) return;
   extern __shared__ float shf[];
   constexpr int BR = 32, BC = 64;
+  A32col += (size_t)blockIdx.y * a_stride;
   float* xs = shf;             // [BR][BC+1]
   float* as = shf + BR * (BC + 1);  // [BC][K]
   const int t = blockIdx.y;
@@ -991,8 +995,10 @@ __global__ void __launch_bounds__(kThreads) k1_simt_q(const Ctl* __restrict__ ct
                                                       const __nv_bfloat16* __restrict__ Xl,
                                                       const float* __restrict__ A32row,
                                                       float* __restrict__ Qo, int NR, int NC,
-                                                      int K, int skip_if_stopped) {
+                                                      int K, int skip_if_stopped,
+                                                      int64_t a_stride = 0) {
   if (skip_if_stopped && ctl->stop) return;
+  A32row += (size_t)blockIdx.y * a_stride;
   extern __shared__ float shf[];
   constexpr int BR = 64, BC = 32;
   float* xs = shf;                  // [BR][BC+1]
@@ -1332,6 +1338,97 @@ RK_DEV double pcg_out_double(u128 state) {
   unsigned rot = (unsigned)(state.hi >> 58);
   uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
   return (double)(out >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ---- NNDSVD helpers (rescal.py:327-372) -----------------------------------
+// Y[i][c] = sum_t A[t][i][c] + B[t][i][c] (fp64), rows < n of per-slice
+// [ld][b] fp32 blocks: the two halves of G V = sum_t X_t (X_t^T V) + X_t^T (X_t V).
+__global__ void __launch_bounds__(256) sum_slices(const float* __restrict__ A, const float* __restrict__ B,
+                                                  int M, int64_t n, int64_t ld, int b, double* __restrict__ Y) {
+  const int64_t total = n * b;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / b;
+    const int c = (int)(e - i * b);
+    double s = 0.0;
+    for (int t = 0; t < M; ++t) {
+      const size_t o = ((size_t)t * ld + i) * b + c;
+      s += (double)A[o] + (double)B[o];
+    }
+    Y[e] = s;
+  }
+}
+
+// Squared norms of the positive and negative parts of every column c of the
+// stacked [P_1..P_m ; Q_1..Q_m] (= M^T U for the unfolding M = [X_t | X_t^T]):
+// part[blk][c] and part[blk][b + c], fixed block order.
+__global__ void __launch_bounds__(256) sign_norms(const float* __restrict__ P, const float* __restrict__ Q, int M,
+                                                  int64_t n, int64_t ld, int b, double* __restrict__ part) {
+  extern __shared__ double sn[];  // [256][2]
+  const int c = blockIdx.y;
+  double pos = 0.0, neg = 0.0;
+  const int64_t total = (int64_t)M * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / n, i = e - t * n;
+    const size_t o = ((size_t)t * ld + i) * b + c;
+    const double p = P[o], q = Q[o];
+    pos += (p > 0 ? p * p : 0.0) + (q > 0 ? q * q : 0.0);
+    neg += (p < 0 ? p * p : 0.0) + (q < 0 ? q * q : 0.0);
+  }
+  sn[2 * threadIdx.x] = pos;
+  sn[2 * threadIdx.x + 1] = neg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, z = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      a += sn[2 * i];
+      z += sn[2 * i + 1];
+    }
+    part[(size_t)blockIdx.x * 2 * b + c] = a;
+    part[(size_t)blockIdx.x * 2 * b + b + c] = z;
+  }
+}
+
+// Sum and count of the positive entries of the stored dense tensor (planes).
+__global__ void __launch_bounds__(256) positive_sum(const __nv_bfloat16* __restrict__ Xh,
+                                                    const __nv_bfloat16* __restrict__ Xl, int M, int64_t NR,
+                                                    int64_t NC, int64_t rows, int64_t cols, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0, c = 0.0;
+  const int64_t total = (int64_t)M * rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / (rows * cols), r = (e / cols) % rows, j = e % cols;
+    const size_t o = ((size_t)t * NR + r) * NC + j;
+    const double v = (double)join_bf16(Xh[o], Xl[o]);
+    if (v > 0) {
+      s += v;
+      c += 1.0;
+    }
+  }
+  s = block_sum(s, red);
+  c = block_sum(c, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) positive_sum_flat(const float* __restrict__ v, int64_t count,
+                                                         double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0, c = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[e];
+    if (x > 0) {
+      s += x;
+      c += 1.0;
+    }
+  }
+  s = block_sum(s, red);
+  c = block_sum(c, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = c;
+  }
 }
 
 // The multiplier 1 + delta (2u - 1) with every operation rounded separately,

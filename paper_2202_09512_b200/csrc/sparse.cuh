@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
                                                       const float* __restrict__ val,
                                                       const float* __restrict__ A32,
                                                       float* __restrict__ P, int n, int Npad, int M,
-                                                      int skip_if_stopped) {
+                                                      int skip_if_stopped, int64_t a_stride = 0) {
+  // a_stride > 0: slice t gathers from its own table A32 + t * a_stride (the
+  // NNDSVD Gram products sum_t X_t B_t, rk_gram_apply)
   if (skip_if_stopped && ctl->stop) return;
   constexpr int G = K / 4;
   const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
   for (; t < M;) {
     const int64_t* pt = ptr + (size_t)t * (n + 1);
     const int64_t b = pt[i], e = pt[i + 1];
+    const float* At = A32 + (size_t)t * a_stride;
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t p = b;
     for (; p + 4 <= e; p += 4) {
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
         v[u] = ld_stream(val + p + u, pf);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = ld_gather(A32 + (size_t)j[u] * K + 4 * q, pl);
+      for (int u = 0; u < 4; ++u) a[u] = ld_gather(At + (size_t)j[u] * K + 4 * q, pl);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         y.x = fmaf(v[u], a[u].x, y.x);
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
     for (; p < e; ++p) {
       const int j = ld_stream(idx + p, pf);
       const float v = ld_stream(val + p, pf);
-      const float4 a = ld_gather(A32 + (size_t)j * K + 4 * q, pl);
+      const float4 a = ld_gather(At + (size_t)j * K + 4 * q, pl);
       y.x = fmaf(v, a.x, y.x);
       y.y = fmaf(v, a.y, y.y);
       y.z = fmaf(v, a.z, y.z);

@@ -266,7 +266,11 @@ def best_match_diagonal(corr: np.ndarray) -> np.ndarray:
 
 def _solve_member(eng, x, k, q, cfg, pcfg, dt):
     eng.perturb((pcfg.base_seed, _SEED_TAG_PERTURB, (k, q)), pcfg.delta)
-    init = random_init(x.n, k, x.m, (cfg.seed, _SEED_TAG_ENSEMBLE, k, q), dtype=dt)
+    if cfg.init == "nndsvd":  # model_select.py:461-462, on the resampled device tensor
+        from .solver import nndsvd_init
+        init = nndsvd_init(x, k, eps=cfg.epsilon, cfg=cfg, engine=eng)
+    else:
+        init = random_init(x.n, k, x.m, (cfg.seed, _SEED_TAG_ENSEMBLE, k, q), dtype=dt)
     f, trace = rescal_solve(x, k, cfg, initial=init, engine=eng)
     f = finalize_normalize(f)
     solved = len(trace) == 0 or bool(np.isfinite(trace[-1]))
@@ -289,8 +293,6 @@ def rescalk(x, k_min: int, k_max: int, r: int, cfg: SolverConfig | None = None,
         raise DataError(f"need 1 <= k_min <= k_max <= n, got [{k_min}, {k_max}], n={x.n}")
     if r < 2:
         raise DataError(f"need r >= 2 perturbations, got {r}")
-    if cfg.init == "nndsvd":
-        raise DataError("init='nndsvd' is not available on the device engine")
     rank, size = world if world is not None else (0, 1)
     dt = tensor_dtype(x)
     t_start = time.perf_counter()

@@ -152,16 +152,16 @@ def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, count
         f = initial.copy()
         if f.A.shape != (x.n, k) or f.R.shape != (x.m, k, k):
             raise DataError("initial factors do not match tensor/k")
-    elif cfg.init == "nndsvd":
-        raise DataError("init='nndsvd' is not available on the device engine (SURVEY.md §8(f)4)")
     else:
-        f = random_init(x.n, k, x.m, cfg.seed, dtype=dt)
-    # the reference casts the start to x.dtype (rescal.py:206-208)
-    a0 = _to_dtype(f.A, dt).astype(np.float64)
-    r0 = _to_dtype(f.R, dt).astype(np.float64)
+        f = None if cfg.init == "nndsvd" else random_init(x.n, k, x.m, cfg.seed, dtype=dt)
     own = engine is None
     eng = engine if engine is not None else _engine_for(x, k, cfg)
     try:
+        if f is None:  # rescal.py:202-203
+            f = nndsvd_init(x, k, eps=cfg.epsilon, cfg=cfg, engine=eng)
+        # the reference casts the start to x.dtype (rescal.py:206-208)
+        a0 = _to_dtype(f.A, dt).astype(np.float64)
+        r0 = _to_dtype(f.R, dt).astype(np.float64)
         if eng.k != k:
             eng.set_rank(k)
         eng.set_factors(a0, r0)
@@ -244,6 +244,97 @@ def regress_r(x, a_fixed: np.ndarray, cfg: SolverConfig | None = None, max_iters
     return r.astype(a.dtype)
 
 
-def nndsvd_init(x, k: int, r_update_iters: int = 20, eps: float = 1e-16) -> RescalFactors:
-    """Not on the device path (SURVEY.md §8(f)4 ranks it 'next')."""
-    raise DataError("nndsvd_init is not implemented on the B200 engine; pass initial= factors")
+def _nndsvd_block(eng, n: int, k: int) -> int:
+    if eng.sparse:
+        if k > 32:
+            raise DataError("nndsvd_init on the sparse engine supports k <= 32")
+        return 16 if k + 4 <= 16 else 32
+    b = min(n, k + 8)
+    if b > 256:
+        raise DataError("nndsvd_init on the device supports k <= 248")
+    return b
+
+
+def _leading_singular(eng, n: int, k: int, max_iters: int = 300, rtol: float = 1e-10):
+    """Top-k left singular vectors / values of the unfolding M = [X_t | X_t^T]
+    by subspace iteration on M M^T (device products, rk_gram_apply) with a
+    Rayleigh-Ritz step; the reference takes them from a full LAPACK SVD
+    (dense) or ARPACK svds (sparse) of M (rescal.py:341-352). Deterministic:
+    fixed start block."""
+    b = _nndsvd_block(eng, n, k)
+
+    def orth(z):
+        q, _ = np.linalg.qr(z)
+        if q.shape[1] < b:  # n < b: keep the block width the kernels expect
+            q = np.concatenate([q, np.zeros((n, b - q.shape[1]))], axis=1)
+        return q
+
+    v = orth(np.random.default_rng(20220218).standard_normal((n, b)))
+    prev = None
+    for it in range(max_iters):
+        y = eng.gram_apply(v)
+        t = v.T @ y
+        lam = np.sort(np.linalg.eigvalsh(0.5 * (t + t.T)))[::-1][:k]
+        scale = max(abs(lam[0]), np.finfo(float).tiny)
+        if prev is not None and it >= 8 and np.max(np.abs(lam - prev)) <= rtol * scale:
+            break
+        prev = lam
+        v = orth(y)
+    y = eng.gram_apply(v)
+    t = v.T @ y
+    w, wv = np.linalg.eigh(0.5 * (t + t.T))
+    order = np.argsort(w)[::-1][:k]
+    u = v @ wv[:, order]
+    s = np.sqrt(np.maximum(w[order], 0.0))
+    return u, s, b
+
+
+def _nndsvd_factor(eng, n: int, k: int) -> np.ndarray:
+    """The A of nndsvd_init (rescal.py:354-370) from device singular data."""
+    u, s, b = _leading_singular(eng, n, k)
+    upad = np.zeros((n, b))
+    upad[:, :k] = u
+    pos2, neg2 = eng.unfold_sign_norms(upad if eng.sparse else upad[:, :max(k, 1)])
+    a = np.zeros((n, k))
+    lead = u[:, 0] if u[:, 0].sum() >= 0 else -u[:, 0]
+    a[:, 0] = np.sqrt(s[0]) * np.maximum(lead, 0.0)
+    for j in range(1, k):
+        if s[j] <= 0:
+            continue  # rank-deficient direction, filled below
+        xu = u[:, j]
+        xp, xm = np.maximum(xu, 0.0), np.maximum(-xu, 0.0)
+        # right singular vector v_j = M^T u_j / s_j: norms of its +/- parts
+        yp, ym = np.sqrt(pos2[j]) / s[j], np.sqrt(neg2[j]) / s[j]
+        mu_p = np.linalg.norm(xp) * yp
+        mu_m = np.linalg.norm(xm) * ym
+        if max(mu_p, mu_m) <= 0:
+            continue
+        part, norm = (xp, np.linalg.norm(xp)) if mu_p >= mu_m else (xm, np.linalg.norm(xm))
+        a[:, j] = np.sqrt(s[j] * max(mu_p, mu_m)) * part / norm
+    positives = eng.positive_mean()
+    fill = 1e-2 * positives if positives > 0 else 1e-2
+    a[a == 0] = fill
+    return a
+
+
+def nndsvd_init(x, k: int, r_update_iters: int = 20, eps: float = 1e-16, cfg: SolverConfig | None = None,
+                engine: "_lib.Engine | None" = None) -> RescalFactors:
+    """Deterministic NNDSVD start (rescal.py:327-372): A from the non-negative
+    parts of the leading singular vectors of [X_1 .. X_m | X_1^T .. X_m^T],
+    zeros filled with 1e-2 x the mean positive entry, then `r_update_iters`
+    R refits with A fixed. The singular vectors come from a device subspace
+    iteration (products with the unfolding on the GPU); ``engine`` (extension)
+    reuses a device-resident tensor."""
+    if not 1 <= k <= x.n:
+        raise DataError(f"need 1 <= k <= n, got k={k}, n={x.n}")
+    cfg = cfg or SolverConfig()
+    own = engine is None
+    eng = engine if engine is not None else _engine_for(x, k, cfg)
+    try:
+        a = _nndsvd_factor(eng, x.n, k).astype(tensor_dtype(x))
+        r = regress_r(x, a, SolverConfig(epsilon=eps, device=cfg.device), max_iters=r_update_iters, tol=None,
+                      engine=eng)
+    finally:
+        if own:
+            eng.close()
+    return RescalFactors(a, r)

@@ -162,6 +162,19 @@ def main():
     pl["p16_3_3_s7_ped_rescalk_rel_error"] = np.array(rep7.entries[0].rel_error)
     out["planted_inputs"] = pl
 
+    # 15. NNDSVD start (rescal.py:327-372): dense full-SVD branch and the sparse
+    #     ARPACK svds branch, on the planted tensor of case 2 (well separated
+    #     leading singular values), plus a short nndsvd-initialised solve
+    fn = rk.nndsvd_init(xp, 4)
+    fs, trs = rk.rescal_solve(xp, 4, rk.SolverConfig(max_iters=50, init="nndsvd"))
+    xsp2 = rk.sparsify(xp, 0.9)  # no all-zero rows: u has no structural zeros
+    fsp = rk.nndsvd_init(xsp2, 3)
+    out["nndsvd64"] = dict(X=xp.slices, A=fn.A, R=fn.R, A50=fs.A, R50=fs.R, trace50=trs,
+                           sp_indptr=np.stack([q.indptr for q in xsp2.slices]),
+                           sp_indices=np.concatenate([q.indices for q in xsp2.slices]),
+                           sp_data=np.concatenate([q.data for q in xsp2.slices]),
+                           sp_nnz=np.array([q.nnz for q in xsp2.slices]), spA=fsp.A, spR=fsp.R)
+
     import numpy, scipy
     meta = dict(numpy=numpy.__version__, scipy=scipy.__version__, reference=REF)
     for name, d in out.items():

@@ -163,3 +163,18 @@ def test_rescalk_oracle_matches_reference():
         assert k == int(k_ref)
         assert abs(s_min - smr) <= 1e-10 and abs(s_avg - sar) <= 1e-10 and abs(err - er) <= 1e-10
         np.testing.assert_allclose(rep["medians"][k], g[f"medians_k{k}"], atol=1e-10)
+
+
+def test_nndsvd_oracle_matches_reference():
+    g = golden("nndsvd64")
+    a, r = oracle.nndsvd_init(_slices(g["X"]), 4)
+    assert rel_fro(a, g["A"]) <= TIGHT and rel_fro(r, g["R"]) <= TIGHT
+    slices, off = [], 0
+    for t in range(len(g["sp_nnz"])):
+        nz = int(g["sp_nnz"][t])
+        slices.append(sp.csr_matrix((g["sp_data"][off:off + nz], g["sp_indices"][off:off + nz],
+                                     g["sp_indptr"][t]), shape=(64, 64)))
+        off += nz
+    a2, r2 = oracle.nndsvd_init(slices, 3)
+    # ARPACK's start vector is random: agreement to the solver tolerance
+    assert rel_fro(a2, g["spA"]) <= 1e-8 and rel_fro(r2, g["spR"]) <= 1e-8
