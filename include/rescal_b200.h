@@ -152,6 +152,21 @@ int rk_perturb_csr_values(int32_t device, uint64_t state_hi, uint64_t state_lo, 
                           double delta, int32_t dtype, int64_t t, int64_t n, const int64_t* indptr,
                           const int32_t* indices, void* values, int64_t nnz);
 
+/* Tensor-file ingest (host only, no GPU needed), csrc/ingest.cpp: parse a
+ * `%rescalk-coo` text file (replaces tensor.py:260-300 _load_sparse, a
+ * pure-Python line loop) into canonical per-slice CSR arrays (tensor.py:96-104
+ * canonical form: duplicates summed, columns sorted, zeros dropped) with the
+ * reference's validation rules and error texts. rk_coo_open returns
+ * RK_ERR_DATA with rk_coo_last_error() on malformed input; then for each
+ * slice t: rk_coo_slice_nnz(h, t) entries, rk_coo_fill copies indptr (n+1,
+ * starting at 0), column ids and fp64 values. */
+typedef struct rk_coo rk_coo;
+int rk_coo_open(const char* path, rk_coo** out, int64_t* n, int64_t* m, int64_t* nnz);
+const char* rk_coo_last_error(void);
+int64_t rk_coo_slice_nnz(const rk_coo* h, int64_t t);
+int rk_coo_fill(const rk_coo* h, int64_t t, int64_t* indptr, int32_t* indices, double* data);
+void rk_coo_close(rk_coo* h);
+
 /* NNDSVD support (nndsvd_init, rescal.py:327-372): products with the
  * unfolding M = [X_1 .. X_m | X_1^T .. X_m^T] (n x 2nm) of the handle's
  * tensor, for a device subspace iteration in place of the reference's

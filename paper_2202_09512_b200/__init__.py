@@ -39,6 +39,7 @@ from .selection import (
     select_k,
 )
 from .multigpu import grid_shape, solve_on_grid
+from .tensor_io import load_matrix, load_tensor, save_matrix, save_tensor
 from ._lib import DeviceError, Engine
 
 __version__ = "0.1.0"

@@ -67,6 +67,12 @@ SIGNATURES = {
     "rk_set_option": (ctypes.c_int, [_vp, _i32, _i64]),
     "rk_uniform_values": (ctypes.c_int, [_u64, _i64, _i64, _pf]),
     "rk_pcg64_draws": (ctypes.c_int, [_u64, _u64, _u64, _u64, _u64, _i64, _pd]),
+    "rk_coo_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "rk_coo_last_error": (ctypes.c_char_p, []),
+    "rk_coo_slice_nnz": (_i64, [_vp, _i64]),
+    "rk_coo_fill": (ctypes.c_int, [_vp, _i64, _pi64, ctypes.POINTER(ctypes.c_int32), _pd]),
+    "rk_coo_close": (None, [_vp]),
     "rk_gram_apply": (ctypes.c_int, [_vp, _pd, _i32, _pd]),
     "rk_unfold_sign_norms": (ctypes.c_int, [_vp, _pd, _i32, _pd, _pd]),
     "rk_positive_mean": (ctypes.c_int, [_vp, _pd]),

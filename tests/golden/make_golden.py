@@ -175,6 +175,48 @@ def main():
                            sp_data=np.concatenate([q.data for q in xsp2.slices]),
                            sp_nnz=np.array([q.nnz for q in xsp2.slices]), spA=fsp.A, spR=fsp.R)
 
+    # 16. %rescalk-coo ingest (tensor.py:249-300): a file written by the
+    #     reference's save_tensor, a hand-written unsorted one with duplicates,
+    #     explicit zeros and blank lines, and malformed files with the
+    #     reference's error messages
+    import tempfile
+    from rescalkit.errors import DataError as RefDataError
+    texts = {}
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "x.coo")
+        rk.save_tensor(xsp2, path)
+        texts["saved"] = open(path, encoding="utf-8").read()
+    texts["messy"] = ("%rescalk-coo 5 2 9\n"
+                      "1 4 0 2.5\n0 3 3 1e-3\n\n0 0 4 0.0\n1 4 0 0.25\n  0 3 1   7 \n"
+                      "1 2 2 +3\n0 3 3 0.125\n1 0 0 inf\n0 1 1 1.5e+2\n")
+    bad = {
+        "bad_header": "%rescalk-co 3 1 1\n0 0 0 1.0\n",
+        "bad_fields": "%rescalk-coo 3 1 2\n0 0 0 1.0\n0 1 1\n",
+        "bad_relation": "%rescalk-coo 3 1 1\n1 0 0 1.0\n",
+        "bad_index": "%rescalk-coo 3 1 1\n0 0 3 1.0\n",
+        "bad_negative": "%rescalk-coo 3 1 1\n0 0 1 -2.0\n",
+        "bad_count": "%rescalk-coo 3 1 3\n0 0 1 2.0\n0 1 1 2.0\n",
+        "bad_float": "%rescalk-coo 3 1 1\n0 0 1 abc\n",
+    }
+    coo = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, txt in list(texts.items()) + list(bad.items()):
+            path = os.path.join(td, name + ".coo")
+            with open(path, "w", encoding="utf-8") as fh:
+                fh.write(txt)
+            coo[f"{name}_text"] = np.array(txt)
+            try:
+                tt = rk.load_tensor(path)
+            except RefDataError as ex:
+                coo[f"{name}_error"] = np.array(str(ex))
+                continue
+            coo[f"{name}_n"] = np.array(tt.n)
+            for t, sl in enumerate(tt.slices):
+                coo[f"{name}_indptr{t}"] = sl.indptr
+                coo[f"{name}_indices{t}"] = sl.indices
+                coo[f"{name}_data{t}"] = sl.data
+    out["coo_ingest"] = coo
+
     import numpy, scipy
     meta = dict(numpy=numpy.__version__, scipy=scipy.__version__, reference=REF)
     for name, d in out.items():
