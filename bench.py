@@ -420,6 +420,8 @@ def run_ours(args, dist, rank, world, local_rank):
                 slices = [sps.csr_matrix((val[ptr[t, 0]:ptr[t, -1]], idx[ptr[t, 0]:ptr[t, -1]], ptr[t] - ptr[t, 0]),
                                          shape=(n, n)) for t in range(m)]
                 x = rk.SparseRelTensor(slices)  # canonical form checked outside the timed region
+                rk.rescal_solve(x, k, rk.SolverConfig(max_iters=max(1, args.warmup), track_error=False,
+                                                      device=local_rank), initial=f0)  # untimed warm-up call
                 t0 = time.perf_counter()
                 f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, track_error=False,
                                                               device=local_rank), initial=f0)
@@ -444,6 +446,9 @@ def run_ours(args, dist, rank, world, local_rank):
             elif world == 1:
                 xh = host_tensor(m, n, pinned=True)
                 x = rk.RelTensor(xh)  # validation outside the timed region, as a caller would
+                # one untimed warm-up call (module loading, allocator warm-up), as for the device timing
+                rk.rescal_solve(x, k, rk.SolverConfig(max_iters=max(1, args.warmup), track_error=False,
+                                                      device=local_rank), initial=f0)
                 t0 = time.perf_counter()
                 f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, track_error=False,
                                                               device=local_rank), initial=f0)
@@ -492,7 +497,9 @@ def run_ours(args, dist, rank, world, local_rank):
                                    "rescal_solve(RelTensor(pinned fp32 host X), k, SolverConfig(max_iters=steps, "
                                    "track_error=False))"
                                    if world == 1 else "Engine grid API: upload_block + run + get_factors"),
-                           "seconds": e2e_s, "phases": phases}
+                           "seconds": e2e_s, "phases": phases,
+                           "protocol": "one untimed warm-up call, then one timed call of `steps` iterations "
+                                       "(upload of X + solve + factor download inside the timed region)"}
         except Exception as exc:  # report, never hide
             line["e2e"] = {"value": None, "unit": "it/s", "error": repr(exc)[:300],
                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

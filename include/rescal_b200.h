@@ -181,6 +181,11 @@ int rk_gram_apply(rk_handle* h, const double* V, int32_t b, double* Y);
 int rk_unfold_sign_norms(rk_handle* h, const double* U, int32_t b, double* pos2, double* neg2);
 int rk_positive_mean(rk_handle* h, double* mean);
 
+/* Device buffers of destroyed handles are cached by the library for reuse
+ * (a caching allocator: handle teardown and re-creation skip cudaFree /
+ * cudaMalloc). This returns every cached block to the driver. */
+void rk_release_cached_memory(void);
+
 /* Raw PCG64 draws u_{offset} .. u_{offset+count-1} (tests of the generator). */
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
                    int64_t count, double* out);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "rk_coo_slice_nnz": (_i64, [_vp, _i64]),
     "rk_coo_fill": (ctypes.c_int, [_vp, _i64, _pi64, ctypes.POINTER(ctypes.c_int32), _pd]),
     "rk_coo_close": (None, [_vp]),
+    "rk_release_cached_memory": (None, []),
     "rk_gram_apply": (ctypes.c_int, [_vp, _pd, _i32, _pd]),
     "rk_unfold_sign_norms": (ctypes.c_int, [_vp, _pd, _i32, _pd, _pd]),
     "rk_positive_mean": (ctypes.c_int, [_vp, _pd]),
@@ -410,6 +411,11 @@ def perturb_csr_values(entropy, delta, t: int, n: int, indptr, indices, values: 
                                        RK_F32 if values.dtype == np.float32 else RK_F64, int(t), int(n),
                                        ip.ctypes.data_as(_pi64), ix.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                        values.ctypes.data, int(values.size)))
+
+
+def release_cached_memory() -> None:
+    """Return the library's cached device blocks to the driver."""
+    load().rk_release_cached_memory()
 
 
 def nccl_unique_id() -> bytes:

@@ -23,8 +23,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rescal_b200.h"
@@ -81,20 +84,96 @@ int guarded(F&& f) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// Process-wide device-memory cache (as PyTorch's caching allocator): freed
+// blocks are kept per (device, size class) and reused by later handles
+// (repeated rescal_solve / RESCALk members / tests), so handle teardown does
+// not pay cudaFree's unmapping and creation does not pay cudaMalloc's
+// mapping of tens of GB. Blocks are released on an allocation failure (then
+// the allocation is retried) or by rk_release_cached_memory().
+struct DevPool {
+  std::mutex mu;
+  std::unordered_map<void*, std::pair<int, size_t>> live;  // ptr -> (device, bytes)
+  std::multimap<std::pair<int, size_t>, void*> idle;        // (device, bytes) -> ptr
+};
+
+DevPool& dev_pool() {
+  static DevPool* p = new DevPool();  // process lifetime (no teardown-order hazards)
+  return *p;
+}
+
+size_t pool_class(size_t b) {
+  return b >= (1u << 20) ? (size_t)round_up((int64_t)b, 2 << 20) : (size_t)round_up((int64_t)b, 512);
+}
+
+void pool_release(int dev) {
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto it = P.idle.begin(); it != P.idle.end();) {
+    if (dev < 0 || it->first.first == dev) {
+      cudaSetDevice(it->first.first);
+      cudaFree(it->second);
+      it = P.idle.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  cudaSetDevice(cur);
+}
+
+void* pool_alloc(size_t bytes) {
+  DevPool& P = dev_pool();
+  int dev = 0;
+  RK_CUDA(cudaGetDevice(&dev));
+  const size_t b = pool_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    // best fit within 12.5 % of the request
+    auto it = P.idle.lower_bound({dev, b});
+    if (it != P.idle.end() && it->first.first == dev && it->first.second <= b + b / 8) {
+      void* p = it->second;
+      P.live[p] = it->first;
+      P.idle.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    pool_release(dev);
+    e = cudaMalloc(&p, b);
+  }
+  if (e != cudaSuccess) throw RkError{RK_ERR_DEVICE, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.live[p] = {dev, b};
+  return p;
+}
+
 template <typename T>
 T* dalloc(size_t count) {
-  void* p = nullptr;
   if (count == 0) count = 1;
-  RK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  void* p = pool_alloc(count * sizeof(T));
   RK_CUDA(cudaMemset(p, 0, count * sizeof(T)));
   // the engine stream is non-blocking w.r.t. the legacy stream the memset
-  // ran on: finish the zeroing before any engine kernel can touch the buffer
+  // ran on: finish the zeroing (and any earlier user of a reused block)
+  // before an engine kernel can touch the buffer
   RK_CUDA(cudaDeviceSynchronize());
   return static_cast<T*>(p);
 }
 
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (!p) return;
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  auto it = P.live.find(p);
+  if (it == P.live.end()) {  // not from dalloc
+    cudaFree(p);
+    return;
+  }
+  P.idle.insert({it->second, p});
+  P.live.erase(it);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -2124,6 +2203,8 @@ int rk_positive_mean(rk_handle* h, double* mean) {
     *mean = c > 0 ? s / c : 0.0;
   });
 }
+
+void rk_release_cached_memory(void) { pool_release(-1); }
 
 int rk_nccl_unique_id(void* out128) {
   return guarded([&] {
