@@ -1044,11 +1044,12 @@ void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iter
 namespace {
 // Shared tail of the CSR uploads: build the CSC copy on the device. The
 // block has `rows` CSR rows and `cols` columns per slice.
-void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
+// bounds[t] = first stored entry of slice t, bounds[M] = nnz.
+void build_csc(rk_handle* h, const std::vector<int64_t>& bounds) {
   const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
   int64_t max_nnz = 0;
   for (int64_t t = 0; t < M; ++t)
-    max_nnz = std::max(max_nnz, indptr_host[t * (rows + 1) + rows] - indptr_host[t * (rows + 1)]);
+    max_nnz = std::max(max_nnz, bounds[t + 1] - bounds[t]);
   uint64_t* keys = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
   uint64_t* keys2 = dalloc<uint64_t>((size_t)std::max<int64_t>(1, max_nnz));
   int* counts = dalloc<int>((size_t)cols);
@@ -1064,7 +1065,7 @@ void build_csc(rk_handle* h, const std::vector<int64_t>& indptr_host) {
   // asynchronous copies (filled before each copy is enqueued)
   std::vector<int64_t> ends((size_t)M);
   for (int64_t t = 0; t < M; ++t) {
-    const int64_t base = indptr_host[t * (rows + 1)], cnt = indptr_host[t * (rows + 1) + rows] - base;
+    const int64_t base = bounds[t], cnt = bounds[t + 1] - base;
     RK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * cols, h->stream));
     if (cnt > 0) {
       rk::sp::sp_make_keys<<<h->num_sms * 4, 256, 0, h->stream>>>(h->csr_ptr + t * (rows + 1), h->csr_idx,
@@ -1201,7 +1202,7 @@ void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_
   };
   const int64_t rows = h->rows_valid, cols = h->cols_valid, M = h->m;
   RK_REQUIRE(dtype == RK_F32 || dtype == RK_F64, RK_ERR_DATA, "unsupported dtype");
-  std::vector<int64_t> ptr_host((size_t)M * (rows + 1));
+  std::vector<int64_t> bounds((size_t)M + 1, 0);
   int64_t nnz = 0;
   for (int64_t t = 0; t < M; ++t) {
     RK_REQUIRE(indptrs[t] != nullptr, RK_ERR_DATA, "null indptr");
@@ -1209,6 +1210,7 @@ void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_
                "inconsistent indptr");
     RK_REQUIRE(nnz_t[t] == 0 || (indices[t] && data[t]), RK_ERR_DATA, "null argument");
     nnz += nnz_t[t];
+    bounds[(size_t)t + 1] = nnz;
   }
   void* old[] = {h->csr_ptr, h->csc_ptr, h->csr_idx, h->csc_idx, h->csr_val, h->csc_val, h->csr_val0,
                  h->csc_val0};
@@ -1239,7 +1241,6 @@ void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_
         rk::sp::sp_rebase_ptr<<<h->num_sms * 2, 256, 0, h->stream>>>(
             static_cast<const int64_t*>(d), (int64_t)(nb / 8), base, dptr + off / 8);
       });
-      for (int64_t e = 0; e <= rows; ++e) ptr_host[(size_t)t * (rows + 1) + e] = indptrs[t][e] + base;
       if (nnz_t[t] > 0) {
         up.copy(indices[t], sizeof(int32_t) * nnz_t[t], h->csr_idx + base, [&](void* d, size_t, size_t nb) {
           rk::sp::sp_check_idx<<<h->num_sms * 2, 256, 0, h->stream>>>(static_cast<const int*>(d),
@@ -1275,7 +1276,7 @@ void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_
   for (double v : ph) s2 += v;
   const double t_copy = ms_since(t_start);
   auto t_csc = now();
-  build_csc(h, ptr_host);
+  build_csc(h, bounds);
   h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
   h->have_x = true;
   h->perturbed = false;
@@ -1526,7 +1527,9 @@ int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_s
     dfree(counts);
     dfree(tmp);
     dfree(col_local);
-    build_csc(h, ptr_host);
+    std::vector<int64_t> bounds((size_t)M + 1);
+    for (int64_t t = 0; t <= M; ++t) bounds[(size_t)t] = t < M ? ptr_host[t * (rows + 1)] : h->nnz;
+    build_csc(h, bounds);
     rk::sp::sp_sq_norm<<<h->nnp, 256, 0, h->stream>>>(h->csr_val, h->nnz, h->npart);
     RK_CUDA(cudaStreamSynchronize(h->stream));
     std::vector<double> p(h->nnp);
@@ -1678,6 +1681,24 @@ int rk_set_factors(rk_handle* h, const double* A, const double* R) {
     RK_REQUIRE(h && A && R, RK_ERR_DATA, "null argument");
     RK_CUDA(cudaSetDevice(h->dev));
     const int K = h->K, k = h->k;
+    std::vector<double> r((size_t)h->m * K * K, 0.0);
+    for (int64_t t = 0; t < h->m; ++t)
+      for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) r[((size_t)t * K + a) * K + b] = R[((size_t)t * k + a) * k + b];
+    if (!h->grid()) {
+      // compact (n, k) straight to the device, padded there to (n, K)
+      double* stage = dalloc<double>((size_t)h->n * k);
+      RK_CUDA(cudaMemcpyAsync(stage, A, sizeof(double) * h->n * k, cudaMemcpyHostToDevice, h->stream));
+      rk::pack_cols<<<h->num_sms * 4, 256, 0, h->stream>>>(stage, h->n, k, h->Arow, K);
+      RK_CUDA(cudaGetLastError());
+      if (h->NR > h->n)  // padding rows stay exactly zero (rescal.py:144 keeps zeros)
+        RK_CUDA(cudaMemsetAsync(h->Arow + (size_t)h->n * K, 0, sizeof(double) * (h->NR - h->n) * K, h->stream));
+      RK_CUDA(cudaMemcpyAsync(h->R, r.data(), r.size() * 8, cudaMemcpyHostToDevice, h->stream));
+      launch_emit(h);
+      RK_CUDA(cudaStreamSynchronize(h->stream));
+      dfree(stage);
+      return;
+    }
     // A: global (n, k) -> this rank's row / col sets, zero padded
     std::vector<double> arow((size_t)h->NR * K, 0.0), acol((size_t)h->NC * K, 0.0);
     const int64_t r0 = h->grid() ? (int64_t)h->gi * h->pc * h->piece : 0;
@@ -1692,10 +1713,6 @@ int rk_set_factors(rk_handle* h, const double* A, const double* R) {
         if (g < h->n)
           for (int c = 0; c < k; ++c) acol[(size_t)j * K + c] = A[g * k + c];
       }
-    std::vector<double> r((size_t)h->m * K * K, 0.0);
-    for (int64_t t = 0; t < h->m; ++t)
-      for (int a = 0; a < k; ++a)
-        for (int b = 0; b < k; ++b) r[((size_t)t * K + a) * K + b] = R[((size_t)t * k + a) * k + b];
     RK_CUDA(cudaMemcpyAsync(h->Arow, arow.data(), arow.size() * 8, cudaMemcpyHostToDevice, h->stream));
     if (h->grid())
       RK_CUDA(cudaMemcpyAsync(h->Acol, acol.data(), acol.size() * 8, cudaMemcpyHostToDevice, h->stream));
@@ -1725,12 +1742,17 @@ int rk_get_factors(rk_handle* h, double* A, double* R) {
         full.resize(rs * h->pr);
         RK_CUDA(cudaMemcpy(full.data(), d, full.size() * 8, cudaMemcpyDeviceToHost));
         dfree(d);
+        for (int64_t i = 0; i < h->n; ++i)
+          for (int c = 0; c < k; ++c) A[i * k + c] = full[(size_t)i * K + c];
       } else {
-        full.resize((size_t)h->NR * K);
-        RK_CUDA(cudaMemcpy(full.data(), h->Arow, full.size() * 8, cudaMemcpyDeviceToHost));
+        // unpadded on the device, one copy into the caller's (n, k) array
+        double* stage = dalloc<double>((size_t)h->n * k);
+        rk::unpack_cols<<<h->num_sms * 4, 256, 0, h->stream>>>(h->Arow, K, h->n, k, stage);
+        RK_CUDA(cudaGetLastError());
+        RK_CUDA(cudaMemcpyAsync(A, stage, sizeof(double) * h->n * k, cudaMemcpyDeviceToHost, h->stream));
+        RK_CUDA(cudaStreamSynchronize(h->stream));
+        dfree(stage);
       }
-      for (int64_t i = 0; i < h->n; ++i)
-        for (int c = 0; c < k; ++c) A[i * k + c] = full[(size_t)i * K + c];
     }
     if (R) {
       std::vector<double> r((size_t)h->m * K * K);

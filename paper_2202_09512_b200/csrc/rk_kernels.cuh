@@ -1340,6 +1340,26 @@ RK_DEV double pcg_out_double(u128 state) {
   return (double)(out >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// Factor (un)packing between the caller's compact (rows, k) fp64 layout and
+// the engine's zero-padded (rows, K) layout.
+__global__ void pack_cols(const double* __restrict__ src, int64_t rows, int k, double* __restrict__ dst, int K) {
+  const int64_t total = rows * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / K;
+    const int c = (int)(e - i * K);
+    dst[e] = c < k ? src[i * k + c] : 0.0;
+  }
+}
+
+__global__ void unpack_cols(const double* __restrict__ src, int K, int64_t rows, int k, double* __restrict__ dst) {
+  const int64_t total = rows * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k;
+    const int c = (int)(e - i * k);
+    dst[e] = src[i * K + c];
+  }
+}
+
 // ---- NNDSVD helpers (rescal.py:327-372) -----------------------------------
 // Y[i][c] = sum_t A[t][i][c] + B[t][i][c] (fp64), rows < n of per-slice
 // [ld][b] fp32 blocks: the two halves of G V = sum_t X_t (X_t^T V) + X_t^T (X_t V).
