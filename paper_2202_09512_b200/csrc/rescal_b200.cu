@@ -750,7 +750,7 @@ void launch_k2b(rk_handle* h) {
             eps_m);
       } else {
         rk::sp::sp_wfrag<<<(unsigned)h->m, 256, 0, h->stream>>>(h->ctl, h->W32, h->wfrag, (int)h->m);
-        rk::sp::sp_numer_tc<<<(unsigned)h->num_sms, 256, rk::sp::SpNumTc::smem, h->stream>>>(
+        rk::sp::sp_numer_tc<<<(unsigned)h->num_sms * 2, 256, rk::sp::SpNumTc::smem, h->stream>>>(
             h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->wfrag, h->Mm, (int)h->n,
             (int)h->m, eps_m);
         h->launches += 1;

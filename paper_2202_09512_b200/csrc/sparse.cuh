@@ -479,14 +479,14 @@ __global__ void __launch_bounds__(256) sp_wfrag(const Ctl* __restrict__ ctl, con
 struct SpNumTc {
   static constexpr int K = 16;
   static constexpr int RB = 256;  // rows per row block (8 warps x 32)
-  static constexpr int NS = 6;    // ~180 KB in flight per SM (HBM latency under load)
+  static constexpr int NS = 3;    // two CTAs per SM: ~140 KB in flight per SM
   static constexpr int PQ_BYTES = RB * K * 4;         // one of P_t / Q_t
   static constexpr int WF_BYTES = 8 * 32 * 16;        // Wf_t
   static constexpr int STAGE = 2 * PQ_BYTES + WF_BYTES;
   static constexpr size_t smem = (size_t)NS * STAGE + K * K * sizeof(double) + NS * 8 + 128;
 };
 
-__global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, double* __restrict__ A64,
+__global__ void __launch_bounds__(256, 2) sp_numer_tc(Ctl* __restrict__ ctl, double* __restrict__ A64,
                                                       float* __restrict__ A32, const float* __restrict__ P,
                                                       const float* __restrict__ Q, int ldp, int ldq,
                                                       const float4* __restrict__ Wf,
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
   if (tid == 0)
     for (int f = 0; f < C::NS - 1 && f < nstage; ++f) issue(f);
   double acc[2][2][4];
-  float c[2][2][2][4];  // [pq][mt][nt][frag]
+  float c[2][2][4];  // [mt][nt][frag]
   bool bad = false;
   for (int f = 0; f < nstage; ++f) {
     const int t = f % M;
@@ -543,18 +543,13 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
     }
     const uint8_t* st = ring + (size_t)(f % C::NS) * C::STAGE;
     const float4* wf = reinterpret_cast<const float4*>(st + 2 * C::PQ_BYTES);
-    // independent accumulators per (pq, mt, nt): 8 MMA chains per warp; the
-    // three split passes are issued pass-major so consecutive MMAs never
-    // depend on each other
     if ((t & 1) == 0) {
 #pragma unroll
-      for (int pq = 0; pq < 2; ++pq)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int x = 0; x < 4; ++x) c[pq][mt][nt][x] = 0.f;
+          for (int x = 0; x < 4; ++x) c[mt][nt][x] = 0.f;
     }
 #pragma unroll
     for (int pq = 0; pq < 2; ++pq) {
@@ -564,7 +559,6 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
       for (int s = 0; s < 2; ++s)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) bw[s][nt] = wf[(pq * 4 + s * 2 + nt) * 32 + lane];
-      uint32_t ah[2][2][4], al[2][2][4];  // [mt][s][q]
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int r = warp * 32 + mt * 16 + g;
@@ -573,29 +567,21 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const float v[4] = {s ? x0.z : x0.x, s ? x1.z : x1.x, s ? x0.w : x0.y, s ? x1.w : x1.y};
+          uint32_t ah[4], al[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // hi = truncation to tf32 (one LOP), lo exact
-            ah[mt][s][q] = __float_as_uint(v[q]) & 0xffffe000u;
-            al[mt][s][q] = __float_as_uint(v[q] - __uint_as_float(ah[mt][s][q]));
+            ah[q] = __float_as_uint(v[q]) & 0xffffe000u;
+            al[q] = __float_as_uint(v[q] - __uint_as_float(ah[q]));
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const float4 b = bw[s][nt];
+            mma_tf32(c[mt][nt], al, __float_as_uint(b.x), __float_as_uint(b.y));
+            mma_tf32(c[mt][nt], ah, __float_as_uint(b.z), __float_as_uint(b.w));
+            mma_tf32(c[mt][nt], ah, __float_as_uint(b.x), __float_as_uint(b.y));
           }
         }
       }
-#pragma unroll
-      for (int pass = 0; pass < 3; ++pass)
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              const float4 b = bw[s][nt];
-              if (pass == 0)
-                mma_tf32(c[pq][mt][nt], al[mt][s], __float_as_uint(b.x), __float_as_uint(b.y));
-              else if (pass == 1)
-                mma_tf32(c[pq][mt][nt], ah[mt][s], __float_as_uint(b.z), __float_as_uint(b.w));
-              else
-                mma_tf32(c[pq][mt][nt], ah[mt][s], __float_as_uint(b.x), __float_as_uint(b.y));
-            }
     }
     if ((t & 1) || t == M - 1) {  // fp32 over <= 2 slices (64 products), then fp64
 #pragma unroll
@@ -603,51 +589,52 @@ __global__ void __launch_bounds__(256, 1) sp_numer_tc(Ctl* __restrict__ ctl, dou
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-          for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)(c[0][mt][nt][x] + c[1][mt][nt][x]);
+          for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)c[mt][nt][x];
     }
     if (t == M - 1) {
       // A update of this row block. Lane (g, tq) holds rows r (c0, c1) and
-      // r + 8 (c2, c3) at columns 8nt + 2tq + {0, 1} of each m-tile.
-      double an[2][2][4];
+      // r + 8 (c2, c3) at columns 8nt + 2tq + {0, 1} of each m-tile. A row is
+      // read and written only by the four lanes of one quad (same warp), so a
+      // warp barrier orders each row's reads before its writes.
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = warp * 32 + mt * 16 + g + 8 * h;
-          if (r < nr) {
-            const double* Ai = A64 + (size_t)(row0 + r) * K;
-            double a[K];
-#pragma unroll
-            for (int d = 0; d < K; ++d) a[d] = Ai[d];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int col = 8 * nt + 2 * tq + e;
-                double deno = eps_m;
-#pragma unroll
-                for (int d = 0; d < K; ++d) deno = fma(a[d], Ms[d * K + col], deno);
-                const double v = Ai[col] * acc[mt][nt][2 * h + e] / deno;
-                an[mt][nt][2 * h + e] = v;
-                bad |= !isfinite(v);
-              }
+          const bool ok = r < nr;
+          double* Ai = A64 + (size_t)(row0 + (ok ? r : 0)) * K;
+          double out[2][2];
+          if (ok) {
+            double deno[2][2] = {{eps_m, eps_m}, {eps_m, eps_m}};
+#pragma unroll 4
+            for (int d = 0; d < K; ++d) {
+              const double a = Ai[d];
+              const double2 m0 = *reinterpret_cast<const double2*>(Ms + d * K + 2 * tq);
+              const double2 m1 = *reinterpret_cast<const double2*>(Ms + d * K + 8 + 2 * tq);
+              deno[0][0] = fma(a, m0.x, deno[0][0]);
+              deno[0][1] = fma(a, m0.y, deno[0][1]);
+              deno[1][0] = fma(a, m1.x, deno[1][0]);
+              deno[1][1] = fma(a, m1.y, deno[1][1]);
+            }
+            const double2 a0 = *reinterpret_cast<const double2*>(Ai + 2 * tq);
+            const double2 a1 = *reinterpret_cast<const double2*>(Ai + 8 + 2 * tq);
+            out[0][0] = a0.x * acc[mt][0][2 * h] / deno[0][0];
+            out[0][1] = a0.y * acc[mt][0][2 * h + 1] / deno[0][1];
+            out[1][0] = a1.x * acc[mt][1][2 * h] / deno[1][0];
+            out[1][1] = a1.y * acc[mt][1][2 * h + 1] / deno[1][1];
+            bad |= !(isfinite(out[0][0]) && isfinite(out[0][1]) && isfinite(out[1][0]) && isfinite(out[1][1]));
           }
-        }
-      __syncthreads();  // all rows of the block read before any write
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = warp * 32 + mt * 16 + g + 8 * h;
-          if (r < nr) {
+          __syncwarp();
+          if (ok) {
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
               const int col = 8 * nt + 2 * tq;
-              const double v0 = an[mt][nt][2 * h], v1 = an[mt][nt][2 * h + 1];
-              *reinterpret_cast<double2*>(A64 + (size_t)(row0 + r) * K + col) = make_double2(v0, v1);
-              *reinterpret_cast<float2*>(A32 + (size_t)(row0 + r) * K + col) = make_float2((float)v0, (float)v1);
+              *reinterpret_cast<double2*>(Ai + col) = make_double2(out[nt][0], out[nt][1]);
+              *reinterpret_cast<float2*>(A32 + (size_t)(row0 + r) * K + col) =
+                  make_float2((float)out[nt][0], (float)out[nt][1]);
             }
           }
+          __syncwarp();
         }
     }
     __syncthreads();  // stage f % NS is refilled next iteration
