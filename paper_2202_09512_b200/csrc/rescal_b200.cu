@@ -458,6 +458,8 @@ void alloc_factor_buffers(rk_handle* h) {
                                    (int)rk::sp::SpNumTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramCfg<16>::smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpNumCfg<16>::smem));
     } else {
@@ -633,7 +635,11 @@ void launch_k2a(rk_handle* h, int skip) {
   if (h->sparse && !h->grid()) {
     // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram)
     const int grid = h->num_sms * 2;
-    if (K == 16)
+    static const bool simt_gram = std::getenv("RK_SP_GRAM_SIMT") != nullptr;  // experiments only
+    if (K == 16 && !simt_gram)
+      rk::sp::sp_gram_tc<<<grid, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    else if (K == 16)
       rk::sp::sp_gram<16><<<grid, 256, rk::sp::SpGramCfg<16>::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
     else

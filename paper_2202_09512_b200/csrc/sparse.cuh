@@ -37,6 +37,28 @@ RK_DEV void sp_cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+RK_DEV uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+RK_DEV void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+RK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+
 // L2 cache-policy helpers (createpolicy + .L2::cache_hint): the index/value
 // streams and the output rows are touched once per pass (evict_first), the
 // gathered factor rows are re-read ~10x per pass from L2 (evict_last, and not
@@ -255,6 +277,132 @@ __global__ void __launch_bounds__(256) sp_gram(const Ctl* __restrict__ ctl, cons
   }
 }
 
+// Tensor-core form of sp_gram for K = 16: S = A^T B over a row chunk is an
+// m16n8k8 TF32 product with the rows as the K dimension (3-pass split,
+// truncation hi / exact lo as in sp_numer_tc). Index permutations make every
+// fragment an LDS.64: output row m <-> c = 2g (m = g) / 2g+1 (m = g+8), output
+// column n of n-tile nt <-> d = 2n + nt, so lane (g, tq) reads columns 2g, 2g+1
+// of rows tq and tq+4 of the 8-row k-step from both A and B; rows are padded
+// to 24 floats (conflict-free). fp32 accumulation over <= 32 rows per warp,
+// then fp64; warp partials summed in fixed order; one fp64 partial per item.
+struct SpGramTc {
+  static constexpr int K = 16, SR = 128, LD = 24, NS = 4;
+  static constexpr int ARR = SR * LD;  // floats per array per stage
+  static constexpr size_t smem = (size_t)NS * 2 * ARR * sizeof(float);  // 96 KB (>= 8 warps x 256 doubles)
+};
+
+__global__ void __launch_bounds__(256, 2) sp_gram_tc(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+                                                     const float* __restrict__ P, int n, int ldp, int M, int nchunk,
+                                                     double* __restrict__ part, int skip_if_stopped) {
+  using C = SpGramTc;
+  constexpr int K = 16;
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ __align__(16) float gts[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rows_per_chunk = (n + nchunk - 1) / nchunk;
+  const int nitems = (M + 1) * nchunk;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int slot = item / nchunk, chunk = item - slot * nchunk;
+    const float* B = slot == 0 ? A32 : P + (size_t)(slot - 1) * ldp * K;
+    const int r0 = chunk * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+    const int nst = r1 > r0 ? (r1 - r0 + C::SR - 1) / C::SR : 0;
+    auto issue = [&](int s) {
+      const int base = r0 + s * C::SR, nr = min(C::SR, r1 - base);
+      float* as = gts + (size_t)(s % C::NS) * 2 * C::ARR;
+      float* bs = as + C::ARR;
+      for (int e = tid; e < C::SR * 4; e += 256) {
+        const int r = e >> 2, c4 = e & 3;
+        if (r < nr) {
+          sp_cp16(as + r * C::LD + 4 * c4, A32 + (size_t)(base + r) * K + 4 * c4);
+          sp_cp16(bs + r * C::LD + 4 * c4, B + (size_t)(base + r) * K + 4 * c4);
+        } else {  // rows past the chunk contribute zero
+          *reinterpret_cast<float4*>(as + r * C::LD + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(bs + r * C::LD + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    };
+    __syncthreads();  // previous item's buffers (and reduction scratch) consumed
+#pragma unroll
+    for (int s = 0; s < C::NS - 1; ++s) {
+      if (s < nst) issue(s);
+      sp_cp_commit();
+    }
+    double acc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[nt][x] = 0.0;
+    float c[2][4];
+    for (int s = 0; s < nst; ++s) {
+      if (s + C::NS - 1 < nst) issue(s + C::NS - 1);
+      sp_cp_commit();
+      sp_cp_wait<C::NS - 1>();
+      __syncthreads();
+      const float* as = gts + (size_t)(s % C::NS) * 2 * C::ARR;
+      const float* bs = as + C::ARR;
+      if ((s & 1) == 0) {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) c[nt][x] = 0.f;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {  // this warp's two 8-row k-steps of the stage
+        const int rb = (warp + 8 * kk) * 8;
+        const float2 a_lo_row = *reinterpret_cast<const float2*>(as + (rb + tq) * C::LD + 2 * g);
+        const float2 a_hi_row = *reinterpret_cast<const float2*>(as + (rb + tq + 4) * C::LD + 2 * g);
+        const float2 b_lo_row = *reinterpret_cast<const float2*>(bs + (rb + tq) * C::LD + 2 * g);
+        const float2 b_hi_row = *reinterpret_cast<const float2*>(bs + (rb + tq + 4) * C::LD + 2 * g);
+        const float av[4] = {a_lo_row.x, a_lo_row.y, a_hi_row.x, a_hi_row.y};
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ah[q] = __float_as_uint(av[q]) & 0xffffe000u;
+          al[q] = __float_as_uint(av[q] - __uint_as_float(ah[q]));
+        }
+        // n-tile nt: b0 = B[row tq][2g + nt], b1 = B[row tq+4][2g + nt]
+        const float bv[2][2] = {{b_lo_row.x, b_hi_row.x}, {b_lo_row.y, b_hi_row.y}};
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const uint32_t bh0 = __float_as_uint(bv[nt][0]) & 0xffffe000u, bh1 = __float_as_uint(bv[nt][1]) & 0xffffe000u;
+          const uint32_t bl0 = __float_as_uint(bv[nt][0] - __uint_as_float(bh0));
+          const uint32_t bl1 = __float_as_uint(bv[nt][1] - __uint_as_float(bh1));
+          mma_tf32(c[nt], al, bh0, bh1);
+          mma_tf32(c[nt], ah, bl0, bl1);
+          mma_tf32(c[nt], ah, bh0, bh1);
+        }
+      }
+      if ((s & 1) || s == nst - 1) {  // fp32 over <= 32 rows per lane product, then fp64
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) acc[nt][x] += (double)c[nt][x];
+      }
+      __syncthreads();  // buffer s % NS is refilled by the next iteration
+    }
+    // warp partials -> fixed-order sum; lane (g, tq) holds
+    // c_nt[0] = S[2g][4tq+nt], c_nt[1] = S[2g][4tq+2+nt], c_nt[2] = S[2g+1][4tq+nt], c_nt[3] = S[2g+1][4tq+2+nt]
+    sp_cp_wait<0>();
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(gts);  // [8 warps][256]
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      red[warp * 256 + (2 * g) * 16 + 4 * tq + nt] = acc[nt][0];
+      red[warp * 256 + (2 * g) * 16 + 4 * tq + 2 + nt] = acc[nt][1];
+      red[warp * 256 + (2 * g + 1) * 16 + 4 * tq + nt] = acc[nt][2];
+      red[warp * 256 + (2 * g + 1) * 16 + 4 * tq + 2 + nt] = acc[nt][3];
+    }
+    __syncthreads();
+    {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[w * 256 + tid];
+      part[((size_t)slot * nchunk + chunk) * K * K + tid] = v;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) sp_gram_reduce(const Ctl* __restrict__ ctl,
                                                       const double* __restrict__ part, int nchunk,
                                                       int KK, double* __restrict__ gs,
@@ -437,27 +585,6 @@ __global__ void __launch_bounds__(256, 2) sp_numer_apply(Ctl* __restrict__ ctl, 
 // (g, tq) holds d = 4tq..4tq+3 of rows g and g+8: k-step s uses d = 4tq+2s and
 // 4tq+2s+1), which is conflict-free on unpadded 64-byte rows. The matching B
 // fragments (hi/lo, per slice) are laid out per lane by sp_wfrag.
-RK_DEV uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-RK_DEV void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-RK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
 // Wf[t][pq][s][nt][lane] = {b0_hi, b1_hi, b0_lo, b1_lo} with lane = 4g + tq,
 // b0 = W[4tq+2s][8nt+g], b1 = W[4tq+2s+1][8nt+g], W = R_t^T (pq 0) | R_t (pq 1)
 // taken from W32 = [R_t^T ; R_t] (K = 16).
