@@ -49,6 +49,19 @@ METRIC = "MU iters/sec + effective TFLOP/s (dense) / HBM GB/s (sparse) at 1/2/4/
 SEED = 20220218
 
 
+def ncu_traffic(config, world):
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/ncu_traffic.json; single-GPU captures)."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f).get(config)
+        return None if e is None else float(e["dram_read_bytes"] + e["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -392,7 +405,7 @@ def run_ours(args, dist, rank, world, local_rank):
         },
         "tflops_effective": tflops,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(args.config, world),
                      "kernel": ("sp_csr_pass (P = X A, CSR, A rows gathered from L2)" if sparse else
                                 "k1_tc_kernel (P=X A, Q=X^T A, 3xBF16)"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_k1, "k1_ms": k1_ms,
