@@ -14,6 +14,10 @@ import paper_2202_09512_b200 as rk
 
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
+# GRID_SHAPE=PRxPC forces a grid (e.g. 1x4 on 4 GPUs exercises 4-rank row
+# communicators, the row-side shape of the 2x4 grid of an 8-GPU box)
+_gs = os.environ.get("GRID_SHAPE")
+GRID = tuple(int(v) for v in _gs.lower().split("x")) if _gs else None
 results = []
 ok = True
 for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "auto"), (700, 2, 32, 12, "auto"),
@@ -21,7 +25,7 @@ for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "aut
     x = np.random.default_rng(n).random((m, n, n), dtype=np.float32).astype(np.float64)
     f0 = rk.random_init(n, k, m, 1)
     f, tr, info = rk.solve_on_grid(rk.RelTensor(x), k, rk.SolverConfig(max_iters=iters, engine=engine),
-                                   initial=f0)
+                                   initial=f0, grid=GRID)
     rb = [None] * world
     dist.all_gather_object(rb, f.R.tobytes())
     if rank == 0:
@@ -46,7 +50,7 @@ for (n, m, k, dens, iters) in [(600, 2, 8, 0.02, 20), (1000, 3, 16, 0.01, 15), (
                                     shape=(n, n)))
     xs = rk.SparseRelTensor(slices)
     f0 = rk.random_init(n, k, m, 2)
-    f, tr, info = rk.solve_on_grid(xs, k, rk.SolverConfig(max_iters=iters), initial=f0)
+    f, tr, info = rk.solve_on_grid(xs, k, rk.SolverConfig(max_iters=iters), initial=f0, grid=GRID)
     rb = [None] * world
     dist.all_gather_object(rb, f.R.tobytes())
     if rank == 0:
