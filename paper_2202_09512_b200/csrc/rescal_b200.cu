@@ -632,13 +632,17 @@ void launch_k5(rk_handle* h, int gate) {
 
 void launch_k2a(rk_handle* h, int skip) {
   const int K = h->K;
-  if (h->sparse && !h->grid()) {
-    // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram)
+  if (h->sparse && (!h->grid() || K == 16)) {
+    // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram);
+    // on a grid G runs over the rank's own piece of A, S_t over its row set
     const int grid = h->num_sms * 2;
     static const bool simt_gram = std::getenv("RK_SP_GRAM_SIMT") != nullptr;  // experiments only
-    if (K == 16 && !simt_gram)
+    const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
+    const int nown = h->grid() ? (int)h->piece : 0;
+    if (K == 16 && (!simt_gram || h->grid()))
       rk::sp::sp_gram_tc<<<grid, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
+          nown);
     else if (K == 16)
       rk::sp::sp_gram<16><<<grid, 256, rk::sp::SpGramCfg<16>::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
@@ -810,7 +814,22 @@ void launch_k2b(rk_handle* h) {
     return;
   }
   const int rpb = 256 / K;
-  if (h->sparse) {
+  if (h->sparse && K == 16) {
+    // Q_t = X_t^T A[I] from the block's CSC (gather kernel), then the row and
+    // column numerator partials U_I = sum_t P_t R_t^T, U_J = sum_t Q_t R_t on
+    // tensor cores (sp_numer_tc single-operand mode)
+    rk::sp::sp_wfrag<<<(unsigned)h->m, 256, 0, h->stream>>>(h->ctl, h->W32, h->wfrag, (int)h->m);
+    rk::sp::sp_csr_pass<16><<<h->num_sms * 16, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val,
+                                                                    h->A32row, h->Q, (int)h->cols_valid,
+                                                                    (int)h->NC, (int)h->m, 1);
+    rk::sp::sp_numer_tc<<<(unsigned)h->num_sms * 2, 256, rk::sp::SpNumTc::smem, h->stream>>>(
+        h->ctl, h->Arow, h->A32row, h->P, nullptr, (int)h->NR, 0, h->wfrag, h->Mm, (int)h->rows_valid,
+        (int)h->m, eps_m, 0, h->UI);
+    rk::sp::sp_numer_tc<<<(unsigned)h->num_sms * 2, 256, rk::sp::SpNumTc::smem, h->stream>>>(
+        h->ctl, h->Arow, h->A32row, h->Q, nullptr, (int)h->NC, 0, h->wfrag, h->Mm, (int)h->cols_valid,
+        (int)h->m, eps_m, 1, h->UJ);
+    h->launches += 3;
+  } else if (h->sparse) {
     // U_I = sum_t P_t R_t^T over the row set (dense P); U_J = sum_t z_t R_t with
     // z_t = X_t^T A_row streamed from the block's CSC (no P part: P_t lives on
     // the row set)

@@ -293,7 +293,10 @@ struct SpGramTc {
 
 __global__ void __launch_bounds__(256, 2) sp_gram_tc(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
                                                      const float* __restrict__ P, int n, int ldp, int M, int nchunk,
-                                                     double* __restrict__ part, int skip_if_stopped) {
+                                                     double* __restrict__ part, int skip_if_stopped,
+                                                     const float* __restrict__ Aown = nullptr, int nown = 0) {
+  // slot 0 (G) runs over Aown's nown rows when given (a grid rank's own piece
+  // of A, rescal.py:124 with the grid's rank-ascending sum, dist_rescal.py:74-92)
   using C = SpGramTc;
   constexpr int K = 16;
   if (skip_if_stopped && ctl->stop) return;
@@ -304,8 +307,12 @@ __global__ void __launch_bounds__(256, 2) sp_gram_tc(const Ctl* __restrict__ ctl
   const int nitems = (M + 1) * nchunk;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int slot = item / nchunk, chunk = item - slot * nchunk;
-    const float* B = slot == 0 ? A32 : P + (size_t)(slot - 1) * ldp * K;
-    const int r0 = chunk * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+    const bool own = slot == 0 && Aown != nullptr;
+    const float* Ai = own ? Aown : A32;
+    const float* B = slot == 0 ? Ai : P + (size_t)(slot - 1) * ldp * K;
+    const int nn = own ? nown : n;
+    const int rpc = own ? (nown + nchunk - 1) / nchunk : rows_per_chunk;
+    const int r0 = chunk * rpc, r1 = min(nn, r0 + rpc);
     const int nst = r1 > r0 ? (r1 - r0 + C::SR - 1) / C::SR : 0;
     auto issue = [&](int s) {
       const int base = r0 + s * C::SR, nr = min(C::SR, r1 - base);
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(256, 2) sp_gram_tc(const Ctl* __restrict__ ctl
       for (int e = tid; e < C::SR * 4; e += 256) {
         const int r = e >> 2, c4 = e & 3;
         if (r < nr) {
-          sp_cp16(as + r * C::LD + 4 * c4, A32 + (size_t)(base + r) * K + 4 * c4);
+          sp_cp16(as + r * C::LD + 4 * c4, Ai + (size_t)(base + r) * K + 4 * c4);
           sp_cp16(bs + r * C::LD + 4 * c4, B + (size_t)(base + r) * K + 4 * c4);
         } else {  // rows past the chunk contribute zero
           *reinterpret_cast<float4*>(as + r * C::LD + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -618,7 +625,12 @@ __global__ void __launch_bounds__(256, 2) sp_numer_tc(Ctl* __restrict__ ctl, dou
                                                       const float* __restrict__ Q, int ldp, int ldq,
                                                       const float4* __restrict__ Wf,
                                                       const double* __restrict__ Mm, int n, int M,
-                                                      double eps_m) {
+                                                      double eps_m, int only = -1,
+                                                      double* __restrict__ U = nullptr) {
+  // only < 0: num from P and Q, then the A update (single GPU).
+  // only = 0 | 1: U = sum_t Y_t R_t^T (0, Y = P) or sum_t Y_t R_t (1, Y passed
+  // as P) written as fp64 rows — the grid's row / column numerator partials
+  // before their reduce-scatter.
   using C = SpNumTc;
   constexpr int K = 16;
   if (ctl->stop) return;
@@ -644,9 +656,9 @@ __global__ void __launch_bounds__(256, 2) sp_numer_tc(Ctl* __restrict__ ctl, dou
     uint8_t* st = ring + (size_t)(f % C::NS) * C::STAGE;
     const uint32_t bar = tc::smem_u32(&full[f % C::NS]);
     const uint32_t bytes = (uint32_t)nr * K * 4;
-    tc::mbar_expect_tx(bar, 2 * bytes + C::WF_BYTES);
-    bulk_g2s(tc::smem_u32(st), P + ((size_t)t * ldp + row0) * K, bytes, bar);
-    bulk_g2s(tc::smem_u32(st + C::PQ_BYTES), Q + ((size_t)t * ldq + row0) * K, bytes, bar);
+    tc::mbar_expect_tx(bar, (only < 0 ? 2 : 1) * bytes + C::WF_BYTES);
+    bulk_g2s(tc::smem_u32(st + (only > 0 ? C::PQ_BYTES : 0)), P + ((size_t)t * ldp + row0) * K, bytes, bar);
+    if (only < 0) bulk_g2s(tc::smem_u32(st + C::PQ_BYTES), Q + ((size_t)t * ldq + row0) * K, bytes, bar);
     bulk_g2s(tc::smem_u32(st + 2 * C::PQ_BYTES), Wf + (size_t)t * 256, C::WF_BYTES, bar);
   };
   if (tid == 0)
@@ -680,6 +692,7 @@ __global__ void __launch_bounds__(256, 2) sp_numer_tc(Ctl* __restrict__ ctl, dou
     }
 #pragma unroll
     for (int pq = 0; pq < 2; ++pq) {
+      if (only >= 0 && pq != only) continue;
       const float* S = reinterpret_cast<const float*>(st + pq * C::PQ_BYTES);
       float4 bw[2][2];
 #pragma unroll
@@ -718,7 +731,22 @@ __global__ void __launch_bounds__(256, 2) sp_numer_tc(Ctl* __restrict__ ctl, dou
 #pragma unroll
           for (int x = 0; x < 4; ++x) acc[mt][nt][x] += (double)c[mt][nt][x];
     }
-    if (t == M - 1) {
+    if (t == M - 1 && only >= 0) {
+      // numerator partial rows (fp64): lane (g, tq) holds rows r / r + 8 at
+      // columns 8nt + 2tq + {0, 1} of each m-tile
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = warp * 32 + mt * 16 + g + 8 * h;
+          if (r < nr) {
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+              *reinterpret_cast<double2*>(U + (size_t)(row0 + r) * K + 8 * nt + 2 * tq) =
+                  make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
+          }
+        }
+    } else if (t == M - 1) {
       // A update of this row block. Lane (g, tq) holds rows r (c0, c1) and
       // r + 8 (c2, c3) at columns 8nt + 2tq + {0, 1} of each m-tile. A row is
       // read and written only by the four lanes of one quad (same warp), so a
