@@ -49,6 +49,11 @@ METRIC = "MU iters/sec + effective TFLOP/s (dense) / HBM GB/s (sparse) at 1/2/4/
 SEED = 20220218
 
 
+# measured random 64-B-row gather ceiling of one B200 (LDG.128, 4 lanes/row, 2^27 rows
+# from a 67 MB table; profiles/r01s3_gather_ceiling.log)
+GATHER_CEILING_GROWS = 145.2
+
+
 def ncu_traffic(config, world):
     """dram read+write bytes per launch of the dominant kernel from the committed
     ncu --set full capture (profiles/ncu_traffic.json; single-GPU captures)."""
@@ -411,6 +416,14 @@ def run_ours(args, dist, rank, world, local_rank):
                      "bytes_per_launch": bytes_k1, "k1_ms": k1_ms,
                      "k1_share_of_step": (k1_ms / (dev_ms / args.steps)) if dev_ms else None},
         "gpu_launches": int(launches),
+        "gather_ceiling": ({
+            "note": "the sparse pass gathers one A row (64 B, its own 128 B line) per stored entry; the "
+                    "LSU/L1TEX path retires ~2.0 cycles per random line per SM whatever the load width "
+                    "or the table size (8-67 MB); TMA gather4 / cp.async.bulk are ~10x slower "
+                    "(tools/tma_gather_bench.cu, profiles/r01s3_gather_ceiling.log)",
+            "rows_per_launch": float(nnz), "achieved_grows_s": nnz / (k1_ms / 1e3) / 1e9,
+            "ceiling_grows_s": GATHER_CEILING_GROWS, "frac": nnz / (k1_ms / 1e3) / 1e9 / GATHER_CEILING_GROWS}
+            if sparse else None),
         "tracked": tracked,
         "clocks": clocks.summary(),
         "device_ms": {"profiled_run": dev_ms, "graph_run": dev_ms2, "wall_s": t_wall},

@@ -55,6 +55,108 @@ __global__ void __launch_bounds__(256, 8) k_ldg(const int* __restrict__ idx, int
   atomicAdd(out, y.x + y.y + y.z + y.w);
 }
 
+
+// LPR lanes per row, VEC floats per lane load (16 = LPR*VEC); ALLOC: 0 no_allocate, 1 L1 allocate
+template <int LPR, int ALLOC>
+__global__ void __launch_bounds__(256, 8) k_ldgv(const int* __restrict__ idx, int64_t E, const float* __restrict__ tab, float* out) {
+  constexpr int VEC = 16 / LPR;
+  const uint64_t pl = pol_last(), pf = pol_first();
+  const int q = threadIdx.x % LPR;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPR;
+  float acc = 0.f;
+  for (int64_t e = g0 * 4; e < E; e += ng * 4) {
+    int j[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(j[u]) : "l"(idx + e + u), "l"(pf));
+    float a[4][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float* src = tab + (size_t)j[u] * 16 + VEC * q;
+      if constexpr (VEC == 16) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                       : "=f"(a[u][8*h+0]), "=f"(a[u][8*h+1]), "=f"(a[u][8*h+2]), "=f"(a[u][8*h+3]), "=f"(a[u][8*h+4]), "=f"(a[u][8*h+5]), "=f"(a[u][8*h+6]), "=f"(a[u][8*h+7])
+                       : "l"(src + 8 * h), "l"(pl));
+      } else if constexpr (VEC == 8) {
+        if (ALLOC)
+          asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                       : "=f"(a[u][0]), "=f"(a[u][1]), "=f"(a[u][2]), "=f"(a[u][3]), "=f"(a[u][4]), "=f"(a[u][5]), "=f"(a[u][6]), "=f"(a[u][7])
+                       : "l"(src), "l"(pl));
+        else
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                       : "=f"(a[u][0]), "=f"(a[u][1]), "=f"(a[u][2]), "=f"(a[u][3]), "=f"(a[u][4]), "=f"(a[u][5]), "=f"(a[u][6]), "=f"(a[u][7])
+                       : "l"(src), "l"(pl));
+      } else if constexpr (VEC == 4) {
+        if (ALLOC)
+          asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=f"(a[u][0]), "=f"(a[u][1]), "=f"(a[u][2]), "=f"(a[u][3]) : "l"(src), "l"(pl));
+        else
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=f"(a[u][0]), "=f"(a[u][1]), "=f"(a[u][2]), "=f"(a[u][3]) : "l"(src), "l"(pl));
+      } else if constexpr (VEC == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(a[u][0]), "=f"(a[u][1]) : "l"(src), "l"(pl));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < VEC; ++h) acc += a[u][h];
+  }
+  atomicAdd(out, acc);
+}
+// one row per LDG: only lanes 0..3 of each warp active (rows per warp-instruction = 1)
+__global__ void __launch_bounds__(256, 8) k_ldg1(const int* __restrict__ idx, int64_t E, const float* __restrict__ tab, float* out) {
+  const uint64_t pl = pol_last();
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float acc = 0.f;
+  for (int64_t e = w0 * 8; e < E; e += nw * 8) {
+    const int jl = idx[e + (lane & 7)];
+    float4 a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = __shfl_sync(0xffffffffu, jl, u);
+      if (lane < 4)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(a[u].x), "=f"(a[u].y), "=f"(a[u].z), "=f"(a[u].w) : "l"(tab + (size_t)j * 16 + 4 * lane), "l"(pl));
+      else a[u] = make_float4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += a[u].x + a[u].y + a[u].z + a[u].w;
+  }
+  atomicAdd(out, acc);
+}
+
+
+// RPL distinct rows per warp-LDG.128 (lane groups of 4 lanes; groups beyond RPL
+// duplicate the addresses of group (g % RPL)); 16 rows per warp iteration.
+template <int RPL>
+__global__ void __launch_bounds__(256, 4) k_rpl(const int* __restrict__ idx, int64_t E, const float* __restrict__ tab, float* out) {
+  const uint64_t pl = pol_last();
+  const int lane = threadIdx.x & 31, q = lane & 3, g = (lane >> 2) % RPL;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float4 acc = make_float4(0, 0, 0, 0);
+  constexpr int NL = 16 / RPL;  // loads per lane per iteration
+  for (int64_t e = w0 * 16; e < E; e += nw * 16) {
+    const int jl = idx[e + (lane & 15)];
+    float4 a[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int j = __shfl_sync(0xffffffffu, jl, u * RPL + g);
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(a[u].x), "=f"(a[u].y), "=f"(a[u].z), "=f"(a[u].w) : "l"(tab + (size_t)j * 16 + 4 * q), "l"(pl));
+    }
+#pragma unroll
+    for (int u = 0; u < NL; ++u) { acc.x += a[u].x; acc.y += a[u].y; acc.z += a[u].z; acc.w += a[u].w; }
+  }
+  if ((lane >> 2) < RPL) atomicAdd(out, acc.x + acc.y + acc.z + acc.w);
+}
+
 // ---------------------------------------------------------------- mbarrier helpers
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* b, int c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(c)); }
@@ -149,7 +251,7 @@ int main(int argc, char** argv) {
   CK(cudaFuncSetAttribute(k_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(k_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int lg = 17; lg <= 20; ++lg) {
+  for (int lg = 19; lg <= 20; ++lg) {
     const int rows = 1 << lg;
     gen_idx<<<4096, 256>>>(idx, E, rows);
     CUtensorMap tm;
@@ -160,14 +262,28 @@ int main(int argc, char** argv) {
     CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tab, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
-    for (int mode = 0; mode < 3; ++mode) {
+    const char* nm[] = {"ldg4x128", "ldg8x64", "ldg2x256", "ldg1x2x256", "ldg4x128_l1", "ldg2x256_l1", "ldg1row", "gather4", "rpl8", "rpl4", "rpl2", "rpl1"};
+    for (int mode = 0; mode < 12; ++mode) {
+      if (mode >= 1 && mode <= 7 && mode != 2) continue;
+      if (mode == 7 && lg != 20) continue;
       float best = 1e30f, chk = 0.f;
       for (int rep = 0; rep < 4; ++rep) {
         CK(cudaMemset(out, 0, 4));
         cudaEventRecord(a);
-        if (mode == 0) k_ldg<<<nsm * 8, 256>>>(idx, E, tab, out);
-        else if (mode == 1) k_tma<0><<<nsm, 32 * (NCW + 1), smem>>>(tm, idx, E, tab, out);
-        else k_tma<1><<<nsm, 32 * (NCW + 1), smem>>>(tm, idx, E, tab, out);
+        switch (mode) {
+          case 0: k_ldgv<4, 0><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 1: k_ldgv<8, 0><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 2: k_ldgv<2, 0><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 3: k_ldgv<1, 0><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 4: k_ldgv<4, 1><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 5: k_ldgv<2, 1><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 6: k_ldg1<<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 8: k_rpl<8><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 9: k_rpl<4><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 10: k_rpl<2><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 11: k_rpl<1><<<nsm * 8, 256>>>(idx, E, tab, out); break;
+          case 7: k_tma<0><<<nsm, 32 * (NCW + 1), smem>>>(tm, idx, E, tab, out); break;
+        }
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         CK(cudaGetLastError());
@@ -175,9 +291,8 @@ int main(int argc, char** argv) {
         if (rep > 0 && ms < best) best = ms;
         CK(cudaMemcpy(&chk, out, 4, cudaMemcpyDeviceToHost));
       }
-      const char* nm[3] = {"ldg", "gather4", "bulk64"};
-      printf("table %5.1f MB %-8s %7.3f ms  %6.1f Grows/s  (%.1f GB/s of rows)  chk %.6e\n", rows * 64.0 / 1e6, nm[mode], best,
-             E / best / 1e6, E * 64.0 / best / 1e6, chk);
+      printf("table %5.1f MB %-12s %7.3f ms  %6.1f Grows/s  %.2f cyc/row/SM  chk %.6e\n", rows * 64.0 / 1e6, nm[mode], best,
+             E / best / 1e6, nsm * 1.965e9 / (E / best * 1e3), chk);
     }
   }
   return 0;
