@@ -407,6 +407,8 @@ def run_ours(args, dist, rank, world, local_rank):
                    f"inputs larger than L2 ({4.0 * elems / 1e9:.1f} GB/GPU vs 0.126 GB)"),
             "engine": {1: "tcgen05", 2: "simt"}.get(einfo["engine"], "?"),
             "grid": f"{grid[0]}x{grid[1]}", "parallelism": f"pxq={grid[0]}x{grid[1]}",
+            **({"exchange": "peer-memory (NVLink IPC, fused into the numerator / A-update kernels)"
+                if einfo.get("peer_exchange") else "nccl"} if world > 1 else {}),
         },
         "tflops_effective": tflops,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",

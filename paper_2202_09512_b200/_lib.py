@@ -365,9 +365,10 @@ class Engine:
         return ms.value
 
     def info(self):
-        out = np.zeros(10, dtype=np.int64)
-        check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 10))
-        keys = ["engine", "n_pad", "k_pad", "strip_tiles", "ctas", "smem", "strips", "slots", "k2a_blocks", "nc_pad"]
+        out = np.zeros(11, dtype=np.int64)
+        check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 11))
+        keys = ["engine", "n_pad", "k_pad", "strip_tiles", "ctas", "smem", "strips", "slots", "k2a_blocks", "nc_pad",
+                "peer_exchange"]
         return dict(zip(keys, (int(v) for v in out)))
 
     @property

@@ -32,6 +32,7 @@
 
 #include "../../include/rescal_b200.h"
 #include "k1_tc.cuh"
+#include "peer.cuh"
 #include "rk_kernels.cuh"
 #include "sparse.cuh"
 
@@ -291,6 +292,15 @@ struct rk_handle {
   float4* wfrag = nullptr;  // per-lane TF32 hi/lo B fragments of [R_t^T ; R_t] (sparse, K = 16)
   int gchunks = 0;
 
+  // peer-memory grid exchange (peer.cuh): IPC arena of every rank, epochs
+  bool peer = false;
+  bool peer_tried = false;
+  char* arena = nullptr;
+  std::vector<void*> peer_open;  // mapped peer arenas (closed on teardown)
+  unsigned* pep = nullptr;       // epochs + tickets [8]
+  rk::peer::Args pargs{};
+  int64_t peer_key[4] = {0, 0, 0, 0};
+
   bool grid() const { return pr * pc > 1; }
 };
 
@@ -547,6 +557,115 @@ void alloc_factor_buffers(rk_handle* h) {
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2ps));
 }
 
+// ------------------------------- peer-memory grid exchange ------------------
+
+void peer_teardown(rk_handle* h) {
+  for (void* p : h->peer_open)
+    if (p) cudaIpcCloseMemHandle(p);
+  h->peer_open.clear();
+  if (h->arena) cudaFree(h->arena);
+  h->arena = nullptr;
+  dfree(h->pep);
+  h->pep = nullptr;
+  h->peer = false;
+}
+
+// Collective over the world communicator (every rank calls it at the same
+// point: the first rk_run after grid init / a rank change). Maps every rank's
+// arena through CUDA IPC; any rank failing (no P2P path, RK_PEER=0) makes all
+// ranks keep the NCCL schedule.
+void ensure_peer(rk_handle* h) {
+  if (!h->grid() || h->sparse || !(h->K == 16 || h->K == 32) || !h->W32) return;
+  const int p = h->pr * h->pc;
+  const int64_t key[4] = {h->K, h->m, h->piece, p};
+  if (h->peer_tried && std::equal(key, key + 4, h->peer_key)) return;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  peer_teardown(h);
+  h->peer_tried = true;
+  std::copy(key, key + 4, h->peer_key);
+  static const bool disabled = [] {
+    const char* e = std::getenv("RK_PEER");
+    return e && std::atoi(e) == 0;
+  }();
+  const int K = h->K;
+  const int64_t b = h->piece;
+  const int L = (int)((h->m + 1) * K * K + 1);
+  auto al = [](int64_t v) { return round_up(v, 256); };
+  rk::peer::Args& a = h->pargs;
+  a = rk::peer::Args{};
+  a.p = p;
+  a.pr = h->pr;
+  a.pc = h->pc;
+  a.rank = h->rank;
+  a.gi = h->gi;
+  a.gj = h->gj;
+  a.K = K;
+  a.L = L;
+  a.b = b;
+  a.off_red = (long long)rk::peer::kFlagBytes;
+  a.off_rxI = a.off_red + al((int64_t)2 * p * L * 8);
+  a.off_rxJ = a.off_rxI + al((int64_t)2 * h->pc * b * K * 8);
+  a.off_rxAr = a.off_rxJ + al((int64_t)2 * h->pr * b * K * 8);
+  a.off_rxAc = a.off_rxAr + al((int64_t)2 * h->pc * b * K * 8);
+  const size_t bytes = (size_t)(a.off_rxAc + al((int64_t)2 * h->pr * b * K * 8));
+  int fail = (disabled || p > rk::peer::kMaxP) ? 1 : 0;
+  cudaIpcMemHandle_t mine{};
+  if (!fail && cudaMalloc(&h->arena, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    h->arena = nullptr;
+    fail = 1;
+  }
+  if (!fail && (cudaMemset(h->arena, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+                cudaIpcGetMemHandle(&mine, h->arena) != cudaSuccess)) {
+    cudaGetLastError();
+    fail = 1;
+  }
+  // exchange the 64-byte handles over NCCL (stream-ordered, then read back)
+  char* dh = dalloc<char>((size_t)p * sizeof(mine));
+  int* dfail = dalloc<int>(1);
+  std::vector<cudaIpcMemHandle_t> all(p);
+  RK_CUDA(cudaMemcpy(dh + (size_t)h->rank * sizeof(mine), &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  RK_NCCL(ncclAllGather(dh + (size_t)h->rank * sizeof(mine), dh, sizeof(mine), ncclChar, h->world, h->stream));
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  RK_CUDA(cudaMemcpy(all.data(), dh, (size_t)p * sizeof(mine), cudaMemcpyDeviceToHost));
+  h->peer_open.assign(p, nullptr);
+  for (int r = 0; r < p && !fail; ++r) {
+    if (r == h->rank) {
+      a.base[r] = h->arena;
+      continue;
+    }
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      fail = 1;
+      break;
+    }
+    h->peer_open[r] = ptr;
+    a.base[r] = static_cast<char*>(ptr);
+  }
+  RK_CUDA(cudaMemcpy(dfail, &fail, sizeof(int), cudaMemcpyHostToDevice));
+  RK_NCCL(ncclAllReduce(dfail, dfail, 1, ncclInt, ncclSum, h->world, h->stream));
+  RK_CUDA(cudaStreamSynchronize(h->stream));
+  int total = 0;
+  RK_CUDA(cudaMemcpy(&total, dfail, sizeof(int), cudaMemcpyDeviceToHost));
+  dfree(dh);
+  dfree(dfail);
+  if (total) {
+    peer_teardown(h);
+    return;
+  }
+  // k2b_u4's 48 KB staging + the ticket word exceed the default dynamic limit
+  RK_CUDA(cudaFuncSetAttribute(rk::peer::k2b_u4_peer<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  RK_CUDA(cudaFuncSetAttribute(rk::peer::k2b_u4_peer<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  h->pep = dalloc<unsigned>(8);
+  a.ep = h->pep;
+  a.ctl = h->ctl;
+  h->peer = true;
+}
+
 // ------------------------------- launches ----------------------------------
 
 void launch_k1(rk_handle* h, bool timed) {
@@ -700,6 +819,13 @@ void launch_k2a(rk_handle* h, int skip) {
 void grid_allreduce_parts(rk_handle* h, bool with_resid) {
   const int K = h->K;
   const int len = (int)((h->m + 1) * K * K);
+  if (h->peer) {
+    rk::peer::peer_allreduce<<<h->pr * h->pc, 512, 0, h->stream>>>(h->pargs, h->red, len, h->rpart,
+                                                                     with_resid ? h->nr : 0);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 1;
+    return;
+  }
   rk::sum_scalars<<<1, 256, 0, h->stream>>>(h->rpart, with_resid ? h->nr : 0, h->red + len);
   if (!h->skip_comm)
     RK_NCCL(ncclAllReduce(h->red, h->red, (size_t)len + 1, ncclDouble, ncclSum, h->world, h->stream));
@@ -847,6 +973,29 @@ void launch_k2b(rk_handle* h) {
       rk::sp::sp_csc_numer<32><<<grid, 512, wsm, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
                                                               nullptr, h->W32, h->UJ, (int)h->cols_valid, (int)h->NC, (int)h->m);
     }
+  } else if (h->W32 && h->peer) {
+    // numerator rows straight into the owners' slots, owner update, pieces
+    // straight into the peers' operand sets (peer.cuh): no NCCL calls
+    const int rb = 2 * (256 / K);
+    const int tg = rk::k2b_u4_tg(K, (int)h->m);
+    const size_t smem = (size_t)tg * (K * K + rb * K) * sizeof(float);
+    const dim3 gu((unsigned)((std::max(h->NR, h->NC) + rb - 1) / rb), 2);
+    if (K == 16)
+      rk::peer::k2b_u4_peer<16><<<gu, 256, smem, h->stream>>>(h->ctl, h->P, h->Q, h->W32, (int)h->NR,
+                                                                (int)h->NC, (int)h->m, tg, h->pargs);
+    else
+      rk::peer::k2b_u4_peer<32><<<gu, 256, smem, h->stream>>>(h->ctl, h->P, h->Q, h->W32, (int)h->NR,
+                                                                (int)h->NC, (int)h->m, tg, h->pargs);
+    RK_CUDA(cudaGetLastError());
+    phase_mark(h, h->profile, 5);
+    rk::peer::apply_peer<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
+        h->ctl, h->Arow + (size_t)h->gj * h->piece * K, h->Mm, K, eps_m, h->pargs);
+    rk::peer::emit_peer<<<h->num_sms * 2, rk::kThreads, 0, h->stream>>>(
+        h->pargs, h->Arow, (int)h->NR, h->A32row, h->ATh_row, h->ATl_row, h->Acol, (int)h->NC, h->A32col,
+        h->ATh_col, h->ATl_col);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 3;
+    return;
   } else if (h->W32) {
     const int rb = 2 * (256 / K);
     const int tg = rk::k2b_u4_tg(K, (int)h->m);
@@ -1397,6 +1546,7 @@ void rk_destroy(rk_handle* h) {
   for (auto e : h->ev_ph) cudaEventDestroy(e);
   if (h->ev_run0) cudaEventDestroy(h->ev_run0);
   if (h->ev_run1) cudaEventDestroy(h->ev_run1);
+  peer_teardown(h);
   if (h->rowc) ncclCommDestroy(h->rowc);
   if (h->colc) ncclCommDestroy(h->colc);
   if (h->world) ncclCommDestroy(h->world);
@@ -1800,6 +1950,7 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
       h->graph = nullptr;
     }
     h->eps = eps;
+    ensure_peer(h);
     ensure_trace(h, iters + 1);
     reset_ctl(h, track_error ? 1 : 0, tol, iters);
     h->k1_count = 0;
@@ -1874,6 +2025,7 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     if (iters_done) *iters_done = c.iter;
     if (track_error && trace_out && c.trace_len > 0)
       RK_CUDA(cudaMemcpy(trace_out, h->trace_dev, sizeof(double) * c.trace_len, cudaMemcpyDeviceToHost));
+    if (c.peer_err) throw RkError{RK_ERR_GRID, "peer-memory exchange timed out (a grid rank stopped early)"};
     if (c.nonfinite == 2) throw RkError{RK_ERR_NUMERICAL, "non-finite reconstruction error"};
     if (c.nonfinite) throw RkError{RK_ERR_NUMERICAL, "non-finite value in factors; aborting"};
   });
@@ -2352,9 +2504,9 @@ void* rk_stream(rk_handle* h) { return h ? (void*)h->stream : nullptr; }
 int rk_info(rk_handle* h, int64_t* out, int32_t n_out) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
-    int64_t v[10] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
-                     h->nstrips, h->nslots, h->nb, h->NC};
-    for (int i = 0; i < n_out && i < 10; ++i) out[i] = v[i];
+    int64_t v[11] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
+                     h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0};
+    for (int i = 0; i < n_out && i < 11; ++i) out[i] = v[i];
   });
 }
 

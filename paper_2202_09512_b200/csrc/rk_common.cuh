@@ -28,7 +28,9 @@ struct Ctl {
   double norm2_dev;  // sum (hi+lo)^2 of the device tensor — identity residual
   double direct_thresh;  // switch to the direct residual below this error
   double last_err;
-  double pad[6];
+  int peer_err;      // 1: a peer-memory exchange timed out (grid; see peer.cuh)
+  int pad_i;
+  double pad[5];
 };
 
 RK_DEV float warp_sum(float v) {

@@ -673,13 +673,11 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
 
 // Grid numerator (K in {16, 32}): U[row] = sum_t PQ_t[row] W_t with W_t =
 // R_t^T (which = 0, P side) or R_t (which = 1, Q side), staged like k2b_v4.
+// Block body shared with the peer-memory variant (peer.cuh k2b_u4_peer): the
+// two rows (rbase + rl, rbase + rl + TR) and column c of this thread.
 template <int K>
-__global__ void __launch_bounds__(256) k2b_u4(const Ctl* __restrict__ ctl,
-                                              const float* __restrict__ PQ,
-                                              const float* __restrict__ W32, int which, int N,
-                                              int M, int tg, double* __restrict__ U) {
-  static_assert(K == 16 || K == 32, "k2b_u4: K in {16, 32}");
-  if (ctl->stop) return;
+RK_DEV void k2b_u4_rows(const float* __restrict__ PQ, const float* __restrict__ W32, int which, int N,
+                        int M, int tg, int rbase, double& n0, double& n1) {
   extern __shared__ float shf[];
   constexpr int TR = 256 / K;
   constexpr int RB = 2 * TR;
@@ -687,9 +685,8 @@ __global__ void __launch_bounds__(256) k2b_u4(const Ctl* __restrict__ ctl,
   float* Ws = shf;                            // [tg][K][K]
   float* Ps = shf + (size_t)tg * K * K;       // [tg][RB][K]
   const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
-  const int rbase = blockIdx.x * RB;
-  const int i0 = rbase + rl, i1 = i0 + TR;
-  double n0 = 0.0, n1 = 0.0;
+  n0 = 0.0;
+  n1 = 0.0;
   for (int tb = 0; tb < M; tb += tg) {
     const int nt = min(tg, M - tb);
     __syncthreads();
@@ -739,6 +736,21 @@ __global__ void __launch_bounds__(256) k2b_u4(const Ctl* __restrict__ ctl,
       n1 += (double)s1;
     }
   }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k2b_u4(const Ctl* __restrict__ ctl,
+                                              const float* __restrict__ PQ,
+                                              const float* __restrict__ W32, int which, int N,
+                                              int M, int tg, double* __restrict__ U) {
+  static_assert(K == 16 || K == 32, "k2b_u4: K in {16, 32}");
+  if (ctl->stop) return;
+  constexpr int TR = 256 / K;
+  const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
+  const int rbase = blockIdx.x * 2 * TR;
+  const int i0 = rbase + rl, i1 = i0 + TR;
+  double n0, n1;
+  k2b_u4_rows<K>(PQ, W32, which, N, M, tg, rbase, n0, n1);
   if (i0 < N) U[(size_t)i0 * K + c] = n0;
   if (i1 < N) U[(size_t)i1 * K + c] = n1;
 }

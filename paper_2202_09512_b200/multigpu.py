@@ -140,8 +140,10 @@ def solve_on_grid(x, k: int, cfg: SolverConfig | None = None, p: int | None = No
         _, trace = eng.run(cfg.max_iters, float(dt.type(cfg.epsilon)), cfg.track_error, cfg.tolerance)
         a, r = eng.get_factors()
         timing = eng.timing()
+        exchange = "peer" if eng.info().get("peer_exchange") else "nccl"
     finally:
         eng.close()
     info = {k_: (v.tolist() if isinstance(v, np.ndarray) else v) for k_, v in info.items()}
     info["timing"] = timing
+    info["exchange"] = exchange
     return RescalFactors(a.astype(dt), r.astype(dt)), np.asarray(trace), info

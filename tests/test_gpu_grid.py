@@ -16,15 +16,22 @@ def _gpus():
     return _lib.device_count()
 
 
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_grid_matches_oracle(nproc):
+def test_grid_matches_oracle(nproc, exchange):
+    """exchange='peer': the per-iteration exchange runs over peer memory
+    (peer.cuh) wherever the dense K in {16, 32} path applies; 'nccl': RK_PEER=0
+    keeps the NCCL collectives."""
     if _gpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc + (10 if exchange == "nccl" else 0)),
            os.path.join(ROOT, "tools", "grid_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, RK_PEER="1" if exchange == "peer" else "0")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert out.returncode == 0 and line, out.stdout[-2000:] + out.stderr[-2000:]
     rep = json.loads(line[-1])
     assert rep["ok"], rep
+    used = {c.get("exchange") for c in rep["cases"] if c["engine"] != "sparse" and c["k"] in (16, 32)}
+    assert used == {exchange}, rep

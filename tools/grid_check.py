@@ -38,6 +38,7 @@ for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "aut
         good = rel_a <= 1e-4 and rel_r <= 1e-4 and derr <= 1e-5 and same_r and len(tr) == iters
         ok = ok and good
         results.append(dict(n=n, m=m, k=k, iters=iters, engine=engine, grid=[info["pr"], info["pc"]],
+                            exchange=info.get("exchange"),
                             relA=rel_a, relR=rel_r, dErr=derr, R_replicated=same_r, ok=good))
 # sparse CSR/CSC grid engine
 import scipy.sparse as sp
