@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_rl,
                  const __grid_constant__ CUtensorMap map_ch, const __grid_constant__ CUtensorMap map_cl,
                  K1Args args) {
+  pdl_entry();
   // map_x*: the block's slices as a (M*NR) x NC bf16 matrix (hi / lo planes)
   // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
   // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
                                                  float* __restrict__ P, float* __restrict__ Q,
                                                  int NR, int NC, int K, int M, int c, int nstrips,
                                                  int skip_if_stopped) {
+  pdl_entry();
   if (skip_if_stopped && ctl->stop) return;
   const int W = c * kTile;
   const int K4 = K / 4;

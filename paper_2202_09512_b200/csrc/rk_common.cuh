@@ -33,6 +33,15 @@ struct Ctl {
   double pad[5];
 };
 
+// Programmatic dependent launch: let the next kernel of the stream be
+// scheduled now (its CTAs wait in their own pdl_entry), then wait until every
+// kernel this one depends on has completed and its writes are visible. A no-op
+// pair for kernels launched without the PDL attribute.
+RK_DEV void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 RK_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
                                                       double eps, int mode, double* gscratch,
                                                       unsigned* __restrict__ counter,
                                                       float* __restrict__ W32) {
+  pdl_entry();
   if (ctl->stop) return;
   extern __shared__ double sh[];
   __shared__ double red[32];
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256, K == 16 ? 2 : 1)
   // products of a BR-row batch in fp32 (short chains: <= 16 terms) and adds
   // the batch partial into fp64 accumulators.
   static_assert(K == 16 || K == 32, "k2a_v4: K in {16, 32}");
+  pdl_entry();
   if (skip_if_stopped && ctl->stop) return;
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
                                               const float* __restrict__ W32,
                                               const double* __restrict__ Mm, int N, int M, int tg,
                                               double eps_m) {
+  pdl_entry();
   static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
   if (ctl->stop) return;
   extern __shared__ float shf[];
@@ -1060,6 +1063,7 @@ __global__ void __launch_bounds__(kThreads) k5_residual(const Ctl* __restrict__ 
                                                         int NC, int K, int M, int rows_valid,
                                                         int cols_valid, double* __restrict__ part,
                                                         int gate) {
+  pdl_entry();
   // gate: 1 = iteration use — run only in direct mode while tracking
   if (gate && (ctl->stop || !ctl->direct || !ctl->track || (ctl->iter < 1 && !ctl->tail))) return;
   extern __shared__ float shf[];

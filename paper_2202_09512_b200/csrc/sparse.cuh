@@ -105,7 +105,13 @@ RK_DEV void st_stream(float* a, float4 v, uint64_t pol) {
 // row); the gather loop keeps 4 independent loads in flight per lane; 32
 // registers -> 64 resident warps per SM (the pass is L1/L2-latency bound).
 template <int K>
-__global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ctl,
+#ifndef RK_SPC_MINB
+#define RK_SPC_MINB 8
+#endif
+#ifndef RK_SPC_UNR
+#define RK_SPC_UNR 4
+#endif
+__global__ void __launch_bounds__(256, RK_SPC_MINB) sp_csr_pass(const Ctl* __restrict__ ctl,
                                                       const int64_t* __restrict__ ptr,
                                                       const int* __restrict__ idx,
                                                       const float* __restrict__ val,
@@ -129,19 +135,19 @@ __global__ void __launch_bounds__(256, 8) sp_csr_pass(const Ctl* __restrict__ ct
     const float* At = A32 + (size_t)t * a_stride;
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t p = b;
-    for (; p + 4 <= e; p += 4) {
-      int j[4];
-      float v[4];
-      float4 a[4];
+    for (; p + RK_SPC_UNR <= e; p += RK_SPC_UNR) {
+      int j[RK_SPC_UNR];
+      float v[RK_SPC_UNR];
+      float4 a[RK_SPC_UNR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RK_SPC_UNR; ++u) {
         j[u] = ld_stream(idx + p + u, pf);
         v[u] = ld_stream(val + p + u, pf);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = ld_gather(At + (size_t)j[u] * K + 4 * q, pl);
+      for (int u = 0; u < RK_SPC_UNR; ++u) a[u] = ld_gather(At + (size_t)j[u] * K + 4 * q, pl);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RK_SPC_UNR; ++u) {
         y.x = fmaf(v[u], a[u].x, y.x);
         y.y = fmaf(v[u], a[u].y, y.y);
         y.z = fmaf(v[u], a[u].z, y.z);
