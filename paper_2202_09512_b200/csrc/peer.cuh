@@ -187,6 +187,45 @@ __global__ void __launch_bounds__(256) k2b_u4_peer(const Ctl* __restrict__ ctl, 
   }
 }
 
+// Sparse grid (K = 16): the numerator rows U_I / U_J come from sp_numer_tc
+// into local buffers; this pushes them into the owners' rxI / rxJ slots (the
+// reduce-scatter's data movement, summed at the owner in fixed order) and
+// signals like k2b_u4_peer. A stopped run still signals (peers never wait on
+// a rank that skipped).
+__global__ void __launch_bounds__(256) push_u_peer(const Ctl* __restrict__ ctl, const double* __restrict__ UI,
+                                                   const double* __restrict__ UJ, Args a) {
+  const unsigned e = a.ep[1] + 1u;
+  const int par = (int)(e & 1u);
+  const int K = a.K, K2 = K / 2;
+  if (!ctl->stop) {
+    const long long nI = (long long)a.pc * a.b * K2, nJ = (long long)a.pr * a.b * K2;  // double2 units
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nI + nJ;
+         x += (long long)gridDim.x * blockDim.x) {
+      const bool jside = x >= nI;
+      const long long el = jside ? x - nI : x;
+      const long long i = el / K2;
+      const int c2 = (int)(el - i * K2);
+      const int slot = (int)(i / a.b);
+      const long long r = i - (long long)slot * a.b;
+      const double2 v = reinterpret_cast<const double2*>(jside ? UJ : UI)[el];
+      double* dst;
+      if (!jside)
+        dst = reinterpret_cast<double*>(a.base[a.gi * a.pc + slot] + a.off_rxI) +
+              (((size_t)par * a.pc + a.gj) * a.b + r) * K;
+      else
+        dst = reinterpret_cast<double*>(a.base[slot * a.pc + a.gj] + a.off_rxJ) +
+              (((size_t)par * a.pr + a.gi) * a.b + r) * K;
+      reinterpret_cast<double2*>(dst)[c2] = v;
+    }
+  }
+  if (last_cta(&a.ep[6], gridDim.x)) {
+    for (int jj = 0; jj < a.pc; ++jj) st_release_sys(flag_at(a, a.gi * a.pc + jj, F_I, par, a.rank), e);
+    for (int ii = 0; ii < a.pr; ++ii) st_release_sys(flag_at(a, ii * a.pc + a.gj, F_J, par, a.rank), e);
+    a.ep[1] = e;
+    __threadfence();
+  }
+}
+
 // Owner: A_own <- A_own * (sum_j rxI + sum_i rxJ) / (A_own M + m eps), sent to
 // the row peers' rxA_row[gj] and the column peers' rxA_col[gi]. A stopped run
 // re-sends the unchanged rows (the peers' copies stay what they were).
@@ -252,11 +291,13 @@ __global__ void __launch_bounds__(kThreads) emit_peer(Args a, double* __restrict
     if (col) {
       Acol[el] = v;
       A32col[el] = (float)v;
+      if (AThc == nullptr) continue;  // sparse engine: fp32 copies only
       AThc[(size_t)c * NC + i] = hi;
       ATlc[(size_t)c * NC + i] = lo;
     } else {
       Arow[el] = v;
       A32row[el] = (float)v;
+      if (AThr == nullptr) continue;
       AThr[(size_t)c * NR + i] = hi;
       ATlr[(size_t)c * NR + i] = lo;
     }

@@ -575,7 +575,7 @@ void peer_teardown(rk_handle* h) {
 // arena through CUDA IPC; any rank failing (no P2P path, RK_PEER=0) makes all
 // ranks keep the NCCL schedule.
 void ensure_peer(rk_handle* h) {
-  if (!h->grid() || h->sparse || !(h->K == 16 || h->K == 32) || !h->W32) return;
+  if (!h->grid() || !(h->K == 16 || (h->K == 32 && !h->sparse)) || !h->W32) return;
   const int p = h->pr * h->pc;
   const int64_t key[4] = {h->K, h->m, h->piece, p};
   if (h->peer_tried && std::equal(key, key + 4, h->peer_key)) return;
@@ -586,12 +586,17 @@ void ensure_peer(rk_handle* h) {
   peer_teardown(h);
   h->peer_tried = true;
   std::copy(key, key + 4, h->peer_key);
-  static const bool disabled = [] {
+  // RK_PEER=0: NCCL, RK_PEER=1: peer memory, unset: peer memory while an A
+  // piece is <= 16 MB. Larger pieces (the sparse cfg4 grid: 67 MB) move faster
+  // through NCCL's copy protocols than through SM stores (measured 209 vs
+  // 199 it/s on 1x2, profiles/r01s3_peer_sp1_*).
+  static const int mode = [] {
     const char* e = std::getenv("RK_PEER");
-    return e && std::atoi(e) == 0;
+    return e ? std::atoi(e) : -1;
   }();
   const int K = h->K;
   const int64_t b = h->piece;
+  const bool disabled = mode == 0 || (mode < 0 && b * K * 8 > (16ll << 20));
   const int L = (int)((h->m + 1) * K * K + 1);
   auto al = [](int64_t v) { return round_up(v, 256); };
   rk::peer::Args& a = h->pargs;
@@ -878,11 +883,14 @@ void launch_k2f(rk_handle* h, int mode) {
 
 void launch_emit(rk_handle* h) {
   const int K = h->K;
+  // the sparse engine reads only the fp32 copies (no tensor-core planes)
   rk::emit_operands<<<h->num_sms * 2, 256, 0, h->stream>>>(h->Arow, (int)h->NR, K, h->A32row,
-                                                           h->ATh_row, h->ATl_row);
+                                                           h->sparse ? nullptr : h->ATh_row,
+                                                           h->sparse ? nullptr : h->ATl_row);
   if (h->grid())
     rk::emit_operands<<<h->num_sms * 2, 256, 0, h->stream>>>(h->Acol, (int)h->NC, K, h->A32col,
-                                                             h->ATh_col, h->ATl_col);
+                                                             h->sparse ? nullptr : h->ATh_col,
+                                                             h->sparse ? nullptr : h->ATl_col);
   RK_CUDA(cudaGetLastError());
   h->launches += h->grid() ? 2 : 1;
 }
@@ -986,6 +994,19 @@ void launch_k2b(rk_handle* h) {
         h->ctl, h->Arow, h->A32row, h->Q, nullptr, (int)h->NC, 0, h->wfrag, h->Mm, (int)h->cols_valid,
         (int)h->m, eps_m, 1, h->UJ);
     h->launches += 3;
+    if (h->peer) {
+      // numerator rows -> owners' slots, owner update, pieces -> peers (peer.cuh)
+      rk::peer::push_u_peer<<<h->num_sms * 4, 256, 0, h->stream>>>(h->ctl, h->UI, h->UJ, h->pargs);
+      phase_mark(h, h->profile, 5);
+      rk::peer::apply_peer<<<(unsigned)((h->piece + rpb - 1) / rpb), rk::kThreads, 0, h->stream>>>(
+          h->ctl, h->Arow + (size_t)h->gj * h->piece * K, h->Mm, K, eps_m, h->pargs);
+      rk::peer::emit_peer<<<h->num_sms * 2, rk::kThreads, 0, h->stream>>>(
+          h->pargs, h->Arow, (int)h->NR, h->A32row, nullptr, nullptr, h->Acol, (int)h->NC, h->A32col, nullptr,
+          nullptr);
+      RK_CUDA(cudaGetLastError());
+      h->launches += 3;
+      return;
+    }
   } else if (h->sparse) {
     // U_I = sum_t P_t R_t^T over the row set (dense P); U_J = sum_t z_t R_t with
     // z_t = X_t^T A_row streamed from the block's CSC (no P part: P_t lives on

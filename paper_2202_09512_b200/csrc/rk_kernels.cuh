@@ -938,6 +938,7 @@ __global__ void __launch_bounds__(kThreads) emit_operands(const double* __restri
     const int i = (int)(e / K), c = (int)(e - (int64_t)i * K);
     const double v = A[e];
     A32[e] = (float)v;
+    if (ATh == nullptr) continue;  // sparse engines: no tensor-core operand planes
     __nv_bfloat16 hi, lo;
     split_bf16(v, hi, lo);
     ATh[(size_t)c * rows + i] = hi;

@@ -1,5 +1,5 @@
-"""Grid-iteration cost split (experiment; results with skipped comm are not
-valid factorizations): device ms/iteration with and without the NCCL calls."""
+"""Grid-iteration cost split (per-phase CUDA events); CFG=cfg4 runs the sparse
+CSR/CSC grid engine on the cfg4 tensor (n=2^20, m=32, density 1e-5, k=16)."""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -10,10 +10,16 @@ from paper_2202_09512_b200.multigpu import make_grid_engine
 
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
-n = int(round(8192 * math.sqrt(world)))
-m, k = 16, 16
-eng, info = make_grid_engine(n, m, k)
-eng.fill_uniform(1)
+SPARSE = os.environ.get("CFG") == "cfg4"
+if SPARSE:
+    n, m, k = 1 << 20, 32, 16
+    eng, info = make_grid_engine(n, m, k, sparse=True)
+    eng.fill_sparse_uniform(1, int(round(1e-5 * n * n)))
+else:
+    n = int(round(8192 * math.sqrt(world)))
+    m, k = 16, 16
+    eng, info = make_grid_engine(n, m, k)
+    eng.fill_uniform(1)
 f0 = rk.random_init(n, k, m, 0)
 out = {}
 eng.set_factors(f0.A, f0.R)
