@@ -793,7 +793,7 @@ void launch_k2a(rk_handle* h, int skip) {
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
     const int nown = h->grid() ? (int)h->piece : 0;
     if (K == 16 && (!simt_gram || h->grid()))
-      rk::sp::sp_gram_tc<<<grid, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+      rk::sp::sp_gram_tc<<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
           nown);
     else if (K == 16)

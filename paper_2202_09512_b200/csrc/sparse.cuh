@@ -291,13 +291,20 @@ __global__ void __launch_bounds__(256) sp_gram(const Ctl* __restrict__ ctl, cons
 // of rows tq and tq+4 of the 8-row k-step from both A and B; rows are padded
 // to 24 floats (conflict-free). fp32 accumulation over <= 32 rows per warp,
 // then fp64; warp partials summed in fixed order; one fp64 partial per item.
+#ifndef RK_SG_NS
+#define RK_SG_NS 2
+#endif
+#ifndef RK_SG_CPS
+#define RK_SG_CPS 4
+#endif
 struct SpGramTc {
-  static constexpr int K = 16, SR = 128, LD = 24, NS = 4;
+  static constexpr int K = 16, SR = 128, LD = 24, NS = RK_SG_NS;
+  static constexpr int CPS = RK_SG_CPS;  // CTAs per SM
   static constexpr int ARR = SR * LD;  // floats per array per stage
-  static constexpr size_t smem = (size_t)NS * 2 * ARR * sizeof(float);  // 96 KB (>= 8 warps x 256 doubles)
+  static constexpr size_t smem = (size_t)NS * 2 * ARR * sizeof(float);  // 48 KB (>= 8 warps x 256 doubles)
 };
 
-__global__ void __launch_bounds__(256, 2) sp_gram_tc(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+__global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
                                                      const float* __restrict__ P, int n, int ldp, int M, int nchunk,
                                                      double* __restrict__ part, int skip_if_stopped,
                                                      const float* __restrict__ Aown = nullptr, int nown = 0) {
