@@ -450,6 +450,8 @@ def run_ours(args, dist, rank, world, local_rank):
                 x = rk.SparseRelTensor(slices)  # canonical form checked outside the timed region
                 rk.rescal_solve(x, k, rk.SolverConfig(max_iters=max(1, args.warmup), track_error=False,
                                                       device=local_rank), initial=f0)  # untimed warm-up call
+                from paper_2202_09512_b200 import solver as _solver
+                phases["engine_reused"] = getattr(_solver._CACHE, "entry", None) is not None
                 t0 = time.perf_counter()
                 f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, track_error=False,
                                                               device=local_rank), initial=f0)
@@ -477,6 +479,8 @@ def run_ours(args, dist, rank, world, local_rank):
                 # one untimed warm-up call (module loading, allocator warm-up), as for the device timing
                 rk.rescal_solve(x, k, rk.SolverConfig(max_iters=max(1, args.warmup), track_error=False,
                                                       device=local_rank), initial=f0)
+                from paper_2202_09512_b200 import solver as _solver
+                phases["engine_reused"] = getattr(_solver._CACHE, "entry", None) is not None
                 t0 = time.perf_counter()
                 f, tr = rk.rescal_solve(x, k, rk.SolverConfig(max_iters=args.steps, track_error=False,
                                                               device=local_rank), initial=f0)
@@ -527,7 +531,9 @@ def run_ours(args, dist, rank, world, local_rank):
                                    if world == 1 else "Engine grid API: upload_block + run + get_factors"),
                            "seconds": e2e_s, "phases": phases,
                            "protocol": "one untimed warm-up call, then one timed call of `steps` iterations "
-                                       "(upload of X + solve + factor download inside the timed region)"}
+                                       "(upload of X + solve + factor download inside the timed region; "
+                                       "tensors <= 1 GiB reuse the engine the warm-up call left behind, "
+                                       "as every repeated rescal_solve call does: phases.engine_reused)"}
         except Exception as exc:  # report, never hide
             line["e2e"] = {"value": None, "unit": "it/s", "error": repr(exc)[:300],
                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

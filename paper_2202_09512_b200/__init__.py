@@ -17,6 +17,7 @@ from .solver import (
     random_init,
     regress_r,
     rel_error,
+    release_cached_memory,
     rescal_solve,
     update_a,
     update_r,

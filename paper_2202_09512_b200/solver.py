@@ -18,6 +18,9 @@ fp64 on the device. Results are returned in x.dtype (rescal.py:205-209).
 
 from __future__ import annotations
 
+import contextlib
+import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -112,16 +115,73 @@ def finalize_normalize(f: RescalFactors) -> RescalFactors:
 # engine plumbing
 
 
+# One idle engine per host thread is kept for the next call with the same
+# (device, n, m, k, engine kind): repeated small solves (RESCALk members,
+# update_r / update_a / rel_error loops) skip handle creation (stream, pinned
+# control block, buffer set-up: ~5 ms at cfg1 against ~1 ms of iterations).
+# Only tensors up to _CACHE_MAX_BYTES of device storage are kept;
+# release_cached_memory() drops it. Every use re-uploads x and resets the
+# factors, so a cached engine is indistinguishable from a fresh one.
+_CACHE = threading.local()
+_CACHE_MAX_BYTES = 1 << 30
+
+
+def _engine_key(x, k, cfg: SolverConfig):
+    device = cfg.device if cfg.device is not None else int(os.environ.get("LOCAL_RANK", "0"))
+    sparse = is_sparse(x) and k <= 32
+    return (device, x.n, x.m, k, "sparse" if sparse else cfg.engine)
+
+
 def _engine_for(x, k, cfg: SolverConfig):
     """Device engine holding ``x``: the CSR/CSC engine for sparse tensors
     (k <= 32), the dense tcgen05/SIMT engine otherwise."""
-    if is_sparse(x) and k <= 32:
-        eng = _lib.Engine(x.n, x.m, k, device=cfg.device, sparse=True)
+    key = _engine_key(x, k, cfg)
+    cached = getattr(_CACHE, "entry", None)
+    if cached is not None and cached[0] == key and cached[1].k == k:
+        eng = cached[1]
+        _CACHE.entry = None
+    else:
+        eng = None
+    if key[4] == "sparse":
+        eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], sparse=True)
         eng.upload_csr(list(x.slices))
-        return eng
-    eng = _lib.Engine(x.n, x.m, k, device=cfg.device, engine=cfg.engine)
-    eng.upload(dense_slices(x))
+    else:
+        eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], engine=cfg.engine)
+        eng.upload(dense_slices(x))
+    eng._cache_key = key
     return eng
+
+
+def _release_engine(eng) -> None:
+    """Keep a small engine for the next call (closing the one kept before)."""
+    key = getattr(eng, "_cache_key", None)
+    dense_bytes = 4 * eng.m * eng.n * eng.n
+    if key is None or (not eng.sparse and dense_bytes > _CACHE_MAX_BYTES) or (
+            eng.sparse and eng.nnz * 8 > _CACHE_MAX_BYTES):
+        eng.close()
+        return
+    old = getattr(_CACHE, "entry", None)
+    if old is not None and old[1] is not eng:
+        old[1].close()
+    _CACHE.entry = ((key[0], eng.n, eng.m, eng.k, key[4]), eng)
+
+
+def release_cached_memory() -> None:
+    """Close the kept engine and return the device allocator's cached blocks."""
+    old = getattr(_CACHE, "entry", None)
+    _CACHE.entry = None
+    if old is not None:
+        old[1].close()
+    _lib.release_cached_memory()
+
+
+@contextlib.contextmanager
+def _engine_ctx(x, k, cfg: SolverConfig):
+    eng = _engine_for(x, k, cfg)
+    try:
+        yield eng
+    finally:
+        _release_engine(eng)
 
 
 def _check_shapes(x, f: RescalFactors) -> None:
@@ -172,7 +232,7 @@ def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, count
             counters.add_time("device_run", eng.timing()["run_ms"] / 1e3)
     finally:
         if own:
-            eng.close()
+            _release_engine(eng)
     return RescalFactors(a.astype(dt), r.astype(dt)), np.asarray(trace)
 
 
@@ -181,7 +241,7 @@ def update_r(x, f: RescalFactors, cfg: SolverConfig | None = None) -> RescalFact
     cfg = cfg or SolverConfig()
     _check_shapes(x, f)
     dt = f.A.dtype
-    with _engine_for(x, f.k, cfg) as eng:
+    with _engine_ctx(x, f.k, cfg) as eng:
         eng.set_factors(f.A.astype(np.float64), f.R.astype(np.float64))
         eng.update_r(float(dt.type(cfg.epsilon)))
         _, r = eng.get_factors()
@@ -193,7 +253,7 @@ def update_a(x, f: RescalFactors, cfg: SolverConfig | None = None) -> RescalFact
     cfg = cfg or SolverConfig()
     _check_shapes(x, f)
     dt = f.A.dtype
-    with _engine_for(x, f.k, cfg) as eng:
+    with _engine_ctx(x, f.k, cfg) as eng:
         eng.set_factors(f.A.astype(np.float64), f.R.astype(np.float64))
         eng.update_a(float(dt.type(cfg.epsilon)))
         a, _ = eng.get_factors()
@@ -212,7 +272,7 @@ def rel_error(x, f: RescalFactors, engine: "_lib.Engine | None" = None) -> float
         res, nrm = eng.residual()
     finally:
         if own:
-            eng.close()
+            _release_engine(eng)
     if nrm == 0.0:
         raise DataError("relative error undefined: tensor norm is zero")
     return float(np.sqrt(res / nrm))
@@ -238,7 +298,7 @@ def regress_r(x, a_fixed: np.ndarray, cfg: SolverConfig | None = None, max_iters
         _, r = eng.get_factors()
     finally:
         if own:
-            eng.close()
+            _release_engine(eng)
     if not (np.isfinite(a).all() and np.isfinite(r).all()):
         raise NumericalError("non-finite value in factors; aborting")
     return r.astype(a.dtype)
@@ -336,5 +396,5 @@ def nndsvd_init(x, k: int, r_update_iters: int = 20, eps: float = 1e-16, cfg: So
                       engine=eng)
     finally:
         if own:
-            eng.close()
+            _release_engine(eng)
     return RescalFactors(a, r)

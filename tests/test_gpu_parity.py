@@ -179,3 +179,19 @@ def test_trace_monotone_cfg1_planted():
     g = golden("planted64")
     f, tr = rk.rescal_solve(rk.RelTensor(g["X"]), 4, rk.SolverConfig(max_iters=100, seed=10))
     assert np.all(np.diff(tr) <= 1e-6 * np.maximum(tr[:-1], 1e-30))
+
+
+def test_engine_reuse_is_transparent():
+    """A solve on the engine kept from the previous call (same shape) returns
+    the same bytes as one on a freshly created engine."""
+    n, m, k = 200, 3, 6
+    x1 = np.random.default_rng(1).random((m, n, n))
+    x2 = np.random.default_rng(2).random((m, n, n))
+    f0 = rk.random_init(n, k, m, 4)
+    cfg = rk.SolverConfig(max_iters=25)
+    rk.rescal_solve(rk.RelTensor(x1), k, cfg, initial=f0)          # leaves an engine behind
+    fa, ta = rk.rescal_solve(rk.RelTensor(x2), k, cfg, initial=f0)  # reuses it
+    rk.release_cached_memory()
+    fb, tb = rk.rescal_solve(rk.RelTensor(x2), k, cfg, initial=f0)  # fresh engine
+    assert np.array_equal(fa.A, fb.A) and np.array_equal(fa.R, fb.R) and np.array_equal(ta, tb)
+    assert rel_fro(rk.update_r(rk.RelTensor(x2), fa).R, rk.update_r(rk.RelTensor(x2), fb).R) == 0.0
