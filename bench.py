@@ -577,12 +577,19 @@ def run_rescalk(args, dist, rank, world, local_rank):
 
     cfg = rk.SolverConfig(max_iters=iters, device=local_rank)
     pcfg = rk.PerturbConfig(delta=0.02, base_seed=0)
-    # warm-up: a 1-member-per-k run on a tiny slice of work (compile, allocate)
+    claim = None
+    if world > 1:  # dynamic member assignment through the rendezvous store
+        from torch.distributed import distributed_c10d as _c10d
+
+        store = _c10d._get_default_store()
+        tag = f"rk_member_{time.time_ns() if rank == 0 else 0}"
+        tag = allgather(tag)[0]
+        claim = lambda: store.add(tag, 1)  # noqa: E731
     barrier(dist)
     t0 = time.perf_counter()
     rep = rk.rescalk(x, k_min, k_max, r, cfg=cfg, pcfg=pcfg,
                      world=(rank, world) if world > 1 else None,
-                     allgather=allgather if world > 1 else None)
+                     allgather=allgather if world > 1 else None, claim=claim)
     secs = max_over_ranks(dist, time.perf_counter() - t0)
     members = (k_max - k_min + 1) * r
     units = members * iters
@@ -594,8 +601,8 @@ def run_rescalk(args, dist, rank, world, local_rank):
         "config": {"workload": f"cfg5: rescalk dense m={m} n={n} k={k_min}..{k_max} r={r} "
                                f"iters={iters} (full sweep is k=2..16)",
                    "per_step": "one member MU iteration inside rescalk() (tracked, default config)",
-                   "parallelism": f"replicas x{world}"},
-        "k_opt": rep.k_opt, "seconds": secs, "members": members,
+                   "parallelism": f"replicas x{world}" + (" (members claimed dynamically)" if world > 1 else "")},
+        "k_opt": rep.k_opt, "seconds": secs, "members": members, "timing_rank0": rep.timing,
         "per_k": {str(e.k): {"s_min": e.s_min, "rel_error": e.rel_error} for e in rep.entries},
         "e2e": {"value": units / secs, "unit": "member-it/s",
                 "h2d_bytes_per_step": int(xh.nbytes / units), "d2h_bytes_per_step": 0,

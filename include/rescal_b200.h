@@ -198,6 +198,16 @@ int rk_grid_init(rk_handle* h, int32_t pr, int32_t pc, int32_t rank, const void*
                  int64_t n_global);
 int rk_nccl_unique_id(void* out128);
 
+/* RESCALk ensembles spread over GPUs ("replicas", model_select.py:445-471 with
+ * the members distributed; one process per GPU): rank 0 uploads the tensor and
+ * rk_tensor_export writes a <= 256-byte record (CUDA IPC handles of the device
+ * planes + norms) that the caller ships to the other ranks; rk_tensor_import
+ * copies the planes peer-to-peer over NVLink instead of every rank uploading
+ * the same tensor over the host links. The exporter must not perturb or free
+ * its tensor until every importer returned. */
+int rk_tensor_export(rk_handle* h, void* out, int32_t out_bytes);
+int rk_tensor_import(rk_handle* h, const void* in);
+
 /* Timing of the last rk_run (device time, CUDA events on the engine stream):
  * out[0]=total ms, out[1]=slice-contraction (K1) ms per launch averaged,
  * out[2]=number of K1 launches, out[3]=kernel launches total. */

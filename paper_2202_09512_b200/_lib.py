@@ -59,6 +59,8 @@ SIGNATURES = {
     "rk_perturb": (ctypes.c_int, [_vp, _u64, _u64, _u64, _u64, _f64, _i64, _i64, _i64, _pi64]),
     "rk_grid_init": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _i64]),
     "rk_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "rk_tensor_export": (ctypes.c_int, [_vp, _vp, _i32]),
+    "rk_tensor_import": (ctypes.c_int, [_vp, _vp]),
     "rk_last_timing": (ctypes.c_int, [_vp, _pd, _i32]),
     "rk_stream": (_vp, [_vp]),
     "rk_info": (ctypes.c_int, [_vp, _pi64, _i32]),
@@ -331,6 +333,18 @@ class Engine:
     def restore(self):
         """Undo rk_perturb: the device tensor goes back to the uploaded one."""
         check(self._lib.rk_restore(self._h))
+
+    # RESCALk replicas ----------------------------------------------------------
+    def tensor_export(self) -> bytes:
+        """IPC record of this engine's uploaded dense tensor (rank 0 of a replica set)."""
+        buf = ctypes.create_string_buffer(256)
+        check(self._lib.rk_tensor_export(self._h, buf, 256))
+        return buf.raw
+
+    def tensor_import(self, record: bytes):
+        """Copy an exported tensor peer-to-peer (NVLink) into this engine."""
+        buf = ctypes.create_string_buffer(bytes(record), 256)
+        check(self._lib.rk_tensor_import(self._h, buf))
 
     # p_r x p_c grid ------------------------------------------------------------
     def grid_init(self, pr, pc, rank, nccl_id: bytes):

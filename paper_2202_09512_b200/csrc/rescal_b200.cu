@@ -1202,6 +1202,17 @@ void alloc_tensor(rk_handle* h) {
   h->Xl = dalloc<__nv_bfloat16>(count);
 }
 
+// A new tensor invalidates the unperturbed base copies rk_perturb keeps (they
+// are re-taken from the new tensor at the next rk_perturb).
+void drop_base_copies(rk_handle* h) {
+  dfree(h->Xh0);
+  dfree(h->Xl0);
+  dfree(h->csr_val0);
+  dfree(h->csc_val0);
+  h->Xh0 = h->Xl0 = nullptr;
+  h->csr_val0 = h->csc_val0 = nullptr;
+}
+
 template <typename T>
 void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
   // chunks of host rows through a pinned staging ring when the host buffer is
@@ -1506,6 +1517,7 @@ void upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int32_
   h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
   h->have_x = true;
   h->perturbed = false;
+  drop_base_copies(h);
   if (timing)
     std::fprintf(stderr, "[rk] upload_csr_slices: copy+validate %.1f ms, csc build %.1f ms (nnz %lld)\n", t_copy,
                  ms_since(t_csc), (long long)nnz);
@@ -1766,6 +1778,7 @@ int rk_fill_sparse_uniform(rk_handle* h, uint64_t seed, int64_t nnz_target_per_s
     h->norm2 = h->norm2_dev = h->norm2_orig = global_sum(h, s2);
     h->have_x = true;
     h->perturbed = false;
+    drop_base_copies(h);
   });
 }
 
@@ -1839,6 +1852,7 @@ int rk_upload_dense(rk_handle* h, const void* x, int32_t dtype) {
     finish_upload_norm(h, true);
     h->have_x = true;
     h->perturbed = false;
+    drop_base_copies(h);
   });
 }
 
@@ -1859,6 +1873,7 @@ int rk_upload_block(rk_handle* h, const void* x, int32_t dtype, int64_t rows, in
     h->norm2 = sq_norm_global;
     h->have_x = true;
     h->perturbed = false;
+    drop_base_copies(h);
   });
 }
 
@@ -1874,6 +1889,7 @@ int rk_fill_uniform(rk_handle* h, uint64_t seed) {
     finish_upload_norm(h, true);
     h->have_x = true;
     h->perturbed = false;
+    drop_base_copies(h);
   });
 }
 
@@ -2499,6 +2515,62 @@ int rk_grid_init(rk_handle* h, int32_t pr, int32_t pc, int32_t rank, const void*
     alloc_tensor(h);
     alloc_factor_buffers(h);
     h->have_x = false;
+  });
+}
+
+// RESCALk replicas: rank 0 exports its uploaded tensor planes through CUDA
+// IPC; the other ranks copy them peer-to-peer over NVLink.
+struct TensorExport {
+  cudaIpcMemHandle_t xh, xl;
+  double norm2, norm2_dev;
+  int64_t m, NR, NC;
+};
+
+int rk_tensor_export(rk_handle* h, void* out, int32_t out_bytes) {
+  return guarded([&] {
+    RK_REQUIRE(h && out && out_bytes >= (int32_t)sizeof(TensorExport), RK_ERR_DATA, "bad argument");
+    RK_REQUIRE(!h->sparse && !h->grid() && h->have_x && !h->perturbed, RK_ERR_DATA,
+               "export needs an uploaded, unperturbed dense single-GPU tensor");
+    RK_CUDA(cudaSetDevice(h->dev));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    TensorExport e{};
+    RK_CUDA(cudaIpcGetMemHandle(&e.xh, h->Xh));
+    RK_CUDA(cudaIpcGetMemHandle(&e.xl, h->Xl));
+    e.norm2 = h->norm2;
+    e.norm2_dev = h->norm2_dev;
+    e.m = h->m;
+    e.NR = h->NR;
+    e.NC = h->NC;
+    std::memcpy(out, &e, sizeof(e));
+  });
+}
+
+int rk_tensor_import(rk_handle* h, const void* in) {
+  return guarded([&] {
+    RK_REQUIRE(h && in, RK_ERR_DATA, "null argument");
+    TensorExport e;
+    std::memcpy(&e, in, sizeof(e));
+    RK_REQUIRE(!h->sparse && !h->grid() && e.m == h->m && e.NR == h->NR && e.NC == h->NC, RK_ERR_DATA,
+               "exported tensor does not match this handle");
+    RK_CUDA(cudaSetDevice(h->dev));
+    void *ph = nullptr, *pl = nullptr;
+    RK_CUDA(cudaIpcOpenMemHandle(&ph, e.xh, cudaIpcMemLazyEnablePeerAccess));
+    cudaError_t err = cudaIpcOpenMemHandle(&pl, e.xl, cudaIpcMemLazyEnablePeerAccess);
+    if (err != cudaSuccess) {
+      cudaIpcCloseMemHandle(ph);
+      RK_CUDA(err);
+    }
+    const size_t bytes = (size_t)h->m * h->NR * h->NC * sizeof(__nv_bfloat16);
+    RK_CUDA(cudaMemcpyAsync(h->Xh, ph, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    RK_CUDA(cudaMemcpyAsync(h->Xl, pl, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    cudaIpcCloseMemHandle(ph);
+    cudaIpcCloseMemHandle(pl);
+    h->norm2 = e.norm2;
+    h->norm2_dev = h->norm2_dev0 = e.norm2_dev;
+    h->have_x = true;
+    h->perturbed = false;
+    drop_base_copies(h);
   });
 }
 

@@ -10,8 +10,13 @@ out of the device scope) is numpy/scipy here.
 
 Ensemble spreading across GPUs (``north_star``): pass ``world=(rank, size)``
 (one process per GPU, e.g. under torchrun) and an ``allgather`` callable; each
-rank solves the members with (index % size == rank) and the factors are
-gathered before clustering — "replicas only", no data-path collective.
+rank solves the members with (index % size == rank) — or takes them
+dynamically through ``claim`` — the factors are gathered once for the whole
+sweep, and the per-k clustering / refit runs on rank (k - k_min) % size with
+the entries gathered after. The tensor is uploaded by rank 0 only; the other
+replicas copy its device planes peer-to-peer over NVLink (CUDA IPC,
+rk_tensor_export / rk_tensor_import). The iterations themselves exchange
+nothing ("replicas only").
 """
 
 from __future__ import annotations
@@ -24,7 +29,7 @@ from scipy.optimize import linear_sum_assignment
 
 from . import _lib
 from .containers import dense_slices, tensor_dtype
-from .exceptions import DataError
+from .exceptions import DataError, RescalkitError
 from .solver import RescalFactors, SolverConfig, finalize_normalize, random_init, rescal_solve
 
 _SEED_TAG_PERTURB = 3
@@ -279,13 +284,17 @@ def _solve_member(eng, x, k, q, cfg, pcfg, dt):
 
 def rescalk(x, k_min: int, k_max: int, r: int, cfg: SolverConfig | None = None,
             pcfg: PerturbConfig | None = None, ctx=None, tau_s: float = 0.75,
-            world: tuple | None = None, allgather=None) -> SelectionReport:
+            world: tuple | None = None, allgather=None, claim=None) -> SelectionReport:
     """Factorize r resamplings per k, score stability, pick k_opt
     (model_select.py:422-503; serial semantics, device compute).
 
     ``ctx`` (the reference's in-process grid) is not used: grids here are
     process grids (multigpu.py). ``world``/``allgather`` spread the members
-    over GPUs (see module docstring).
+    over GPUs (see module docstring); ``claim`` (optional, with ``world``) is
+    a callable shared by all ranks returning 1, 2, 3, ... in turn (e.g. a
+    torch.distributed store counter): members are then taken dynamically, so
+    a rank whose tensor upload was slow takes fewer. Results do not depend on
+    which rank solved a member.
     """
     cfg = cfg or SolverConfig()
     pcfg = pcfg or PerturbConfig()
@@ -299,35 +308,80 @@ def rescalk(x, k_min: int, k_max: int, r: int, cfg: SolverConfig | None = None,
     eng = _lib.Engine(x.n, x.m, k_min, device=cfg.device, engine=cfg.engine)
     entries, timing = [], {"per_k_seconds": {}}
     try:
-        eng.upload(dense_slices(x))
-        member = 0
-        for k in range(k_min, k_max + 1):
+        if size > 1 and allgather is not None:
+            # the replicas share one tensor: rank 0 uploads it over PCIe, the
+            # others copy its device planes peer-to-peer over NVLink (every
+            # rank uploading the same tensor contends for the host links);
+            # a rank without a peer path uploads its own copy
+            if rank == 0:
+                eng.upload(dense_slices(x))
+            record = allgather(eng.tensor_export() if rank == 0 else None)[0]
+            if rank != 0:
+                try:
+                    eng.tensor_import(record)
+                except RescalkitError:
+                    eng.upload(dense_slices(x))
+            allgather(None)  # rank 0 keeps its planes unperturbed until every copy is done
+        else:
+            eng.upload(dense_slices(x))
+        timing["upload_seconds"] = time.perf_counter() - t_start
+        ks = list(range(k_min, k_max + 1))
+        # 1) the members: (k, q) in the reference's order, member i on rank
+        #    i % size — one gather for the whole sweep, so no rank idles at a
+        #    per-k barrier (each member depends only on its (k, q) seeds)
+        mine = {}
+        order = [(k, q) for k in ks for q in range(1, r + 1)]
+        if claim is not None and size > 1:
+            while True:
+                i = int(claim()) - 1
+                if i >= len(order):
+                    break
+                k, q = order[i]
+                mine[(k, q)] = _solve_member(eng, x, k, q, cfg, pcfg, dt)
+        else:
+            for i, (k, q) in enumerate(order):
+                if i % size == rank:
+                    mine[(k, q)] = _solve_member(eng, x, k, q, cfg, pcfg, dt)
+        timing["members_seconds"] = time.perf_counter() - t_start - timing["upload_seconds"]
+        if size > 1:
+            t_g = time.perf_counter()
+            merged = {}
+            for part in allgather(mine):
+                merged.update(part)
+            mine = merged
+            timing["gather_seconds"] = time.perf_counter() - t_g
+        eng.restore()
+        # 2) per k: clustering, stability, refit and residual on the original
+        #    tensor — k on rank (k - k_min) % size, entries gathered after
+        from .solver import regress_r, rel_error
+        mine_entries = {}
+        for i, k in enumerate(ks):
+            if i % size != rank:
+                continue
             t_k = time.perf_counter()
-            mine = {}
-            for q in range(1, r + 1):
-                if member % size == rank:
-                    mine[q] = _solve_member(eng, x, k, q, cfg, pcfg, dt)
-                member += 1
-            if size > 1:
-                merged = {}
-                for part in allgather(mine):
-                    merged.update(part)
-                mine = merged
-            a_cols = [mine[q][0] for q in range(1, r + 1)]
-            r_slabs = [mine[q][1] for q in range(1, r + 1)]
-            solved = all(mine[q][2] for q in range(1, r + 1))
+            a_cols = [mine[(k, q)][0] for q in range(1, r + 1)]
+            r_slabs = [mine[(k, q)][1] for q in range(1, r + 1)]
+            solved = all(mine[(k, q)][2] for q in range(1, r + 1))
             ens = FactorEnsemble(np.stack(a_cols, axis=2),
                                  np.stack([np.transpose(s, (1, 2, 0)) for s in r_slabs], axis=3))
             clus = custom_cluster(ens)
             stats = cluster_stability(clus.ensemble)
-            eng.restore()
-            from .solver import regress_r, rel_error
             core = regress_r(x, clus.medians, cfg, engine=eng)
             err = rel_error(x, RescalFactors(clus.medians, core), engine=eng)
-            entries.append(SelectionEntry(k=k, s_min=stats.s_min, s_avg=stats.s_avg, rel_error=err,
-                                          medians=clus.medians, core=core,
-                                          converged=clus.converged and solved))
+            mine_entries[k] = SelectionEntry(k=k, s_min=stats.s_min, s_avg=stats.s_avg, rel_error=err,
+                                             medians=clus.medians, core=core,
+                                             converged=clus.converged and solved)
             timing["per_k_seconds"][str(k)] = time.perf_counter() - t_k
+        if size > 1:
+            merged, secs, members_s = {}, {}, []
+            for part in allgather((mine_entries, timing["per_k_seconds"], timing["members_seconds"],
+                                   timing["upload_seconds"])):
+                merged.update(part[0])
+                secs.update(part[1])
+                members_s.append((round(part[3], 3), round(part[2], 3)))
+            mine_entries, timing["per_k_seconds"] = merged, secs
+            timing["upload_members_seconds_per_rank"] = members_s
+        entries = [mine_entries[k] for k in ks]
     finally:
         eng.close()
     k_opt = select_k(entries, tau_s)
