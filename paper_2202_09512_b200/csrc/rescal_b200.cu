@@ -266,7 +266,10 @@ struct rk_handle {
       *d_slot_count = nullptr;
   CUtensorMap maps[6];
   // graph
-  cudaGraphExec_t graph = nullptr;
+  // [track][batched]: one iteration, or kGraphBatch iterations in one graph;
+  // the untracked variants leave out the (then always gated-off) K5 node
+  cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int graph_launches[2][2] = {{0, 0}, {0, 0}};
   bool use_graph = true;
   // timing
   bool profile = false;
@@ -278,7 +281,8 @@ struct rk_handle {
   int ph_iters = 0;
   double ph_ms[kPhases] = {0, 0, 0, 0, 0, 0};
   double last_ms = 0.0, k1_ms_sum = 0.0;
-  int k1_count = 0, launches = 0, iter_launches = 0;
+  int k1_count = 0, launches = 0;
+  static constexpr int kGraphBatch = 16;
   double eps = 1e-16;
 
   // sparse tensor (CSR + device-built CSC, fp32 values)
@@ -306,16 +310,22 @@ struct rk_handle {
 
 namespace {
 
+void drop_graphs(rk_handle* h) {
+  for (auto& row : h->graphs)
+    for (auto& g : row)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+}
+
 size_t k2f_smem(int K) {
   size_t s = (size_t)5 * K * K * sizeof(double);
   return s <= 200 * 1024 ? s : 0;
 }
 
 void free_factor_buffers(rk_handle* h) {
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);
   dfree(h->numer);
   h->numer = nullptr;
   dfree(h->gpart);
@@ -520,6 +530,10 @@ void alloc_factor_buffers(rk_handle* h) {
   RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
   const size_t k5s = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
   RK_CUDA(cudaFuncSetAttribute(rk::k5_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s));
+  if (K == 16)
+    RK_CUDA(cudaFuncSetAttribute(rk::k2af<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rk::k2af_smem(16)));
+  if (K == 32)
+    RK_CUDA(cudaFuncSetAttribute(rk::k2af<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rk::k2af_smem(32)));
   if (k2f_smem(K))
     RK_CUDA(cudaFuncSetAttribute(rk::k2f_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
   if (rk::k2b_fused_smem(K, (int)M) <= 200 * 1024)
@@ -579,10 +593,7 @@ void ensure_peer(rk_handle* h) {
   const int p = h->pr * h->pc;
   const int64_t key[4] = {h->K, h->m, h->piece, p};
   if (h->peer_tried && std::equal(key, key + 4, h->peer_key)) return;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);
   peer_teardown(h);
   h->peer_tried = true;
   std::copy(key, key + 4, h->peer_key);
@@ -849,6 +860,46 @@ void launch_k2a(rk_handle* h, int skip) {
   h->launches += 1;
 }
 
+// K2a + K2f fused (single GPU, dense, K in {16, 32}) behind RK_K2AF=1:
+// bit-identical to the two-kernel path but measured 0.3-2 % slower (every
+// cluster also forms G; the per-slice chain, not the launch, is the cost),
+// so the two-kernel path stays the default (tools/k2af_check.py).
+bool use_k2af(const rk_handle* h) {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_K2AF");
+    return e && e[0] == '1';
+  }();
+  return on && h->fast && !h->sparse && !h->grid() && (h->K == 16 || h->K == 32);
+}
+
+void launch_k2af(rk_handle* h) {
+  const int K = h->K;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(rk::kCluster, (unsigned)h->m);
+  cfg.blockDim = dim3(K == 16 ? 512 : 256);
+  cfg.dynamicSmemBytes = rk::k2af_smem(K);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = rk::kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
+  unsigned* counter = h->counters + h->m + 1;
+  if (K == 16)
+    RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2af<16>, h->ctl, (const float*)h->A32row, (const float*)h->P, (int)h->NR,
+                               (int)h->m, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, (const double*)h->rpart,
+                               h->nr, h->trace_dev, h->eps, counter, h->W32));
+  else
+    RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2af<32>, h->ctl, (const float*)h->A32row, (const float*)h->P, (int)h->NR,
+                               (int)h->m, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, (const double*)h->rpart,
+                               h->nr, h->trace_dev, h->eps, counter, h->W32));
+  h->launches += 1;
+}
+
 // On a grid: append the direct-residual scalar to the reduced [G, S_t] and
 // all-reduce over the world communicator (the only fp64 all-reduce of the
 // iteration; it returns identical bytes on every rank, so R stays replicated).
@@ -1100,16 +1151,22 @@ void phase_mark(rk_handle* h, bool timed, int idx) {
 }
 
 // phases: 0 K1(+reduce) | 1 K5+K2a | 2 grid all-reduce | 3 K2f | 4 K2b/numerator (+RS) | 5 A update/gather
-void enqueue_iteration(rk_handle* h, bool timed) {
+void enqueue_iteration(rk_handle* h, bool timed, bool with_k5) {
   phase_mark(h, timed, 0);
   launch_k1(h, timed);
   phase_mark(h, timed, 1);
-  launch_k5(h, 1);
-  launch_k2a(h, 1);
-  phase_mark(h, timed, 2);
-  if (h->grid()) grid_allreduce_parts(h, true);
-  phase_mark(h, timed, 3);
-  launch_k2f(h, 0);
+  if (with_k5) launch_k5(h, 1);
+  if (use_k2af(h)) {
+    launch_k2af(h);
+    phase_mark(h, timed, 2);
+    phase_mark(h, timed, 3);
+  } else {
+    launch_k2a(h, 1);
+    phase_mark(h, timed, 2);
+    if (h->grid()) grid_allreduce_parts(h, true);
+    phase_mark(h, timed, 3);
+    launch_k2f(h, 0);
+  }
   phase_mark(h, timed, 4);
   launch_k2b(h);
   phase_mark(h, timed, 6);
@@ -1146,6 +1203,7 @@ void read_ctl(rk_handle* h) {
 
 void ensure_trace(rk_handle* h, int cap) {
   if (cap + 1 > h->trace_cap) {
+    drop_graphs(h);  // the captured trace/commit nodes hold the old pointer
     dfree(h->trace_dev);
     h->trace_cap = cap + 1;
     h->trace_dev = dalloc<double>(h->trace_cap);
@@ -1828,10 +1886,7 @@ int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
     else if (key == 4) h->skip_comm = value != 0;
     else if (key == 2) {
       h->use_graph = value != 0;
-      if (!h->use_graph && h->graph) {
-        cudaGraphExecDestroy(h->graph);
-        h->graph = nullptr;
-      }
+      if (!h->use_graph) drop_graphs(h);
     } else
       throw RkError{RK_ERR_DATA, "unknown option"};
   });
@@ -2013,10 +2068,7 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     check_ready(h);
     RK_REQUIRE(iters >= 1, RK_ERR_DATA, "max_iters must be >= 1");
     if (track_error) RK_REQUIRE(h->norm2 > 0.0, RK_ERR_DATA, "cannot track relative error: tensor norm is zero");
-    if (h->eps != eps && h->graph) {
-      cudaGraphExecDestroy(h->graph);
-      h->graph = nullptr;
-    }
+    if (h->eps != eps) drop_graphs(h);
     h->eps = eps;
     ensure_peer(h);
     ensure_trace(h, iters + 1);
@@ -2027,30 +2079,40 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
     const bool timed = h->profile;
     // NCCL collectives are stream-capturable: the grid iteration is a graph too
     const bool graph = h->use_graph && !timed;
-    if (graph && !h->graph) {
-      cudaGraph_t g;
-      RK_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      const int before = h->launches;
-      enqueue_iteration(h, false);
-      h->iter_launches = h->launches - before;
-      RK_CUDA(cudaStreamEndCapture(h->stream, &g));
-      RK_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
-      cudaGraphDestroy(g);
-    }
+    const int ti = track_error ? 1 : 0;
+    auto get_graph = [&](int batched) {
+      cudaGraphExec_t& ge = h->graphs[ti][batched];
+      if (!ge) {
+        cudaGraph_t g;
+        RK_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        const int before = h->launches;
+        for (int q = 0; q < (batched ? rk_handle::kGraphBatch : 1); ++q) enqueue_iteration(h, false, ti != 0);
+        h->graph_launches[ti][batched] = h->launches - before;
+        RK_CUDA(cudaStreamEndCapture(h->stream, &g));
+        RK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+      }
+      return ge;
+    };
     RK_CUDA(cudaEventRecord(h->ev_run0, h->stream));
-    const int chunk = 16;
+    const int chunk = rk_handle::kGraphBatch;
     cudaEvent_t chk[2];
     for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&chk[i], cudaEventDisableTiming));
     h->launches = 0;
     int launched = 0, pending = -1;
     while (launched < iters) {
       const int nthis = std::min(chunk, iters - launched);
-      for (int q = 0; q < nthis; ++q) {
-        if (graph) {
-          RK_CUDA(cudaGraphLaunch(h->graph, h->stream));
-          h->launches += h->iter_launches;
-        } else {
-          enqueue_iteration(h, timed);
+      if (graph && nthis == rk_handle::kGraphBatch) {
+        RK_CUDA(cudaGraphLaunch(get_graph(1), h->stream));
+        h->launches += h->graph_launches[ti][1];
+      } else {
+        for (int q = 0; q < nthis; ++q) {
+          if (graph) {
+            RK_CUDA(cudaGraphLaunch(get_graph(0), h->stream));
+            h->launches += h->graph_launches[ti][0];
+          } else {
+            enqueue_iteration(h, timed, ti != 0);
+          }
         }
       }
       launched += nthis;

@@ -1,0 +1,31 @@
+"""A/B of the fused K2a+K2f kernel (k2af) against the two-kernel path:
+python tools/k2af_check.py cfgX  (run once with RK_K2AF=1 and once without).
+Prints the graph-replayed ms/iteration (untracked and tracked), the trace and
+a hash of the factor bytes after 20 iterations (the two paths must agree bit
+for bit)."""
+import hashlib, json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import paper_2202_09512_b200 as rk
+from paper_2202_09512_b200 import _lib
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+n, m, k = {"cfg1": (256, 8, 4), "cfg5": (16384, 8, 16), "cfg2": (8192, 16, 16),
+           "cfg3": (32768, 16, 32), "k32s": (4096, 8, 32), "k20": (2048, 4, 20)}[cfg]
+eng = _lib.Engine(n, m, k, device=0)
+eng.fill_uniform(1)
+f0 = rk.random_init(n, k, m, 0)
+out = {"cfg": cfg, "k2af": os.environ.get("RK_K2AF", "0")}
+for track in (False, True):
+    eng.set_factors(f0.A, f0.R)
+    done, tr = eng.run(20, 1e-16, track)
+    a, r = eng.get_factors()
+    out[f"hash_track{int(track)}"] = hashlib.sha1(a.tobytes() + r.tobytes()).hexdigest()[:16]
+    out[f"trace_track{int(track)}"] = [float(x) for x in np.asarray(tr)[-3:]]
+    reps = 200 if n <= 8192 else 20
+    eng.set_factors(f0.A, f0.R)
+    eng.run(reps, 1e-16, track)
+    out[f"ms_per_iter_track{int(track)}"] = eng.timing()["run_ms"] / reps
+print(json.dumps(out))
+eng.close()
