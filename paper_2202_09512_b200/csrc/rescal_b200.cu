@@ -557,13 +557,15 @@ void alloc_factor_buffers(rk_handle* h) {
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
     else
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
-    const int rb = 2 * (256 / K);
-    const int tg = rk::k2b_v4_tg(K, (int)M);
+    const int rb = rk::k2b_v4_rb(K, h->NR);
+    const int tg = rk::k2b_v4_tg(K, (int)M, h->NR);
     const int smem = tg * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
     if (K == 16)
-      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    else if (rk::k2b_v4_rpt(K, h->NR) == 8)
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     else
-      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
   const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
@@ -993,16 +995,20 @@ void launch_k2b(rk_handle* h) {
     return;
   }
   if (h->fast) {
-    const int rb = 2 * (256 / K);
-    const int tg = rk::k2b_v4_tg(K, (int)h->m);
+    const int rb = rk::k2b_v4_rb(K, h->NR);
+    const int tg = rk::k2b_v4_tg(K, (int)h->m, h->NR);
     const size_t smem = (size_t)tg * (2 * K * K + 2 * rb * K) * sizeof(float);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
     if (K == 16)
-      launch_pdl(rk::k2b_v4<16>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
+      launch_pdl(rk::k2b_v4<16, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
+                 h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
+                 (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+    else if (rk::k2b_v4_rpt(K, h->NR) == 8)
+      launch_pdl(rk::k2b_v4<32, 8>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
                  h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
                  (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
     else
-      launch_pdl(rk::k2b_v4<32>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
+      launch_pdl(rk::k2b_v4<32, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
                  h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
                  (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
     RK_CUDA(cudaGetLastError());

@@ -820,9 +820,18 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256, 1)
 // k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
 // block stages W32 = [R_t^T ; R_t] (fp32, written by the K2f commit) and its
 // RB rows of P_t / Q_t in shared memory with coalesced float4 loads (one
-// latency per group); thread = (2 rows, column c) then runs from shared
-// memory: every W value feeds 2 rows, P/Q reads are broadcasts.
-template <int K>
+// latency per group); thread = (RPT rows, column c) then runs from shared
+// memory: every W value feeds RPT rows, P/Q reads are broadcasts. RPT = 8 at
+// K = 32 (64-row blocks) so the 8 KB-per-slice W is staged once per 64 rows,
+// not per 16 (the 16-row version was L1/shared-memory bound on W staging).
+// The per-row arithmetic (order of every fma and add) does not depend on RPT.
+// RPT = 8 only pays while the 64-row blocks still fill two waves of the GPU
+// (n >= 2 * 148 * 64); smaller K = 32 blocks keep RPT = 2 (16-row blocks).
+inline int k2b_v4_rpt(int K, int64_t N) { return (K == 32 && N >= 2 * 148 * 64) ? 8 : 2; }
+
+inline int k2b_v4_rb(int K, int64_t N) { return k2b_v4_rpt(K, N) * (256 / K); }
+
+template <int K, int RPT>
 __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __restrict__ A64,
                                               float* __restrict__ A32,
                                               __nv_bfloat16* __restrict__ ATh,
@@ -836,15 +845,16 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
   static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
   if (ctl->stop) return;
   extern __shared__ float shf[];
-  constexpr int TR = 256 / K;      // thread rows
-  constexpr int RB = 2 * TR;       // rows per block
+  constexpr int TR = 256 / K;   // thread rows
+  constexpr int RB = RPT * TR;  // rows per block
   constexpr int K4 = K / 4;
   float* Ws = shf;                                   // [tg][2][K][K]
   float* PQs = shf + (size_t)tg * 2 * K * K;         // [tg][2][RB][K]
   const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
   const int rbase = blockIdx.x * RB;
-  const int i0 = rbase + rl, i1 = i0 + TR;
-  double n0 = 0.0, n1 = 0.0;
+  double nacc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) nacc[j] = 0.0;
   for (int tb = 0; tb < M; tb += tg) {
     const int nt = min(tg, M - tb);
     __syncthreads();
@@ -893,65 +903,63 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
     for (int u = 0; u < nt; ++u) {
       const float* WrT = Ws + (size_t)u * 2 * K * K;  // [d][c] = R_t[c][d]
       const float* Wr = WrT + K * K;                  // [d][c] = R_t[d][c]
-      const float* pr0 = PQs + ((size_t)u * 2 * RB + rl) * K;
-      const float* pr1 = pr0 + TR * K;
-      const float* qr0 = PQs + ((size_t)u * 2 * RB + RB + rl) * K;
-      const float* qr1 = qr0 + TR * K;
-      float s0 = 0.f, s1 = 0.f;
+      const float* pr = PQs + ((size_t)u * 2 * RB + rl) * K;       // row rl + j*TR at + j*TR*K
+      const float* qr = PQs + ((size_t)u * 2 * RB + RB + rl) * K;
+      float sacc[RPT];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) sacc[j] = 0.f;
 #pragma unroll
       for (int d4 = 0; d4 < K4; ++d4) {
-        const float4 a0 = *reinterpret_cast<const float4*>(pr0 + 4 * d4);
-        const float4 a1 = *reinterpret_cast<const float4*>(pr1 + 4 * d4);
-        const float4 b0 = *reinterpret_cast<const float4*>(qr0 + 4 * d4);
-        const float4 b1 = *reinterpret_cast<const float4*>(qr1 + 4 * d4);
-        const float pa[4] = {a0.x, a0.y, a0.z, a0.w}, pb[4] = {a1.x, a1.y, a1.z, a1.w};
-        const float qa[4] = {b0.x, b0.y, b0.z, b0.w}, qb[4] = {b1.x, b1.y, b1.z, b1.w};
+        float wr[4], wq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int d = d4 * 4 + q;
-          const float wr = WrT[d * K + c], wq = Wr[d * K + c];
-          s0 = fmaf(pa[q], wr, fmaf(qa[q], wq, s0));
-          s1 = fmaf(pb[q], wr, fmaf(qb[q], wq, s1));
+          wr[q] = WrT[(d4 * 4 + q) * K + c];
+          wq[q] = Wr[(d4 * 4 + q) * K + c];
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const float4 a = *reinterpret_cast<const float4*>(pr + (size_t)j * TR * K + 4 * d4);
+          const float4 b = *reinterpret_cast<const float4*>(qr + (size_t)j * TR * K + 4 * d4);
+          const float pa[4] = {a.x, a.y, a.z, a.w};
+          const float qa[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sacc[j] = fmaf(pa[q], wr[q], fmaf(qa[q], wq[q], sacc[j]));
         }
       }
-      n0 += (double)s0;
-      n1 += (double)s1;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) nacc[j] += (double)sacc[j];
     }
   }
-  double an0 = 0.0, an1 = 0.0;
-  const bool v0 = i0 < N, v1 = i1 < N;
-  if (v0) {
-    const double* Ai = A64 + (size_t)i0 * K;
-    double deno = eps_m;
-    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
-    an0 = Ai[c] * n0 / deno;
+  double an[RPT];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int i = rbase + rl + j * TR;
+    an[j] = 0.0;
+    if (i < N) {
+      const double* Ai = A64 + (size_t)i * K;
+      double deno = eps_m;
+      for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+      an[j] = Ai[c] * nacc[j] / deno;
+      if (!isfinite(an[j])) bad = true;
+    }
   }
-  if (v1) {
-    const double* Ai = A64 + (size_t)i1 * K;
-    double deno = eps_m;
-    for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
-    an1 = Ai[c] * n1 / deno;
-  }
-  if ((v0 && !isfinite(an0)) || (v1 && !isfinite(an1))) {
+  if (bad) {
     ctl->nonfinite = 1;
     ctl->stop = 1;
   }
   __syncthreads();  // the denominators above read whole rows
-  if (v0) {
-    A64[(size_t)i0 * K + c] = an0;
-    A32[(size_t)i0 * K + c] = (float)an0;
-    __nv_bfloat16 hi, lo;
-    split_bf16(an0, hi, lo);
-    ATh[(size_t)c * N + i0] = hi;
-    ATl[(size_t)c * N + i0] = lo;
-  }
-  if (v1) {
-    A64[(size_t)i1 * K + c] = an1;
-    A32[(size_t)i1 * K + c] = (float)an1;
-    __nv_bfloat16 hi, lo;
-    split_bf16(an1, hi, lo);
-    ATh[(size_t)c * N + i1] = hi;
-    ATl[(size_t)c * N + i1] = lo;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int i = rbase + rl + j * TR;
+    if (i < N) {
+      A64[(size_t)i * K + c] = an[j];
+      A32[(size_t)i * K + c] = (float)an[j];
+      __nv_bfloat16 hi, lo;
+      split_bf16(an[j], hi, lo);
+      ATh[(size_t)c * N + i] = hi;
+      ATl[(size_t)c * N + i] = lo;
+    }
   }
 }
 
@@ -1045,8 +1053,8 @@ inline int k2b_u4_tg(int K, int M) {
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (48 * 1024) / per));
 }
 
-inline int k2b_v4_tg(int K, int M) {
-  const int RB = 2 * (256 / K);
+inline int k2b_v4_tg(int K, int M, int64_t N) {
+  const int RB = k2b_v4_rb(K, N);
   const size_t per = (size_t)(2 * K * K + 2 * RB * K) * sizeof(float);
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (96 * 1024) / per));
 }
