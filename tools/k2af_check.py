@@ -17,7 +17,7 @@ n, m, k = {"cfg1": (256, 8, 4), "cfg5": (16384, 8, 16), "cfg2": (8192, 16, 16),
 eng = _lib.Engine(n, m, k, device=0)
 eng.fill_uniform(1)
 f0 = rk.random_init(n, k, m, 0)
-out = {"cfg": cfg, "k2af": os.environ.get("RK_K2AF", "0")}
+out = {"cfg": cfg, "k2af": os.environ.get("RK_K2AF", "0"), "env": {a: b for a, b in os.environ.items() if a.startswith("RK_")}}
 for track in (False, True):
     eng.set_factors(f0.A, f0.R)
     done, tr = eng.run(20, 1e-16, track)
