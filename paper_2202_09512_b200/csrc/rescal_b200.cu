@@ -319,6 +319,17 @@ void drop_graphs(rk_handle* h) {
       }
 }
 
+// Dense single-GPU K = 16: G and S_t on tensor cores (sparse.cuh sp_gram_tc,
+// TF32 3-pass, fp64 per 32 rows) instead of the SIMT cluster kernel k2a_v4.
+// RK_DENSE_GRAM_TC=0 keeps k2a_v4.
+bool dense_gram_tc(const rk_handle* h) {
+  static const bool off = [] {
+    const char* e = std::getenv("RK_DENSE_GRAM_TC");
+    return e && e[0] == '0';
+  }();
+  return !off && !h->sparse && !h->grid() && h->K == 16;
+}
+
 size_t k2f_smem(int K) {
   size_t s = (size_t)5 * K * K * sizeof(double);
   return s <= 200 * 1024 ? s : 0;
@@ -468,6 +479,14 @@ void alloc_factor_buffers(rk_handle* h) {
   h->fast = !h->grid() && (K == 16 || K == 32);
   const bool grid_fast = h->grid() && (K == 16 || K == 32);
   if (grid_fast) h->W32 = dalloc<float>((size_t)M * 2 * KK);
+  if (dense_gram_tc(h)) {
+    // tensor-core G / S_t over the reduced P (sp_gram_tc): 512-row chunks so
+    // the (m+1) x chunks items cover the GPU at cfg2-sized n
+    h->gchunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (h->rows_valid + 511) / 512));
+    h->gpart = dalloc<double>((size_t)(M + 1) * h->gchunks * KK);
+    RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rk::sp::SpGramTc::smem));
+  }
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
     h->gchunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (h->rows_valid + 2047) / 2048));
@@ -815,6 +834,15 @@ void launch_k2a(rk_handle* h, int skip) {
     else
       rk::sp::sp_gram<32><<<grid, 256, rk::sp::SpGramCfg<32>::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
+                                                                        h->red, skip);
+    RK_CUDA(cudaGetLastError());
+    h->launches += 2;
+    return;
+  }
+  if (dense_gram_tc(h) && h->gpart) {
+    rk::sp::sp_gram_tc<<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+        h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
     rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
                                                                         h->red, skip);
     RK_CUDA(cudaGetLastError());
