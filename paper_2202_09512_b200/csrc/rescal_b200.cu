@@ -955,9 +955,20 @@ void launch_k2f(rk_handle* h, int mode) {
   const int len = (int)((h->m + 1) * K * K);
   const double* rres = h->grid() ? h->red + len : h->rpart;
   const int nres = h->grid() ? 1 : h->nr;
-  launch_pdl(rk::k2f_fused, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
-             (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K,
-             (int)h->m, h->eps, mode, h->gscratch, h->counters + h->m + 1, h->W32);
+  static const bool rt_only = [] {  // RK_K2F_T=0: runtime-K kernel only (A/B)
+    const char* e = std::getenv("RK_K2F_T");
+    return e && e[0] == '0';
+  }();
+  if (!h->gscratch && !rt_only && (K == 16 || K == 32)) {
+    auto kern = K == 16 ? rk::k2f_fused_t<16> : rk::k2f_fused_t<32>;
+    launch_pdl(kern, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
+               (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, (int)h->m,
+               h->eps, mode, h->counters + h->m + 1, h->W32);
+  } else {
+    launch_pdl(rk::k2f_fused, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
+               (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K,
+               (int)h->m, h->eps, mode, h->gscratch, h->counters + h->m + 1, h->W32);
+  }
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
 }

@@ -39,6 +39,24 @@ RK_DEV void mm_kk(double* __restrict__ C, const double* __restrict__ A, bool ta,
   }
 }
 
+// C = op(A) op(B) for compile-time K (shared-memory operands); the same
+// ascending-l fma chain as mm_kk, so the results are bit-identical to it.
+template <int K>
+RK_DEV void mm_kk_t(double* __restrict__ C, const double* __restrict__ A, bool ta,
+                    const double* __restrict__ B, bool tb) {
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int i = e / K, j = e % K;
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      const double a = ta ? A[l * K + i] : A[i * K + l];
+      const double bb = tb ? B[j * K + l] : B[l * K + j];
+      s = fma(a, bb, s);
+    }
+    C[e] = s;
+  }
+}
+
 RK_DEV double block_sum(double v, double* scratch) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -149,7 +167,8 @@ __global__ void __launch_bounds__(kThreads) k2a_gs(const Ctl* __restrict__ ctl,
 // tolerance stop, non-finite check, M = sum_t M_t and the commit R <- R'.
 // mode: 0 iteration, 1 tail (trace only), 2 split update_r (no trace),
 // 3 split update_a (M from the current cores, no trace, no core change).
-__global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
+template <int KT>
+RK_DEV void k2f_body(Ctl* __restrict__ ctl,
                                                       const double* __restrict__ gs,
                                                       double* __restrict__ R,
                                                       double* __restrict__ Rnext,
@@ -160,13 +179,17 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
                                                       double* __restrict__ trace, int K, int M,
                                                       double eps, int mode, double* gscratch,
                                                       unsigned* __restrict__ counter,
-                                                      float* __restrict__ W32) {
-  pdl_entry();
-  if (ctl->stop) return;
-  extern __shared__ double sh[];
+                                                      float* __restrict__ W32, double* sh) {
+  // KT > 0: compile-time K (unrolled shared-memory products, constant index
+  // arithmetic); KT = 0: runtime K. Same arithmetic either way.
+  if (KT) K = KT;
   __shared__ double red[32];
   __shared__ bool s_last;
   __shared__ int s_stop;
+  auto mm = [&](double* C, const double* A, bool ta, const double* B, bool tb) {
+    if constexpr (KT > 0) mm_kk_t<KT>(C, A, ta, B, tb);
+    else mm_kk(C, A, ta, B, tb, K);
+  };
   const int t = blockIdx.x;
   const int KK = K * K;
   double* base = gscratch ? gscratch + (size_t)t * 5 * KK : sh;
@@ -181,9 +204,9 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
     Rt[e] = R[(size_t)t * KK + e];
   }
   __syncthreads();
-  mm_kk(T1, Rt, false, G, false, K);  // R G
+  mm(T1, Rt, false, G, false);  // R G
   __syncthreads();
-  mm_kk(T2, G, false, T1, false, K);  // G (R G)
+  mm(T2, G, false, T1, false);  // G (R G)
   __syncthreads();
   double rs = 0.0, rgrg = 0.0;
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
@@ -203,13 +226,13 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
       Rnext[(size_t)t * KK + e] = v;
     }
     __syncthreads();
-    mm_kk(T1, G, false, Rn, false, K);  // G R'
+    mm(T1, G, false, Rn, false);  // G R'
     __syncthreads();
-    mm_kk(T2, Rn, true, T1, false, K);  // R'^T G R'
+    mm(T2, Rn, true, T1, false);  // R'^T G R'
     __syncthreads();
-    mm_kk(T1, G, false, Rn, true, K);   // G R'^T
+    mm(T1, G, false, Rn, true);   // G R'^T
     __syncthreads();
-    mm_kk(Rt, Rn, false, T1, false, K);  // R' G R'^T
+    mm(Rt, Rn, false, T1, false);  // R' G R'^T
     __syncthreads();
     for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + Rt[e];
   }
@@ -299,6 +322,35 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl,
     Mout[e] = (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]))) + tail;
   }
   if (threadIdx.x == 0) ctl->iter += 1;
+}
+
+
+__global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl, const double* __restrict__ gs,
+                                                      double* __restrict__ R, double* __restrict__ Rnext,
+                                                      double* __restrict__ Mt, double* __restrict__ Mout,
+                                                      double* __restrict__ tt, const double* __restrict__ rres,
+                                                      int nres, double* __restrict__ trace, int K, int M,
+                                                      double eps, int mode, double* gscratch,
+                                                      unsigned* __restrict__ counter, float* __restrict__ W32) {
+  pdl_entry();
+  if (ctl->stop) return;
+  extern __shared__ double sh[];
+  k2f_body<0>(ctl, gs, R, Rnext, Mt, Mout, tt, rres, nres, trace, K, M, eps, mode, gscratch, counter, W32, sh);
+}
+
+// k2f_fused with compile-time K (16 or 32; shared-memory scratch only)
+template <int KT>
+__global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, const double* __restrict__ gs,
+                                                        double* __restrict__ R, double* __restrict__ Rnext,
+                                                        double* __restrict__ Mt, double* __restrict__ Mout,
+                                                        double* __restrict__ tt, const double* __restrict__ rres,
+                                                        int nres, double* __restrict__ trace, int M, double eps,
+                                                        int mode, unsigned* __restrict__ counter,
+                                                        float* __restrict__ W32) {
+  pdl_entry();
+  if (ctl->stop) return;
+  extern __shared__ double sh[];
+  k2f_body<KT>(ctl, gs, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode, nullptr, counter, W32, sh);
 }
 
 // K2b (v2): A update. Every core is staged once in shared memory as fp32
@@ -534,24 +586,6 @@ __global__ void __launch_bounds__(K == 16 ? 512 : 256, K == 16 ? 2 : 1)
 inline size_t k2a_v4_smem(int K) {
   const int warps = K == 16 ? 16 : 8;
   return (size_t)2 * warps * kBatchRows * K * sizeof(float);
-}
-
-// C = op(A) op(B) for compile-time K (shared-memory operands); the same
-// ascending-l fma chain as mm_kk, so the results are bit-identical to it.
-template <int K>
-RK_DEV void mm_kk_t(double* __restrict__ C, const double* __restrict__ A, bool ta,
-                    const double* __restrict__ B, bool tb) {
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, j = e % K;
-    double s = 0.0;
-#pragma unroll
-    for (int l = 0; l < K; ++l) {
-      const double a = ta ? A[l * K + i] : A[i * K + l];
-      const double bb = tb ? B[j * K + l] : B[l * K + j];
-      s = fma(a, bb, s);
-    }
-    C[e] = s;
-  }
 }
 
 // k2af: K2a + K2f in ONE launch for the single-GPU dense iteration (K in
