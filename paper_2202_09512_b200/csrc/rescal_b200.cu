@@ -327,7 +327,11 @@ bool dense_gram_tc(const rk_handle* h) {
     const char* e = std::getenv("RK_DENSE_GRAM_TC");
     return e && e[0] == '0';
   }();
-  return !off && !h->sparse && !h->grid() && h->K == 16;
+  static const bool off32 = [] {  // RK_DENSE_GRAM_TC32=0: K = 32 keeps k2a_v4
+    const char* e = std::getenv("RK_DENSE_GRAM_TC32");
+    return e && e[0] == '0';
+  }();
+  return !off && !h->sparse && !h->grid() && (h->K == 16 || (h->K == 32 && !off32));
 }
 
 size_t k2f_smem(int K) {
@@ -484,8 +488,10 @@ void alloc_factor_buffers(rk_handle* h) {
     // the (m+1) x chunks items cover the GPU at cfg2-sized n
     h->gchunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (h->rows_valid + 511) / 512));
     h->gpart = dalloc<double>((size_t)(M + 1) * h->gchunks * KK);
-    RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)rk::sp::SpGramTc::smem));
+    if (K == 16)
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramTc::smem));
+    else
   }
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
@@ -497,13 +503,15 @@ void alloc_factor_buffers(rk_handle* h) {
                                    (int)rk::sp::SpNumTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramCfg<16>::smem));
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpNumCfg<16>::smem));
     } else {
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramCfg<32>::smem));
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpNumCfg<32>::smem));
     }
@@ -825,7 +833,7 @@ void launch_k2a(rk_handle* h, int skip) {
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
     const int nown = h->grid() ? (int)h->piece : 0;
     if (K == 16 && (!simt_gram || h->grid()))
-      rk::sp::sp_gram_tc<<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+      rk::sp::sp_gram_tc_k<16><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
           nown);
     else if (K == 16)
@@ -841,8 +849,12 @@ void launch_k2a(rk_handle* h, int skip) {
     return;
   }
   if (dense_gram_tc(h) && h->gpart) {
-    rk::sp::sp_gram_tc<<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-        h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    if (K == 16)
+      rk::sp::sp_gram_tc_k<16><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+    else
+      rk::sp::sp_gram_tc_k<32><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
     rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
                                                                         h->red, skip);
     RK_CUDA(cudaGetLastError());

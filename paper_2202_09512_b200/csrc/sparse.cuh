@@ -304,25 +304,32 @@ struct SpGramTc {
   static constexpr size_t smem = (size_t)NS * 2 * ARR * sizeof(float);  // 48 KB (>= 8 warps x 256 doubles)
 };
 
-__global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+// KT = 32 (dense single GPU): each (slot, chunk) item is split into the four
+// 16 x 16 column quadrants of S (item-minor), each the K = 16 product above on
+// column slices of the 32-wide rows; quadrants write disjoint partial entries.
+template <int KT>
+__global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc_k(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
                                                      const float* __restrict__ P, int n, int ldp, int M, int nchunk,
                                                      double* __restrict__ part, int skip_if_stopped,
                                                      const float* __restrict__ Aown = nullptr, int nown = 0) {
   // slot 0 (G) runs over Aown's nown rows when given (a grid rank's own piece
   // of A, rescal.py:124 with the grid's rank-ascending sum, dist_rescal.py:74-92)
   using C = SpGramTc;
-  constexpr int K = 16;
+  static_assert(KT == 16 || KT == 32, "sp_gram_tc_k: K = 16 or 32");
+  constexpr int NQ1 = KT / 16, NQ = NQ1 * NQ1;
   if (skip_if_stopped && ctl->stop) return;
   extern __shared__ __align__(16) float gts[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int rows_per_chunk = (n + nchunk - 1) / nchunk;
-  const int nitems = (M + 1) * nchunk;
+  const int nitems = (M + 1) * nchunk * NQ;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int slot = item / nchunk, chunk = item - slot * nchunk;
+    const int q = item % NQ, sc = item / NQ;
+    const int slot = sc / nchunk, chunk = sc - slot * nchunk;
+    const int ca = (q / NQ1) * 16, cb = (q % NQ1) * 16;
     const bool own = slot == 0 && Aown != nullptr;
     const float* Ai = own ? Aown : A32;
-    const float* B = slot == 0 ? Ai : P + (size_t)(slot - 1) * ldp * K;
+    const float* B = slot == 0 ? Ai : P + (size_t)(slot - 1) * ldp * KT;
     const int nn = own ? nown : n;
     const int rpc = own ? (nown + nchunk - 1) / nchunk : rows_per_chunk;
     const int r0 = chunk * rpc, r1 = min(nn, r0 + rpc);
@@ -334,8 +341,8 @@ __global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc(const Ctl* __restri
       for (int e = tid; e < C::SR * 4; e += 256) {
         const int r = e >> 2, c4 = e & 3;
         if (r < nr) {
-          sp_cp16(as + r * C::LD + 4 * c4, Ai + (size_t)(base + r) * K + 4 * c4);
-          sp_cp16(bs + r * C::LD + 4 * c4, B + (size_t)(base + r) * K + 4 * c4);
+          sp_cp16(as + r * C::LD + 4 * c4, Ai + (size_t)(base + r) * KT + ca + 4 * c4);
+          sp_cp16(bs + r * C::LD + 4 * c4, B + (size_t)(base + r) * KT + cb + 4 * c4);
         } else {  // rows past the chunk contribute zero
           *reinterpret_cast<float4*>(as + r * C::LD + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<float4*>(bs + r * C::LD + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc(const Ctl* __restri
       double v = 0.0;
 #pragma unroll
       for (int w = 0; w < 8; ++w) v += red[w * 256 + tid];
-      part[((size_t)slot * nchunk + chunk) * K * K + tid] = v;
+      part[((size_t)slot * nchunk + chunk) * KT * KT + (ca + (tid >> 4)) * KT + cb + (tid & 15)] = v;
     }
   }
 }

@@ -135,7 +135,7 @@ def test_rescalk_selects_reference_k():
         np.testing.assert_allclose(e.medians, g[f"medians_k{e.k}"], atol=1e-4)
 
 
-@pytest.mark.parametrize("n,m,k,iters", [(1024, 4, 16, 20), (640, 3, 32, 15), (200, 2, 5, 30),
+@pytest.mark.parametrize("n,m,k,iters", [(1024, 4, 16, 20), (640, 3, 32, 15), (1100, 2, 27, 10), (200, 2, 5, 30),
                                          (300, 2, 40, 8), (400, 2, 130, 4)])
 def test_engines_match_oracle_midsize(n, m, k, iters):
     x = uniform_x(m, n, 7).astype(np.float64)
