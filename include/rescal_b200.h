@@ -190,6 +190,12 @@ void rk_release_cached_memory(void);
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
                    int64_t count, double* out);
 
+/* The same draws generated on `device` (the random start of rescal.py:173-183,
+ * np.random.default_rng(SeedSequence(...)).random((n, k)): one host copy of the
+ * result instead of a sequential host generator over n*k doubles). */
+int rk_pcg64_draws_on(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      uint64_t offset, int64_t count, double* out);
+
 /* Multi-GPU p_r x p_c grid (dist_rescal.py:113-161 generalised to non-square
  * grids). nccl_id is a 128-byte ncclUniqueId broadcast by the caller. The
  * handle then holds the (m, n/p_r, n/p_c) block of rank (i, j); A pieces of

@@ -69,6 +69,7 @@ SIGNATURES = {
     "rk_set_option": (ctypes.c_int, [_vp, _i32, _i64]),
     "rk_uniform_values": (ctypes.c_int, [_u64, _i64, _i64, _pf]),
     "rk_pcg64_draws": (ctypes.c_int, [_u64, _u64, _u64, _u64, _u64, _i64, _pd]),
+    "rk_pcg64_draws_on": (ctypes.c_int, [_i32, _u64, _u64, _u64, _u64, _u64, _i64, _pd]),
     "rk_coo_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "rk_coo_last_error": (ctypes.c_char_p, []),
@@ -402,6 +403,15 @@ def pcg64_draws(entropy, offset, count):
     sh, sl, ih, il = pcg64_seed_state(entropy)
     out = np.empty(count, dtype=np.float64)
     check(load().rk_pcg64_draws(sh, sl, ih, il, int(offset), int(count), _dp(out)))
+    return out
+
+
+def pcg64_random_on(device, entropy, count):
+    """np.random.default_rng(SeedSequence(entropy)).random(count), bit for bit,
+    drawn on `device` (PCG64 jump-ahead per thread) and copied back."""
+    sh, sl, ih, il = pcg64_seed_state(entropy)
+    out = np.empty(count, dtype=np.float64)
+    check(load().rk_pcg64_draws_on(int(device), sh, sl, ih, il, 0, int(count), _dp(out)))
     return out
 
 

@@ -492,6 +492,8 @@ void alloc_factor_buffers(rk_handle* h) {
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramTc::smem));
     else
+      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)rk::sp::SpGramTc::smem));
   }
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
@@ -510,8 +512,6 @@ void alloc_factor_buffers(rk_handle* h) {
     } else {
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpGramCfg<32>::smem));
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)rk::sp::SpGramTc::smem));
       RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_numer_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)rk::sp::SpNumCfg<32>::smem));
     }
@@ -2383,6 +2383,18 @@ int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64
     RK_CUDA(cudaGetLastError());
     RK_CUDA(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
     dfree(d);
+  });
+}
+
+int rk_pcg64_draws_on(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      uint64_t offset, int64_t count, double* out) {
+  return guarded([&] {
+    RK_REQUIRE(count >= 0 && (count == 0 || out), RK_ERR_DATA, "null argument");
+    RK_CUDA(cudaSetDevice(device));
+    if (count == 0) return;
+    RK_CUDA(cudaGetLastError());
+    const int rc = rk_pcg64_draws(state_hi, state_lo, inc_hi, inc_lo, offset, count, out);
+    RK_REQUIRE(rc == 0, rc, "device PCG64 draws failed");
   });
 }
 

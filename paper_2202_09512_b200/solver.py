@@ -98,10 +98,31 @@ def random_init(n: int, k: int, m: int, seed, dtype=np.float64) -> RescalFactors
     """Seeded uniform start, partition independent (rescal.py:173-183):
     A from SeedSequence((seed, 1)), R from SeedSequence((seed, 2)), drawn in
     fp64 then cast."""
-    ga = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_A)))
     gr = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_R)))
-    return RescalFactors(ga.random((n, k), dtype=np.float64).astype(dtype),
+    a = _device_uniform(seed, _SEED_TAG_A, n * k)
+    if a is None:
+        ga = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_A)))
+        a = ga.random((n, k), dtype=np.float64)
+    return RescalFactors(a.reshape(n, k).astype(dtype),
                          gr.random((m, k, k), dtype=np.float64).astype(dtype))
+
+
+# Large starts (n*k >= 2^20 doubles, e.g. 0.3 s of sequential host PCG64 at
+# n = 2^20, k = 16) are drawn on the GPU: the same PCG64 stream, each thread
+# jumping ahead to its element (rk_pcg64_draws_on), bit-identical to numpy.
+_DEVICE_DRAW_MIN = 1 << 20
+
+
+def _device_uniform(seed, tag, count):
+    if count < _DEVICE_DRAW_MIN or not isinstance(seed, (int, np.integer)):
+        return None
+    try:
+        if _lib.device_count() < 1:
+            return None
+    except Exception:  # noqa: BLE001 — no built library / no GPU visible
+        return None  # no built library / no GPU here: the host generator gives the same values
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    return _lib.pcg64_random_on(device, (int(seed), tag), count)
 
 
 def finalize_normalize(f: RescalFactors) -> RescalFactors:
