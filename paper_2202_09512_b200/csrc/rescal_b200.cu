@@ -331,7 +331,11 @@ bool dense_gram_tc(const rk_handle* h) {
     const char* e = std::getenv("RK_DENSE_GRAM_TC32");
     return e && e[0] == '0';
   }();
-  return !off && !h->sparse && !h->grid() && (h->K == 16 || (h->K == 32 && !off32));
+  static const bool offgrid = [] {  // RK_GRID_GRAM_TC=0: grid ranks keep k2a_v4
+    const char* e = std::getenv("RK_GRID_GRAM_TC");
+    return e && e[0] == '0';
+  }();
+  return !off && !h->sparse && !(h->grid() && offgrid) && (h->K == 16 || (h->K == 32 && !off32));
 }
 
 size_t k2f_smem(int K) {
@@ -849,12 +853,17 @@ void launch_k2a(rk_handle* h, int skip) {
     return;
   }
   if (dense_gram_tc(h) && h->gpart) {
+    // on a grid G runs over the rank's own piece of A (as k2a_v4's aown), S_t over its row set
+    const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
+    const int nown = h->grid() ? (int)h->piece : 0;
     if (K == 16)
       rk::sp::sp_gram_tc_k<16><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
+          nown);
     else
       rk::sp::sp_gram_tc_k<32><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
+          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
+          nown);
     rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
                                                                         h->red, skip);
     RK_CUDA(cudaGetLastError());
