@@ -10,6 +10,7 @@ touch the GPU, the first solver call does.
 from .exceptions import DataError, GridDeadlockError, GridError, NumericalError, RescalkitError
 from .containers import RelTensor, SparseRelTensor, fro_norm
 from .solver import (
+    KernelCounters,
     RescalFactors,
     SolverConfig,
     finalize_normalize,
@@ -39,8 +40,21 @@ from .selection import (
     rescalk,
     select_k,
 )
-from .multigpu import grid_shape, solve_on_grid
-from .tensor_io import load_matrix, load_tensor, save_matrix, save_tensor
+from .multigpu import (
+    BlockSource,
+    DistFactors,
+    GridContext,
+    TensorBlock,
+    block_dim,
+    dist_perturb,
+    dist_rescal_solve,
+    gather_factors,
+    grid_block,
+    grid_shape,
+    partition_block,
+    solve_on_grid,
+)
+from .tensor_io import DenseFile, load_matrix, load_tensor, save_matrix, save_tensor
 from ._lib import DeviceError, Engine
 
 __version__ = "0.1.0"

@@ -46,7 +46,6 @@ struct K1Args {
   const int* cta_slot;   // [grid] first Q slot of the CTA
   const Ctl* ctl;
   int skip_if_stopped;
-  int debug;  // experiments only: 1 = no MMA (stream X), 2 = no Q-drain wait
 };
 
 // ------------------------------- PTX helpers -------------------------------
@@ -92,6 +91,27 @@ RK_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, ui
 RK_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+
+// One lane of a converged warp (elect.sync). Issuing tcgen05.mma from an
+// elected lane of a warp-uniform loop keeps the descriptors in uniform
+// registers; issuing from an `if (lane == 0)` region instead makes ptxas wrap
+// every UTCHMMA in an ELECT / BRA.U.ANY waterfall loop (measured ~20 cycles
+// more per MMA, tools/umma_bench.cu).
+RK_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px mov.s32 %0, 1;\n"
+      "}\n"
+      : "+r"(pred));
+  return pred != 0;
+}
+
+// warp index as a value ptxas can prove warp-uniform
+RK_DEV int warp_id_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
 
 RK_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 RK_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -165,15 +185,23 @@ RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
 // ([X_hi A_hi + X_lo A_hi | X_hi A_lo]) and the epilogue adds the halves.
 // MERGE_Q does the same for Q. Halves the X_hi shared-memory reads of the
 // MMA phase (the N = 16 MMAs are smem-read bound, not tensor bound).
-template <int K>
+//
+// MMA count, not shared-memory bytes, paces the MMA phase: a kind::f16
+// M = 128, K = 16 tcgen05.mma with N <= 64 costs ~45 cycles whatever N, A
+// source (smem or TMEM) or major-ness (tools/umma_bench.cu,
+// profiles/r02_umma_bench.log). Per 128 x 128 tile: 4 MMAs per k-step with
+// both products merged (32 per tile), 5 with Q unmerged (40 per tile).
+// MQ = merge Q; at K = 32 it costs TMEM (Q accumulators 2K wide: 6 column
+// tiles per strip instead of 12, so twice the P partial traffic).
+template <int K, bool MQ>
 struct K1Cfg {
   static constexpr bool kMergeP = true;
-  static constexpr bool kMergeQ = (K == 16);
+  static constexpr bool kMergeQ = MQ;
   static constexpr int kPW = kMergeP ? 2 * K : K;  // TMEM columns per P buffer
   static constexpr int kQW = kMergeQ ? 2 * K : K;  // TMEM columns per Q accumulator
 };
 
-template <int K>
+template <int K, bool MQ>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
                  const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_rl,
@@ -184,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
   // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
   static_assert(K == 16 || K == 32, "tcgen05 path supports k_pad 16 or 32");
-  constexpr bool kMergeP = K1Cfg<K>::kMergeP, kMergeQ = K1Cfg<K>::kMergeQ;
-  constexpr int kPW = K1Cfg<K>::kPW, kQW = K1Cfg<K>::kQW;
+  constexpr bool kMergeP = K1Cfg<K, MQ>::kMergeP, kMergeQ = K1Cfg<K, MQ>::kMergeQ;
+  constexpr int kPW = K1Cfg<K, MQ>::kPW, kQW = K1Cfg<K, MQ>::kQW;
   constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
   // A operand tiles hold the boxes as [hi b0][lo b0][hi b1][lo b1] so that
   // the hi and lo rows of one 64-column K chunk are contiguous (N = 2K view)
@@ -212,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_empty = bars + 13;     // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_id_uniform();
   const int lane = threadIdx.x & 31;
   const int item_b = args.cta_begin[blockIdx.x];
   const int item_e = args.cta_begin[blockIdx.x + 1];
@@ -297,7 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    if (lane == 0) {
+    // the whole warp walks the schedule (warp-uniform); one elected lane
+    // issues each k-step's MMAs and the commits
+    {
       const uint32_t id_p = idesc_bf16(K, 0);  // A = X tile, K-major (K-dim = j)
       const uint32_t id_q = idesc_bf16(K, 1);  // A = X tile, MN-major (M = j, K-dim = i)
       const uint32_t id_p2 = idesc_bf16(2 * K, 0);  // merged [hi ; lo] B operand
@@ -313,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ts = item / nrb;
         const bool first_in_seg = item == item_b || (item - 1) / nrb != ts;
         const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
-        if (first_in_seg && seg > 0 && !(args.debug & 2)) {
+        if (first_in_seg && seg > 0) {
           mbar_wait(smem_u32(q_empty), qe_phase);  // previous segment's Q drained
           qe_phase ^= 1;
           tc_fence_after();
@@ -335,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t xh = st, xl = st + 2 * kXBox;
           const uint32_t aj = st + kStageX;
           const uint32_t q_tmem = tmem + (uint32_t)(cb * kQW);
-          if (!(args.debug & 1)) {
+          {
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
               // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
@@ -346,40 +376,45 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
               const uint64_t dah = umma_desc(aj + hoff, 16, 1024);
               const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
-              if (kMergeP) {
-                tc_mma(p_tmem, dxh, dah, id_p2, accp);  // [Xh Ah | Xh Al], N = 2K
-              } else {
-                tc_mma(p_tmem, dxh, dah, id_p, accp);
-                tc_mma(p_tmem, dxh, umma_desc(aj + loff, 16, 1024), id_p, 1u);
-              }
-              tc_mma(p_tmem, dxl, dah, id_p, 1u);  // Xl Ah into the first half
               // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
               const uint32_t roff = ks * 16 * 128;
               const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
               const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
               const uint64_t qah = umma_desc(ai + hoff, 16, 1024);
               const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
-              if (kMergeQ) {
-                tc_mma(q_tmem, qxh, qah, id_q2, accq);
-              } else {
-                tc_mma(q_tmem, qxh, qah, id_q, accq);
-                tc_mma(q_tmem, qxh, umma_desc(ai + loff, 16, 1024), id_q, 1u);
+              if (elect_one()) {
+                if (kMergeP) {
+                  tc_mma(p_tmem, dxh, dah, id_p2, accp);  // [Xh Ah | Xh Al], N = 2K
+                } else {
+                  tc_mma(p_tmem, dxh, dah, id_p, accp);
+                  tc_mma(p_tmem, dxh, umma_desc(aj + loff, 16, 1024), id_p, 1u);
+                }
+                tc_mma(p_tmem, dxl, dah, id_p, 1u);  // Xl Ah into the first half
+                if (kMergeQ) {
+                  tc_mma(q_tmem, qxh, qah, id_q2, accq);
+                } else {
+                  tc_mma(q_tmem, qxh, qah, id_q, accq);
+                  tc_mma(q_tmem, qxh, umma_desc(ai + loff, 16, 1024), id_q, 1u);
+                }
+                tc_mma(q_tmem, qxl, qah, id_q, 1u);
               }
-              tc_mma(q_tmem, qxl, qah, id_q, 1u);
+              __syncwarp();
             }
           }
-          tc_commit(smem_u32(&empty[stage]));
+          if (elect_one()) tc_commit(smem_u32(&empty[stage]));
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(smem_u32(&p_full[pb]));
-        tc_commit(smem_u32(&ai_empty[ab]));
-        if (last_in_seg) {
-          tc_commit(smem_u32(q_full));
-          ++seg;
+        if (elect_one()) {
+          tc_commit(smem_u32(&p_full[pb]));
+          tc_commit(smem_u32(&ai_empty[ab]));
+          if (last_in_seg) tc_commit(smem_u32(q_full));
         }
+        __syncwarp();
+        if (last_in_seg) ++seg;
       }
     }
   } else {
@@ -459,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int K>
-constexpr uint32_t k1_smem_bytes() {
+constexpr uint32_t k1_smem_bytes() {  // same for both MQ variants
   return 1024 /*align slack*/ + kStages * (4 * kXBox + 4 * K * 128) + 2 * (4 * K * 128) + 256;
 }
 

@@ -251,10 +251,11 @@ __global__ void __launch_bounds__(kThreads) apply_peer(Ctl* __restrict__ ctl, co
       double deno = eps_m;
       for (int dd = 0; dd < K; ++dd) deno = fma(Ai[dd], Mm[dd * K + c], deno);
       anew = Ai[c] * (sI + sJ) / deno;
-      if (!isfinite(anew)) {
-        ctl->nonfinite = 1;
-        ctl->stop = 1;
-      }
+      // no stop here: only this rank would see it and its peers would wait
+      // for its next exchange. The value travels to every peer with the
+      // piece, turns the next replicated core update non-finite on ALL
+      // ranks, and there every rank stops at the same iteration.
+      if (!isfinite(anew)) ctl->nonfinite = 1;
     }
     for (int jj = 0; jj < a.pc; ++jj)
       reinterpret_cast<double*>(a.base[a.gi * a.pc + jj] + a.off_rxAr)[(((size_t)par * a.pc + a.gj) * a.b + i) * K + c] = anew;

@@ -32,6 +32,7 @@
 
 #include "../../include/rescal_b200.h"
 #include "k1_tc.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "peer.cuh"
 #include "rk_kernels.cuh"
 #include "sparse.cuh"
@@ -238,7 +239,6 @@ struct rk_handle {
   int nb = 1;               // K2a row chunks
   int chunk_rows = 64;
   unsigned* counters = nullptr;  // last-block tickets (self-resetting)
-  int k1_debug = 0;              // K1 experiment switches (bench/profiling only)
   bool skip_comm = false;        // experiments only: skip the per-iteration NCCL calls
   bool fast = false;             // single GPU, K in {16, 32}: k2a_v4 / k2b_v4 path
   float* W32 = nullptr;          // [M][2][K][K] fp32 (R_t^T ; R_t) for k2b_v4
@@ -260,6 +260,7 @@ struct rk_handle {
   int nnp = 0;
   // tcgen05 schedule
   int c = 0, nstrips = 0, grid_tc = 0, nslots = 0;
+  bool k1_mq = true;  // K1 merges the Q hi/lo operands (always at K = 16; see k1_merge_q)
   size_t smem_tc = 0;
   float *Ppart = nullptr, *Qpart = nullptr;
   int *d_cta_begin = nullptr, *d_cta_slot = nullptr, *d_slot_first = nullptr,
@@ -319,24 +320,11 @@ void drop_graphs(rk_handle* h) {
       }
 }
 
-// Dense single-GPU K = 16: G and S_t on tensor cores (sparse.cuh sp_gram_tc,
-// TF32 3-pass, fp64 per 32 rows) instead of the SIMT cluster kernel k2a_v4.
-// RK_DENSE_GRAM_TC=0 keeps k2a_v4.
-bool dense_gram_tc(const rk_handle* h) {
-  static const bool off = [] {
-    const char* e = std::getenv("RK_DENSE_GRAM_TC");
-    return e && e[0] == '0';
-  }();
-  static const bool off32 = [] {  // RK_DENSE_GRAM_TC32=0: K = 32 keeps k2a_v4
-    const char* e = std::getenv("RK_DENSE_GRAM_TC32");
-    return e && e[0] == '0';
-  }();
-  static const bool offgrid = [] {  // RK_GRID_GRAM_TC=0: grid ranks keep k2a_v4
-    const char* e = std::getenv("RK_GRID_GRAM_TC");
-    return e && e[0] == '0';
-  }();
-  return !off && !h->sparse && !(h->grid() && offgrid) && (h->K == 16 || (h->K == 32 && !off32));
-}
+// Dense K in {16, 32} (one GPU or a grid rank): G and S_t on tensor cores
+// (sparse.cuh sp_gram_tc_k, TF32 3-pass, fp64 per 32 rows) over the reduced
+// P instead of the SIMT cluster kernel k2a_v4 (cfg2 K2a 27 -> 16 us, cfg3
+// 197 -> 110 us).
+bool dense_gram_tc(const rk_handle* h) { return !h->sparse && (h->K == 16 || h->K == 32); }
 
 size_t k2f_smem(int K) {
   size_t s = (size_t)5 * K * K * sizeof(double);
@@ -375,12 +363,26 @@ void free_factor_buffers(rk_handle* h) {
   h->d_cta_begin = h->d_cta_slot = h->d_slot_first = h->d_slot_count = nullptr;
 }
 
+// K = 32: merge Q's hi/lo operands (4 MMAs per k-step instead of 5) only when
+// that does not add column strips: merged Q accumulators are 2K wide, so a
+// strip holds 6 column tiles instead of 12, and every extra strip is one more
+// copy of P written by K1 and read by k1_reduce. At cfg3 (256 column tiles)
+// merging measured 79.8 vs 81.2 it/s (same K1 time: the MMA issue is no
+// longer the bound once it runs warp-uniform; profiles/r02k1_*.json).
+bool k1_merge_q(int K, int64_t NC) {
+  if (K == 16) return true;
+  const int64_t ncb = NC / 128;
+  return (ncb + 5) / 6 == (ncb + 11) / 12;
+}
+
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
 void plan_tc(rk_handle* h) {
   const int K = h->K;
   const int nrb = (int)(h->NR / 128), ncb = (int)(h->NC / 128);
-  const int pw = K == 16 ? rk::tc::K1Cfg<16>::kPW : rk::tc::K1Cfg<32>::kPW;
-  const int qw = K == 16 ? rk::tc::K1Cfg<16>::kQW : rk::tc::K1Cfg<32>::kQW;
+  h->k1_mq = k1_merge_q(K, h->NC);
+  const int pw = K == 16 ? rk::tc::K1Cfg<16, true>::kPW : rk::tc::K1Cfg<32, true>::kPW;
+  const int qw = K == 16 ? rk::tc::K1Cfg<16, true>::kQW
+                         : (h->k1_mq ? rk::tc::K1Cfg<32, true>::kQW : rk::tc::K1Cfg<32, false>::kQW);
   const int cmax = (512 - 2 * pw) / qw;  // TMEM columns: c Q accumulators + 2 P buffers
   int c = std::min(cmax, ncb);
   int nstrips = (ncb + c - 1) / c;
@@ -444,10 +446,13 @@ void plan_tc(rk_handle* h) {
   h->maps[5] = make_map(h->ATl_col, h->NC, K, K);
   h->smem_tc = K == 16 ? rk::tc::k1_smem_bytes<16>() : rk::tc::k1_smem_bytes<32>();
   if (K == 16)
-    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)h->smem_tc));
+  else if (h->k1_mq)
+    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)h->smem_tc));
   else
-    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)h->smem_tc));
 }
 
@@ -561,10 +566,6 @@ void alloc_factor_buffers(rk_handle* h) {
   RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
   const size_t k5s = (size_t)(2 * 64 * (K + 1) + (K <= 128 ? K * K : 0)) * sizeof(float);
   RK_CUDA(cudaFuncSetAttribute(rk::k5_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5s));
-  if (K == 16)
-    RK_CUDA(cudaFuncSetAttribute(rk::k2af<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rk::k2af_smem(16)));
-  if (K == 32)
-    RK_CUDA(cudaFuncSetAttribute(rk::k2af<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rk::k2af_smem(32)));
   if (k2f_smem(K))
     RK_CUDA(cudaFuncSetAttribute(rk::k2f_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
   if (rk::k2b_fused_smem(K, (int)M) <= 200 * 1024)
@@ -786,13 +787,10 @@ void launch_k1(rk_handle* h, bool timed) {
     a.cta_slot = h->d_cta_slot;
     a.ctl = h->ctl;
     a.skip_if_stopped = 1;
-    a.debug = h->k1_debug;
-    if (K == 16)
-      launch_pdl(rk::tc::k1_tc_kernel<16>, dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0],
-                 h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
-    else
-      launch_pdl(rk::tc::k1_tc_kernel<32>, dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0],
-                 h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
+    auto kern = K == 16 ? rk::tc::k1_tc_kernel<16, true>
+                        : (h->k1_mq ? rk::tc::k1_tc_kernel<32, true> : rk::tc::k1_tc_kernel<32, false>);
+    launch_pdl(kern, dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0], h->maps[1], h->maps[2],
+               h->maps[3], h->maps[4], h->maps[5], a);
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
@@ -833,10 +831,9 @@ void launch_k2a(rk_handle* h, int skip) {
     // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram);
     // on a grid G runs over the rank's own piece of A, S_t over its row set
     const int grid = h->num_sms * 2;
-    static const bool simt_gram = std::getenv("RK_SP_GRAM_SIMT") != nullptr;  // experiments only
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
     const int nown = h->grid() ? (int)h->piece : 0;
-    if (K == 16 && (!simt_gram || h->grid()))
+    if (K == 16)
       rk::sp::sp_gram_tc_k<16><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
           nown);
@@ -874,11 +871,7 @@ void launch_k2a(rk_handle* h, int skip) {
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : h->A32row;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
     // P/Q already reduced (k1_reduce / SIMT K1 / sparse CSR pass)
-    static const int env_cluster = [] {
-      const char* e = std::getenv("RK_K2A_CLUSTER");  // experiments only
-      return e ? std::atoi(e) : 0;
-    }();
-    const int ncta = env_cluster ? env_cluster : 8;
+    const int ncta = 8;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncta, (unsigned)(h->m + 1));
     cfg.blockDim = dim3(K == 16 ? 512 : 256);
@@ -911,46 +904,6 @@ void launch_k2a(rk_handle* h, int skip) {
   h->launches += 1;
 }
 
-// K2a + K2f fused (single GPU, dense, K in {16, 32}) behind RK_K2AF=1:
-// bit-identical to the two-kernel path but measured 0.3-2 % slower (every
-// cluster also forms G; the per-slice chain, not the launch, is the cost),
-// so the two-kernel path stays the default (tools/k2af_check.py).
-bool use_k2af(const rk_handle* h) {
-  static const bool on = [] {
-    const char* e = std::getenv("RK_K2AF");
-    return e && e[0] == '1';
-  }();
-  return on && h->fast && !h->sparse && !h->grid() && (h->K == 16 || h->K == 32);
-}
-
-void launch_k2af(rk_handle* h) {
-  const int K = h->K;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(rk::kCluster, (unsigned)h->m);
-  cfg.blockDim = dim3(K == 16 ? 512 : 256);
-  cfg.dynamicSmemBytes = rk::k2af_smem(K);
-  cfg.stream = h->stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = rk::kCluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_on() ? 2 : 1;
-  unsigned* counter = h->counters + h->m + 1;
-  if (K == 16)
-    RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2af<16>, h->ctl, (const float*)h->A32row, (const float*)h->P, (int)h->NR,
-                               (int)h->m, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, (const double*)h->rpart,
-                               h->nr, h->trace_dev, h->eps, counter, h->W32));
-  else
-    RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2af<32>, h->ctl, (const float*)h->A32row, (const float*)h->P, (int)h->NR,
-                               (int)h->m, h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, (const double*)h->rpart,
-                               h->nr, h->trace_dev, h->eps, counter, h->W32));
-  h->launches += 1;
-}
-
 // On a grid: append the direct-residual scalar to the reduced [G, S_t] and
 // all-reduce over the world communicator (the only fp64 all-reduce of the
 // iteration; it returns identical bytes on every rank, so R stays replicated).
@@ -976,11 +929,7 @@ void launch_k2f(rk_handle* h, int mode) {
   const int len = (int)((h->m + 1) * K * K);
   const double* rres = h->grid() ? h->red + len : h->rpart;
   const int nres = h->grid() ? 1 : h->nr;
-  static const bool rt_only = [] {  // RK_K2F_T=0: runtime-K kernel only (A/B)
-    const char* e = std::getenv("RK_K2F_T");
-    return e && e[0] == '0';
-  }();
-  if (!h->gscratch && !rt_only && (K == 16 || K == 32)) {
+  if (!h->gscratch && (K == 16 || K == 32)) {
     auto kern = K == 16 ? rk::k2f_fused_t<16> : rk::k2f_fused_t<32>;
     launch_pdl(kern, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
                (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, (int)h->m,
@@ -1031,18 +980,11 @@ void launch_k2b(rk_handle* h) {
     if (K == 16) {
       rk::sp::sp_csr_pass<16><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
                                                           h->Q, (int)h->cols_valid, (int)h->NC, (int)h->m, 1);
-      static const bool simt_numer = std::getenv("RK_SP_NUMER_SIMT") != nullptr;  // experiments only
-      if (simt_numer) {
-        rk::sp::sp_numer_apply<16><<<nb, 256, rk::sp::SpNumCfg<16>::smem, h->stream>>>(
-            h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->W32, h->Mm, (int)h->n, (int)h->m,
-            eps_m);
-      } else {
-        rk::sp::sp_wfrag<<<(unsigned)h->m, 256, 0, h->stream>>>(h->ctl, h->W32, h->wfrag, (int)h->m);
-        rk::sp::sp_numer_tc<<<(unsigned)h->num_sms * 2, 256, rk::sp::SpNumTc::smem, h->stream>>>(
-            h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->wfrag, h->Mm, (int)h->n,
-            (int)h->m, eps_m);
-        h->launches += 1;
-      }
+      rk::sp::sp_wfrag<<<(unsigned)h->m, 256, 0, h->stream>>>(h->ctl, h->W32, h->wfrag, (int)h->m);
+      rk::sp::sp_numer_tc<<<(unsigned)h->num_sms * 2, 256, rk::sp::SpNumTc::smem, h->stream>>>(
+          h->ctl, h->Arow, h->A32row, h->P, h->Q, (int)h->NR, (int)h->NC, h->wfrag, h->Mm, (int)h->n,
+          (int)h->m, eps_m);
+      h->launches += 1;
     } else {
       rk::sp::sp_csr_pass<32><<<grid, 256, 0, h->stream>>>(h->ctl, h->csc_ptr, h->csc_idx, h->csc_val, h->A32row,
                                                           h->Q, (int)h->cols_valid, (int)h->NC, (int)h->m, 1);
@@ -1216,25 +1158,48 @@ void phase_mark(rk_handle* h, bool timed, int idx) {
   RK_CUDA(cudaEventRecord(h->ev_ph[i], h->stream));
 }
 
+// NVTX ranges with the reference's phase names (grid.py:97-111 counted_mm
+// phases, perf.py:32-33) around the host enqueue of each phase; emitted only
+// in profile mode (per-phase events, no graph replay), so a timeline tool
+// shows matrix_mul / gram_mul / row_reduce ... next to the kernels.
+struct NvtxPhase {
+  bool on;
+  NvtxPhase(bool enable, const char* name) : on(enable) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxPhase() {
+    if (on) nvtxRangePop();
+  }
+};
+
 // phases: 0 K1(+reduce) | 1 K5+K2a | 2 grid all-reduce | 3 K2f | 4 K2b/numerator (+RS) | 5 A update/gather
 void enqueue_iteration(rk_handle* h, bool timed, bool with_k5) {
   phase_mark(h, timed, 0);
-  launch_k1(h, timed);
+  {
+    NvtxPhase r(timed, h->sparse ? "matrix_mul_sparse" : "matrix_mul");
+    launch_k1(h, timed);
+  }
   phase_mark(h, timed, 1);
-  if (with_k5) launch_k5(h, 1);
-  if (use_k2af(h)) {
-    launch_k2af(h);
-    phase_mark(h, timed, 2);
-    phase_mark(h, timed, 3);
-  } else {
+  {
+    NvtxPhase r(timed, "gram_mul");
+    if (with_k5) launch_k5(h, 1);
     launch_k2a(h, 1);
-    phase_mark(h, timed, 2);
-    if (h->grid()) grid_allreduce_parts(h, true);
-    phase_mark(h, timed, 3);
+  }
+  phase_mark(h, timed, 2);
+  if (h->grid()) {
+    NvtxPhase r(timed, "column_reduce");
+    grid_allreduce_parts(h, true);
+  }
+  phase_mark(h, timed, 3);
+  {
+    NvtxPhase r(timed, "matrix_mul");
     launch_k2f(h, 0);
   }
   phase_mark(h, timed, 4);
-  launch_k2b(h);
+  {
+    NvtxPhase r(timed, h->grid() ? "row_reduce" : "matrix_mul");
+    launch_k2b(h);
+  }
   phase_mark(h, timed, 6);
   if (timed) h->ph_iters += 1;
 }
@@ -1948,7 +1913,6 @@ int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     if (key == 1) h->profile = value != 0;
-    else if (key == 3) h->k1_debug = (int)value;
     else if (key == 4) h->skip_comm = value != 0;
     else if (key == 2) {
       h->use_graph = value != 0;
@@ -2382,31 +2346,43 @@ int rk_restore(rk_handle* h) {
   });
 }
 
+namespace {
+// device buffer freed on every exit path (a throwing launch or copy included)
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { dfree(p); }
+};
+
+void pcg64_draws_body(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
+                      int64_t count, double* out) {
+  RK_REQUIRE(count >= 0 && (count == 0 || out), RK_ERR_DATA, "null argument");
+  if (count == 0) return;
+  DevBuf d;
+  d.p = dalloc<double>((size_t)count);
+  rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
+  const int64_t threads = (count + 63) / 64;
+  rk::pcg64_draws<<<(unsigned)((threads + 255) / 256), 256>>>(st, inc, offset, count, static_cast<double*>(d.p));
+  RK_CUDA(cudaGetLastError());
+  RK_CUDA(cudaMemcpy(out, d.p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                    uint64_t offset, int64_t count, double* out) {
-  return guarded([&] {
-    double* d = dalloc<double>((size_t)count);
-    rk::u128 st{state_lo, state_hi}, inc{inc_lo, inc_hi};
-    const int64_t threads = (count + 63) / 64;
-    rk::pcg64_draws<<<(unsigned)((threads + 255) / 256), 256>>>(st, inc, offset, count, d);
-    RK_CUDA(cudaGetLastError());
-    RK_CUDA(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
-    dfree(d);
-  });
+  return guarded([&] { pcg64_draws_body(state_hi, state_lo, inc_hi, inc_lo, offset, count, out); });
 }
-
 int rk_pcg64_draws_on(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                       uint64_t offset, int64_t count, double* out) {
-  return guarded([&] {
-    RK_REQUIRE(count >= 0 && (count == 0 || out), RK_ERR_DATA, "null argument");
+  // runs on `device` and leaves the calling thread's current device as it was
+  int prev = -1;
+  cudaGetDevice(&prev);
+  const int rc = guarded([&] {
     RK_CUDA(cudaSetDevice(device));
-    if (count == 0) return;
-    RK_CUDA(cudaGetLastError());
-    const int rc = rk_pcg64_draws(state_hi, state_lo, inc_hi, inc_lo, offset, count, out);
-    RK_REQUIRE(rc == 0, rc, "device PCG64 draws failed");
+    pcg64_draws_body(state_hi, state_lo, inc_hi, inc_lo, offset, count, out);
   });
+  if (prev >= 0) cudaSetDevice(prev);
+  return rc;
 }
-
 int rk_perturb_values(int32_t device, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                       double delta, int32_t dtype, void* values, int64_t count, uint64_t e0, int32_t field_only) {
   return guarded([&] {

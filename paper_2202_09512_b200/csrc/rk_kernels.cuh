@@ -588,269 +588,6 @@ inline size_t k2a_v4_smem(int K) {
   return (size_t)2 * warps * kBatchRows * K * sizeof(float);
 }
 
-// k2af: K2a + K2f in ONE launch for the single-GPU dense iteration (K in
-// {16, 32}). Cluster t (kCluster CTAs) forms S_t = A^T P_t exactly as
-// k2a_v4's slot 1+t AND G = A^T A exactly as its slot 0 (same row
-// partition, batch order and reduction order, from the A rows the cluster
-// stages anyway), so every cluster holds bit-identical G and the results
-// equal the two-kernel path bit for bit. CTA 0 of the cluster then runs
-// k2f_fused's per-slice core update for slice t from shared memory, and the
-// last CTA 0 to finish (atomic ticket) runs k2f_fused's trace / stop /
-// commit. Saves the k2f launch, the G/S round trip through global memory
-// and the separate G cluster.
-inline size_t k2af_smem(int K) {
-  const size_t stage = k2a_v4_smem(K), scratch = (size_t)5 * K * K * sizeof(double);
-  return (stage > scratch ? stage : scratch) + (size_t)3 * K * K * sizeof(double);
-}
-
-template <int K>
-__global__ void __launch_bounds__(K == 16 ? 512 : 256, 1)
-    k2af(Ctl* __restrict__ ctl, const float* __restrict__ A32, const float* __restrict__ P, int N, int M,
-         double* __restrict__ gs, double* __restrict__ R, double* __restrict__ Rnext, double* __restrict__ Mt,
-         double* __restrict__ Mout, double* __restrict__ tt, const double* __restrict__ rres, int nres,
-         double* __restrict__ trace, double eps, unsigned* __restrict__ counter, float* __restrict__ W32) {
-  static_assert(K == 16 || K == 32, "k2af: K in {16, 32}");
-  pdl_entry();
-  if (ctl->stop) return;
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  constexpr int KK = K * K;
-  constexpr int K4 = K / 4;
-  constexpr int E = KK / 32;
-  constexpr int kWarps = K == 16 ? 16 : 8;
-  constexpr int BR = kBatchRows;
-  constexpr int NI = (BR * K4 + 31) / 32;
-  extern __shared__ __align__(16) float dynf[];
-  // floats of the staging area = max(k2a_v4 staging, k2f scratch of 5 KxK doubles)
-  constexpr int stage_f = (2 * kWarps * BR * K > 10 * KK) ? 2 * kWarps * BR * K : 10 * KK;
-  float (*pst)[BR][K] = reinterpret_cast<float (*)[BR][K]>(dynf);
-  float (*ast)[BR][K] = reinterpret_cast<float (*)[BR][K]>(dynf + kWarps * BR * K);
-  double* bS = reinterpret_cast<double*>(dynf + stage_f);  // CTA partial of S_t
-  double* bG = bS + KK;                                     // CTA partial of G
-  double* Sred = bG + KK;                                   // CTA 0: reduced S_t
-  __shared__ double red[32];
-  __shared__ bool s_last;
-  __shared__ int s_stop;
-  const int ncta = gridDim.x;
-  const int rank = blockIdx.x;
-  const int t = blockIdx.y;
-  const float* B = P + (size_t)t * N * K;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int RB = (((N + ncta - 1) / ncta) + BR * kWarps - 1) / (BR * kWarps) * (BR * kWarps);
-  const int WR = RB / kWarps;
-  const int r_begin = rank * RB + warp * WR;
-  const int r_end = min(N, r_begin + WR);
-  const int c = (lane * E) / K;
-  const int d0 = (lane * E) - c * K;
-  double accS[E], accG[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) accS[q] = accG[q] = 0.0;
-  float4 pa[NI], pb[NI];
-  auto fetch = [&](int b0) {
-    const int nrow = min(BR, r_end - b0);
-#pragma unroll
-    for (int u = 0; u < NI; ++u) {
-      const int item = lane + 32 * u;
-      const int r8 = item / K4, q = item - r8 * K4;
-      const bool ok = item < BR * K4 && r8 < nrow;
-      pa[u] = ok ? __ldg(reinterpret_cast<const float4*>(A32 + (size_t)(b0 + r8) * K) + q)
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-      pb[u] = ok ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(b0 + r8) * K) + q)
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  if (r_begin < r_end) fetch(r_begin);
-  for (int b0 = r_begin; b0 < r_end; b0 += BR) {
-    const int nrow = min(BR, r_end - b0);
-#pragma unroll
-    for (int u = 0; u < NI; ++u) {
-      const int item = lane + 32 * u;
-      if (item < BR * K4) {
-        const int r8 = item / K4, q = item - r8 * K4;
-        *reinterpret_cast<float4*>(&ast[warp][r8][q * 4]) = pa[u];
-        *reinterpret_cast<float4*>(&pst[warp][r8][q * 4]) = pb[u];
-      }
-    }
-    __syncwarp();
-    if (b0 + BR < r_end) fetch(b0 + BR);
-    float ps[E], pg[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) ps[q] = pg[q] = 0.f;
-    for (int r8 = 0; r8 < nrow; ++r8) {
-      const float a = ast[warp][r8][c];
-#pragma unroll
-      for (int q = 0; q < E; q += 4) {
-        const float4 p4 = *reinterpret_cast<const float4*>(&pst[warp][r8][d0 + q]);
-        const float4 a4 = *reinterpret_cast<const float4*>(&ast[warp][r8][d0 + q]);
-        ps[q] = fmaf(a, p4.x, ps[q]);
-        ps[q + 1] = fmaf(a, p4.y, ps[q + 1]);
-        ps[q + 2] = fmaf(a, p4.z, ps[q + 2]);
-        ps[q + 3] = fmaf(a, p4.w, ps[q + 3]);
-        pg[q] = fmaf(a, a4.x, pg[q]);
-        pg[q + 1] = fmaf(a, a4.y, pg[q + 1]);
-        pg[q + 2] = fmaf(a, a4.z, pg[q + 2]);
-        pg[q + 3] = fmaf(a, a4.w, pg[q + 3]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      accS[q] += (double)ps[q];
-      accG[q] += (double)pg[q];
-    }
-    __syncwarp();
-  }
-  for (int w = 0; w < kWarps; ++w) {
-    if (warp == w) {
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        double* p = &bS[lane * E + q];
-        *p = (w == 0 ? 0.0 : *p) + accS[q];
-        double* g = &bG[lane * E + q];
-        *g = (w == 0 ? 0.0 : *g) + accG[q];
-      }
-    }
-    __syncthreads();
-  }
-  cluster.sync();
-  // CTA 0: cluster sums in CTA order (k2a_v4's order) -> G into the scratch
-  // head, S_t into Sred; the staging area becomes k2f's scratch
-  double* G = reinterpret_cast<double*>(dynf);
-  double* Rt = G + KK;
-  double* T1 = G + 2 * KK;
-  double* T2 = G + 3 * KK;
-  double* Rn = G + 4 * KK;
-  if (rank == 0) {
-    for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-      double vs = 0.0, vg = 0.0;
-      for (int r = 0; r < ncta; ++r) {
-        vs += cluster.map_shared_rank(bS, r)[e];
-        vg += cluster.map_shared_rank(bG, r)[e];
-      }
-      Sred[e] = vs;
-      G[e] = vg;
-      gs[(size_t)(1 + t) * KK + e] = vs;
-      if (t == 0) gs[e] = vg;
-      Rt[e] = R[(size_t)t * KK + e];
-    }
-  }
-  cluster.sync();
-  if (rank != 0) return;
-  // ---- k2f_fused, per-slice part (mode 0) ----
-  const double* S = Sred;
-  mm_kk_t<K>(T1, Rt, false, G, false);  // R G
-  __syncthreads();
-  mm_kk_t<K>(T2, G, false, T1, false);  // G (R G)
-  __syncthreads();
-  double rs = 0.0, rgrg = 0.0;
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    rs += Rt[e] * S[e];
-    rgrg += Rt[e] * T2[e];
-  }
-  rs = block_sum(rs, red);
-  rgrg = block_sum(rgrg, red);
-  if (threadIdx.x == 0) {
-    tt[2 * t] = rs;
-    tt[2 * t + 1] = rgrg;
-  }
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    const double v = Rt[e] * S[e] / (T2[e] + eps);
-    Rn[e] = v;
-    Rnext[(size_t)t * KK + e] = v;
-  }
-  __syncthreads();
-  mm_kk_t<K>(T1, G, false, Rn, false);  // G R'
-  __syncthreads();
-  mm_kk_t<K>(T2, Rn, true, T1, false);  // R'^T G R'
-  __syncthreads();
-  mm_kk_t<K>(T1, G, false, Rn, true);   // G R'^T
-  __syncthreads();
-  mm_kk_t<K>(Rt, Rn, false, T1, false);  // R' G R'^T
-  __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + Rt[e];
-  // ---- last CTA 0: trace / stop / commit (k2f_fused, mode 0) ----
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == (unsigned)(M - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (threadIdx.x == 0) {
-    s_stop = 0;
-    *counter = 0u;
-  }
-  __syncthreads();
-  if (ctl->track && ctl->iter >= 1) {
-    double res;
-    if (ctl->direct) {
-      double acc = 0.0;
-      for (int i = threadIdx.x; i < nres; i += blockDim.x) acc += __ldcg(rres + i);
-      res = block_sum(acc, red);
-    } else {
-      double acc = 0.0;
-      for (int q = threadIdx.x; q < M; q += blockDim.x) acc += -2.0 * __ldcg(tt + 2 * q) + __ldcg(tt + 2 * q + 1);
-      res = ctl->norm2_dev + block_sum(acc, red);
-    }
-    if (threadIdx.x == 0) {
-      double err = sqrt(fmax(res, 0.0) / ctl->norm2);
-      trace[ctl->trace_len] = err;
-      ctl->trace_len += 1;
-      ctl->last_err = err;
-      if (!isfinite(err)) {
-        ctl->nonfinite = 2;
-        s_stop = 1;
-      } else if (ctl->tol >= 0.0 && err < ctl->tol) {
-        s_stop = 1;
-      } else if (!ctl->direct && err < ctl->direct_thresh) {
-        ctl->direct = 1;
-      }
-    }
-    __syncthreads();
-  }
-  if (s_stop) {
-    if (threadIdx.x == 0) ctl->stop = 1;
-    return;
-  }
-  int bad = 0;
-  for (int e0 = threadIdx.x; e0 < M * KK; e0 += 4 * blockDim.x) {
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * blockDim.x;
-      v[u] = e < M * KK ? __ldcg(Rnext + e) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e >= M * KK) break;
-      if (!isfinite(v[u])) bad = 1;
-      R[e] = v[u];
-      const int q = e / KK, rem = e - q * KK, a = rem / K, b = rem - a * K;
-      W32[(size_t)q * 2 * KK + b * K + a] = (float)v[u];       // R_t^T
-      W32[(size_t)q * 2 * KK + KK + a * K + b] = (float)v[u];  // R_t
-    }
-  }
-  bad = __syncthreads_or(bad);
-  if (bad) {
-    if (threadIdx.x == 0) {
-      ctl->nonfinite = 1;
-      ctl->stop = 1;
-    }
-    return;
-  }
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int q = 0;
-    for (; q + 8 <= M; q += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s8[u] += __ldcg(Mt + (size_t)(q + u) * KK + e);
-    }
-    double tail = 0.0;
-    for (; q < M; ++q) tail += __ldcg(Mt + (size_t)q * KK + e);
-    Mout[e] = (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]))) + tail;
-  }
-  if (threadIdx.x == 0) ctl->iter += 1;
-}
-
 // k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
 // block stages W32 = [R_t^T ; R_t] (fp32, written by the K2f commit) and its
 // RB rows of P_t / Q_t in shared memory with coalesced float4 loads (one
@@ -1241,10 +978,9 @@ __global__ void __launch_bounds__(kThreads) k2b_apply_own(Ctl* __restrict__ ctl,
     for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
     const double num = numI[(size_t)i * K + c] + numJ[(size_t)i * K + c];
     anew = Ai[c] * num / deno;
-    if (!isfinite(anew)) {
-      ctl->nonfinite = 1;
-      ctl->stop = 1;
-    }
+    // grid: flag only; the all-gathered piece makes the next replicated core
+    // update non-finite on every rank, which then all stop together
+    if (!isfinite(anew)) ctl->nonfinite = 1;
   }
   __syncthreads();
   if (active) Aown[(size_t)i * K + c] = anew;

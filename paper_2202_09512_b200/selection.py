@@ -28,12 +28,13 @@ import numpy as np
 from scipy.optimize import linear_sum_assignment
 
 from . import _lib
-from .containers import dense_slices, tensor_dtype
+from .containers import dense_slices, is_sparse, tensor_dtype
 from .exceptions import DataError, RescalkitError
 from .solver import RescalFactors, SolverConfig, finalize_normalize, random_init, rescal_solve
 
 _SEED_TAG_PERTURB = 3
 _SEED_TAG_ENSEMBLE = 4
+_DENSIFY_MAX = 1 << 28  # elements: a sparse tensor this small may run on the dense engine (k > 32)
 
 
 @dataclass
@@ -48,13 +49,18 @@ class PerturbConfig:
             raise DataError(f"delta must be > 0, got {self.delta}")
 
 
+def _perturb_entropy(pcfg: PerturbConfig, q):
+    """SeedSequence entropy of perturbation q (dist_rescal.py:167-168)."""
+    return (pcfg.base_seed, _SEED_TAG_PERTURB, q)
+
+
 def perturbation_field(n: int, m: int, pcfg: PerturbConfig, q, dtype=np.float64, device: int = 0) -> np.ndarray:
     """The full (m, n, n) multiplier field for perturbation q
     (dist_rescal.py:164-171), drawn on the device, bit-exact with numpy."""
     out = np.empty((m, n, n), dtype=np.dtype(dtype))
     if out.dtype not in (np.float32, np.float64):
         raise DataError(f"unsupported field dtype {out.dtype}")
-    _lib.perturb_values((pcfg.base_seed, _SEED_TAG_PERTURB, q), pcfg.delta, out, 0, True, device)
+    _lib.perturb_values(_perturb_entropy(pcfg, q), pcfg.delta, out, 0, True, device)
     return out
 
 
@@ -66,7 +72,7 @@ def perturb(x, pcfg: PerturbConfig, q, device: int = 0):
     from .containers import RelTensor, SparseRelTensor, is_sparse
     import scipy.sparse as sps
 
-    key = (pcfg.base_seed, _SEED_TAG_PERTURB, q)
+    key = _perturb_entropy(pcfg, q)
     if is_sparse(x):
         slices = []
         for t, s in enumerate(x.slices):
@@ -305,10 +311,21 @@ def rescalk(x, k_min: int, k_max: int, r: int, cfg: SolverConfig | None = None,
     rank, size = world if world is not None else (0, 1)
     dt = tensor_dtype(x)
     t_start = time.perf_counter()
-    eng = _lib.Engine(x.n, x.m, k_min, device=cfg.device, engine=cfg.engine)
+    # a sparse tensor stays sparse on the device (CSR + device-built CSC,
+    # k <= 32): every member resamples the stored values only
+    # (dist_rescal.py:205-214), as the reference does
+    sparse = is_sparse(x)
+    if sparse and k_max > 32:
+        if x.m * x.n * x.n > _DENSIFY_MAX:
+            raise DataError(f"sparse RESCALk runs on the CSR engine, which supports k <= 32 (k_max={k_max}); "
+                            f"a dense copy of this tensor ({x.m}x{x.n}x{x.n}) is too large")
+        sparse = False  # small tensor: the dense engine on the densified copy
+    eng = _lib.Engine(x.n, x.m, k_min, device=cfg.device, engine=cfg.engine, sparse=sparse)
     entries, timing = [], {"per_k_seconds": {}}
     try:
-        if size > 1 and allgather is not None:
+        if sparse:
+            eng.upload_csr(list(x.slices))
+        elif size > 1 and allgather is not None:
             # the replicas share one tensor: rank 0 uploads it over PCIe, the
             # others copy its device planes peer-to-peer over NVLink (every
             # rank uploading the same tensor contends for the host links);

@@ -21,6 +21,7 @@ from __future__ import annotations
 import contextlib
 import os
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,7 @@ from .containers import dense_slices, is_sparse, tensor_dtype
 
 _SEED_TAG_A = 1
 _SEED_TAG_R = 2
+_DENSIFY_MAX = 1 << 28  # elements: a sparse tensor this small may run on the dense engine when k > 32
 
 
 @dataclass
@@ -94,12 +96,14 @@ class RescalFactors:
         return RescalFactors(self.A.copy(), self.R.copy())
 
 
-def random_init(n: int, k: int, m: int, seed, dtype=np.float64) -> RescalFactors:
+def random_init(n: int, k: int, m: int, seed, dtype=np.float64, device: int | None = None) -> RescalFactors:
     """Seeded uniform start, partition independent (rescal.py:173-183):
     A from SeedSequence((seed, 1)), R from SeedSequence((seed, 2)), drawn in
-    fp64 then cast."""
+    fp64 then cast. ``device`` (extension): the GPU that draws a large A
+    (default: LOCAL_RANK); any device failure falls back to the host draw,
+    which gives the same values."""
     gr = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_R)))
-    a = _device_uniform(seed, _SEED_TAG_A, n * k)
+    a = _device_uniform(seed, _SEED_TAG_A, n * k, device)
     if a is None:
         ga = np.random.default_rng(np.random.SeedSequence((seed, _SEED_TAG_A)))
         a = ga.random((n, k), dtype=np.float64)
@@ -113,16 +117,17 @@ def random_init(n: int, k: int, m: int, seed, dtype=np.float64) -> RescalFactors
 _DEVICE_DRAW_MIN = 1 << 20
 
 
-def _device_uniform(seed, tag, count):
+def _device_uniform(seed, tag, count, device=None):
     if count < _DEVICE_DRAW_MIN or not isinstance(seed, (int, np.integer)):
         return None
     try:
-        if _lib.device_count() < 1:
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0"))
+        if not 0 <= device < _lib.device_count():
             return None
-    except Exception:  # noqa: BLE001 — no built library / no GPU visible
-        return None  # no built library / no GPU here: the host generator gives the same values
-    device = int(os.environ.get("LOCAL_RANK", "0"))
-    return _lib.pcg64_random_on(device, (int(seed), tag), count)
+        return _lib.pcg64_random_on(int(device), (int(seed), tag), count)
+    except Exception:  # noqa: BLE001 — no library / no GPU / OOM: the host generator gives the same values
+        return None
 
 
 def finalize_normalize(f: RescalFactors) -> RescalFactors:
@@ -167,6 +172,9 @@ def _engine_for(x, k, cfg: SolverConfig):
         eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], sparse=True)
         eng.upload_csr(list(x.slices))
     else:
+        if is_sparse(x) and x.m * x.n * x.n > _DENSIFY_MAX:
+            raise DataError(f"the sparse (CSR) engine supports k <= 32 (k={k}); a dense copy of this "
+                            f"tensor ({x.m}x{x.n}x{x.n}) is too large")
         eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], engine=cfg.engine)
         eng.upload(dense_slices(x))
     eng._cache_key = key
@@ -215,15 +223,77 @@ def _to_dtype(a, dt):
     return np.asarray(a).astype(dt, copy=False)
 
 
+class KernelCounters:
+    """Multiply-add and time accounting per kernel phase (grid.py:72-94).
+
+    The reference counts the MACs of every ``counted_mm`` call under the
+    phases ``gram_mul`` (A^T A, A^T X A), ``matrix_mul`` (dense products) and
+    ``matrix_mul_sparse`` (sparse-left products) and times them on the host.
+    Here ``rescal_solve(counters=...)`` records the same MAC counts (the
+    reference's per-call formulas summed analytically, rescal.py:124-153) and
+    the device time of the kernels behind each phase, measured with CUDA
+    events between the phases of every iteration (the run is not graph-
+    replayed while counting); ``device_run`` is the whole solve."""
+
+    def __init__(self):
+        self.flops = {}
+        self.seconds = {}
+
+    def add_flops(self, phase: str, n: int) -> None:
+        self.flops[phase] = self.flops.get(phase, 0) + int(n)
+
+    def add_time(self, phase: str, dt: float) -> None:
+        self.seconds[phase] = self.seconds.get(phase, 0.0) + dt
+
+    @contextlib.contextmanager
+    def timed(self, phase: str):
+        t0 = time.perf_counter()
+        try:
+            yield
+        finally:
+            self.add_time(phase, time.perf_counter() - t0)
+
+    def total_flops(self) -> int:
+        return sum(self.flops.values())
+
+
+def _count_iteration(counters, x, k: int, iters: int, tracked: int) -> None:
+    """MACs of `iters` MU iterations and `tracked` residual evaluations, with
+    the reference's counted_mm formulas (x@y of (a,b)@(b,c) counts a*b*c; a
+    sparse left operand counts nnz*c)."""
+    n, m = x.n, x.m
+    sparse = is_sparse(x)
+    gram = n * k * k + m * k * n * k  # ata, atxa per slice
+    small = m * (5 * n * k * k + 4 * k ** 3)  # xart ar art artatar aratart + rata deno_r atar atart
+    counters.add_flops("gram_mul", iters * gram)
+    counters.add_flops("matrix_mul", iters * small + tracked * m * (n * k * k + n * k * n))
+    if sparse:
+        counters.add_flops("matrix_mul_sparse", iters * 2 * k * sum(s.nnz for s in x.slices))
+    else:
+        counters.add_flops("matrix_mul", iters * m * 2 * n * n * k)
+
+
+def _phase_times(counters, eng, iters: int) -> None:
+    """Device time per phase of the last profiled run -> reference phase names."""
+    ph = eng.phase_timing()  # ms per iteration: k1, k2a, allreduce, k2f, numer_rs, apply_gather
+    big = "matrix_mul_sparse" if eng.sparse else "matrix_mul"
+    counters.add_time(big, ph["k1"] * iters / 1e3)
+    counters.add_time("gram_mul", ph["k2a"] * iters / 1e3)
+    counters.add_time("matrix_mul", (ph["k2f"] + ph["numer_rs"] + ph["apply_gather"]) * iters / 1e3)
+    if ph["allreduce"]:
+        counters.add_time("all_reduce", ph["allreduce"] * iters / 1e3)
+
+
 def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, counters=None,
                  engine: "_lib.Engine | None" = None):
     """Factorize ``x`` at rank ``k``; returns (RescalFactors, error trace).
 
     Same contract as rescal.py:186-225: ``initial`` is copied, otherwise the
     seeded random start; the trace holds err_l after each iteration and the
-    loop stops once err_l < tolerance. ``counters`` is accepted for signature
-    compatibility (device timing replaces MAC counting; see Engine.timing).
-    ``engine`` (extension) reuses a device-resident tensor across calls.
+    loop stops once err_l < tolerance. ``counters`` (a KernelCounters)
+    receives the reference's per-phase MAC counts and the device time of
+    each phase. ``engine`` (extension) reuses a device-resident tensor across
+    calls.
     """
     cfg = cfg or SolverConfig()
     if not 1 <= k <= x.n:
@@ -234,7 +304,7 @@ def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, count
         if f.A.shape != (x.n, k) or f.R.shape != (x.m, k, k):
             raise DataError("initial factors do not match tensor/k")
     else:
-        f = None if cfg.init == "nndsvd" else random_init(x.n, k, x.m, cfg.seed, dtype=dt)
+        f = None if cfg.init == "nndsvd" else random_init(x.n, k, x.m, cfg.seed, dtype=dt, device=cfg.device)
     own = engine is None
     eng = engine if engine is not None else _engine_for(x, k, cfg)
     try:
@@ -247,9 +317,17 @@ def rescal_solve(x, k: int, cfg: SolverConfig | None = None, initial=None, count
             eng.set_rank(k)
         eng.set_factors(a0, r0)
         eps = float(dt.type(cfg.epsilon))
-        _, trace = eng.run(cfg.max_iters, eps, track_error=cfg.track_error, tol=cfg.tolerance)
+        if counters is not None:
+            eng.set_option(1, 1)  # per-phase CUDA events (no graph replay while counting)
+        try:
+            done, trace = eng.run(cfg.max_iters, eps, track_error=cfg.track_error, tol=cfg.tolerance)
+        finally:
+            if counters is not None:
+                eng.set_option(1, 0)
         a, r = eng.get_factors()
-        if counters is not None and hasattr(counters, "add_time"):
+        if counters is not None:
+            _count_iteration(counters, x, k, done, len(trace))
+            _phase_times(counters, eng, done)
             counters.add_time("device_run", eng.timing()["run_ms"] / 1e3)
     finally:
         if own:

@@ -226,5 +226,71 @@ def main():
         print("wrote", name)
 
 
+def extra_cases(names):
+    """Round-2 fixtures, written one by one (``make_golden.py <name> ...``)
+    so the earlier fixtures are not rewritten."""
+    sys.path.insert(0, REF)
+    import rescalkit as rk
+    import tempfile
+
+    meta = np.array(repr(dict(numpy=np.__version__, scipy=sp.__version__ if hasattr(sp, "__version__") else "",
+                              reference=REF)))
+    if "rescalk_cfg5" in names:
+        # cfg5's sweep shape (k = 2..16, r = 10, delta = 0.02, 200 iterations,
+        # SolverConfig defaults otherwise) at a host-affordable n: a planted
+        # k_true = 6 tensor, m = 8 (model_select.py:422-503)
+        x, _, _ = rk.generate(rk.SynthSpec(n=256, m=8, k_true=6, noise=0.01, seed=21))
+        rep = rk.rescalk(x, 2, 16, r=10, cfg=rk.SolverConfig(max_iters=200, seed=0),
+                         pcfg=rk.PerturbConfig(delta=0.02, base_seed=0))
+        d = dict(X=x.slices, k_opt=np.array(rep.k_opt), low_conf=np.array(rep.low_confidence),
+                 ks=np.array([e.k for e in rep.entries]),
+                 s_min=np.array([e.s_min for e in rep.entries]),
+                 s_avg=np.array([e.s_avg for e in rep.entries]),
+                 rel_error=np.array([e.rel_error for e in rep.entries]), meta=meta)
+        np.savez_compressed(os.path.join(HERE, "rescalk_cfg5.npz"), **d)
+        print("wrote rescalk_cfg5", rep.k_opt, [round(e.s_min, 4) for e in rep.entries])
+    if "rescalk_sparse" in names:
+        # RESCALk on a SparseRelTensor: the reference resamples the stored
+        # values only (dist_rescal.py:205-214, model_select.py:450)
+        xp, _, _ = rk.generate(rk.SynthSpec(n=64, m=3, k_true=3, noise=0.01, seed=23))
+        xs = rk.sparsify(xp, 0.4)
+        rep = rk.rescalk(xs, 2, 4, r=4, cfg=rk.SolverConfig(max_iters=150, seed=2),
+                         pcfg=rk.PerturbConfig(delta=0.02, base_seed=5))
+        d = dict(X=xs.to_dense().slices, k_opt=np.array(rep.k_opt), ks=np.array([e.k for e in rep.entries]),
+                 s_min=np.array([e.s_min for e in rep.entries]), s_avg=np.array([e.s_avg for e in rep.entries]),
+                 rel_error=np.array([e.rel_error for e in rep.entries]),
+                 **{f"medians_k{e.k}": e.medians for e in rep.entries}, meta=meta)
+        np.savez_compressed(os.path.join(HERE, "rescalk_sparse.npz"), **d)
+        print("wrote rescalk_sparse", rep.k_opt, [round(e.s_min, 4) for e in rep.entries])
+    if "io_bytes" in names:
+        # the reference writer's exact bytes for a dense f32 / f64 tensor, a
+        # factor matrix and a COO file (tensor.py:188-327)
+        rng = np.random.default_rng(31)
+        d = {}
+        with tempfile.TemporaryDirectory() as td:
+            for tag, dt in (("f32", np.float32), ("f64", np.float64)):
+                xt = rk.RelTensor(rng.random((3, 9, 9)).astype(dt))
+                path = os.path.join(td, f"{tag}.rsk")
+                rk.save_tensor(xt, path)
+                d[f"dense_{tag}_X"] = xt.slices
+                d[f"dense_{tag}_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            a = rng.random((11, 4))
+            path = os.path.join(td, "a.rskm")
+            rk.save_matrix(a, path)
+            d["matrix_A"] = a
+            d["matrix_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            xs = rk.sparsify(rk.RelTensor(rng.random((2, 10, 10))), 0.3)
+            path = os.path.join(td, "x.coo")
+            rk.save_tensor(xs, path)
+            d["coo_dense"] = xs.to_dense().slices
+            d["coo_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        d["meta"] = meta
+        np.savez_compressed(os.path.join(HERE, "io_bytes.npz"), **d)
+        print("wrote io_bytes")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:
+        extra_cases(sys.argv[1:])
+    else:
+        main()

@@ -35,3 +35,21 @@ def test_grid_matches_oracle(nproc, exchange):
     assert rep["ok"], rep
     used = {c.get("exchange") for c in rep["cases"] if c["engine"] != "sparse" and c["k"] in (16, 32)}
     assert used == {exchange}, rep
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_grid_cfg3_block_matches_oracle(nproc, exchange):
+    """cfg3's n = 32768, k = 32 on the 1x2 / 2x2 grid: solve_on_grid with a
+    per-rank BlockSource vs the fp64 oracle (tools/grid_check_big.py)."""
+    if _gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + nproc + (10 if exchange == "nccl" else 0)),
+           os.path.join(ROOT, "tools", "grid_check_big.py")]
+    env = dict(os.environ, RK_PEER="1" if exchange == "peer" else "0")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert out.returncode == 0 and line, out.stdout[-2000:] + out.stderr[-2000:]
+    rep = json.loads(line[-1])
+    assert rep["ok"] and rep["exchange"] == exchange, rep
