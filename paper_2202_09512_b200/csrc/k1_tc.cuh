@@ -501,6 +501,57 @@ constexpr uint32_t k1_smem_bytes() {  // same for both MQ variants
 // Deterministic reduction of the partials:
 //   P[t][i] = sum_s Ppart[t][s][i]                         (i < NR)
 //   Q[t][j] = sum_{slots of (t, strip(j))} Qpart[slot][j - strip0]   (j < NC)
+// Body over a grid-stride range (thread g0 of gstride); also run as phase 1
+// of the fused k-wide chain (k2_chain.cuh).
+// One float4 of P (row i of slice t, columns 4 q4 .. 4 q4 + 3): strips summed in order.
+RK_DEV void k1_reduce_p4(const float* __restrict__ Ppart, float* __restrict__ P, int NR, int K, int M,
+                         int nstrips, int t, int i, int q4) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < nstrips; ++s) {
+    float4 v = reinterpret_cast<const float4*>(Ppart + ((((size_t)s * M + t) * NR) + i) * K)[q4];
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  reinterpret_cast<float4*>(P + ((size_t)t * NR + i) * K)[q4] = acc;
+}
+
+// One float4 of Q (row j of slice t): the Q-partial slots of its strip in order.
+RK_DEV void k1_reduce_q4(const float* __restrict__ Qpart, const int* __restrict__ slot_first,
+                         const int* __restrict__ slot_count, float* __restrict__ Q, int NC, int K, int c,
+                         int nstrips, int t, int j, int q4) {
+  const int W = c * kTile;
+  const int s = j / W;
+  const int jl = j - s * W;
+  const int f = slot_first[t * nstrips + s], nsl = slot_count[t * nstrips + s];
+  float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < nsl; ++q) {
+    float4 v = reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K)[q4];
+    qa.x += v.x; qa.y += v.y; qa.z += v.z; qa.w += v.w;
+  }
+  reinterpret_cast<float4*>(Q + ((size_t)t * NC + j) * K)[q4] = qa;
+}
+
+RK_DEV void k1_reduce_body(const float* __restrict__ Ppart, const float* __restrict__ Qpart,
+                           const int* __restrict__ slot_first, const int* __restrict__ slot_count,
+                           float* __restrict__ P, float* __restrict__ Q, int NR, int NC, int K, int M, int c,
+                           int nstrips, int64_t g0, int64_t gstride) {
+  const int K4 = K / 4;
+  const int64_t totalP = (int64_t)M * NR * K4;
+  const int64_t total = totalP + (int64_t)M * NC * K4;
+#pragma unroll 2
+  for (int64_t e = g0; e < total; e += gstride) {
+    if (e < totalP) {
+      const int q4 = (int)(e % K4);
+      const int64_t ti = e / K4;
+      k1_reduce_p4(Ppart, P, NR, K, M, nstrips, (int)(ti / NR), (int)(ti % NR), q4);
+    } else {
+      const int64_t e2 = e - totalP;
+      const int q4 = (int)(e2 % K4);
+      const int64_t tj = e2 / K4;
+      k1_reduce_q4(Qpart, slot_first, slot_count, Q, NC, K, c, nstrips, (int)(tj / NC), (int)(tj % NC), q4);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
                                                  const float* __restrict__ Ppart,
                                                  const float* __restrict__ Qpart,
@@ -511,42 +562,8 @@ __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
                                                  int skip_if_stopped) {
   pdl_entry();
   if (skip_if_stopped && ctl->stop) return;
-  const int W = c * kTile;
-  const int K4 = K / 4;
-  const int64_t totalP = (int64_t)M * NR * K4;
-  const int64_t total = totalP + (int64_t)M * NC * K4;
-#pragma unroll 2
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < totalP) {
-      const int q4 = (int)(e % K4);
-      const int64_t ti = e / K4;
-      const int i = (int)(ti % NR);
-      const int t = (int)(ti / NR);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s = 0; s < nstrips; ++s) {
-        float4 v = reinterpret_cast<const float4*>(
-            Ppart + ((((size_t)s * M + t) * NR) + i) * K)[q4];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      reinterpret_cast<float4*>(P + ((size_t)t * NR + i) * K)[q4] = acc;
-    } else {
-      const int64_t e2 = e - totalP;
-      const int q4 = (int)(e2 % K4);
-      const int64_t tj = e2 / K4;
-      const int j = (int)(tj % NC);
-      const int t = (int)(tj / NC);
-      const int s = j / W;
-      const int jl = j - s * W;
-      const int f = slot_first[t * nstrips + s], nsl = slot_count[t * nstrips + s];
-      float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q = 0; q < nsl; ++q) {
-        float4 v = reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K)[q4];
-        qa.x += v.x; qa.y += v.y; qa.z += v.z; qa.w += v.w;
-      }
-      reinterpret_cast<float4*>(Q + ((size_t)t * NC + j) * K)[q4] = qa;
-    }
-  }
+  k1_reduce_body(Ppart, Qpart, slot_first, slot_count, P, Q, NR, NC, K, M, c, nstrips,
+                 (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 }  // namespace tc

@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(kThreads) k2a_gs(const Ctl* __restrict__ ctl,
 // 3 split update_a (M from the current cores, no trace, no core change).
 template <int KT>
 RK_DEV void k2f_body(Ctl* __restrict__ ctl,
-                                                      const double* __restrict__ gs,
+                                                      const double* __restrict__ gsG,
+                                                      const double* __restrict__ gsS,
                                                       double* __restrict__ R,
                                                       double* __restrict__ Rnext,
                                                       double* __restrict__ Mt,
@@ -179,9 +180,10 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
                                                       double* __restrict__ trace, int K, int M,
                                                       double eps, int mode, double* gscratch,
                                                       unsigned* __restrict__ counter,
-                                                      float* __restrict__ W32, double* sh) {
+                                                      float* __restrict__ W32, double* sh, int t) {
   // KT > 0: compile-time K (unrolled shared-memory products, constant index
-  // arithmetic); KT = 0: runtime K. Same arithmetic either way.
+  // arithmetic); KT = 0: runtime K. Same arithmetic either way. t: the slice
+  // (the block index of the standalone kernel).
   if (KT) K = KT;
   __shared__ double red[32];
   __shared__ bool s_last;
@@ -190,7 +192,6 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
     if constexpr (KT > 0) mm_kk_t<KT>(C, A, ta, B, tb);
     else mm_kk(C, A, ta, B, tb, K);
   };
-  const int t = blockIdx.x;
   const int KK = K * K;
   double* base = gscratch ? gscratch + (size_t)t * 5 * KK : sh;
   double* G = base;
@@ -198,9 +199,9 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
   double* T1 = base + 2 * KK;
   double* T2 = base + 3 * KK;
   double* Rn = base + 4 * KK;
-  const double* S = gs + (size_t)(1 + t) * KK;
+  const double* S = gsS;  // S_t (gs + (1 + t) K^2 of the reduced [G, S_1..S_m])
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    G[e] = gs[e];
+    G[e] = gsG[e];
     Rt[e] = R[(size_t)t * KK + e];
   }
   __syncthreads();
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl, con
   pdl_entry();
   if (ctl->stop) return;
   extern __shared__ double sh[];
-  k2f_body<0>(ctl, gs, R, Rnext, Mt, Mout, tt, rres, nres, trace, K, M, eps, mode, gscratch, counter, W32, sh);
+  k2f_body<0>(ctl, gs, gs + (size_t)(1 + blockIdx.x) * K * K, R, Rnext, Mt, Mout, tt, rres, nres, trace, K, M, eps, mode, gscratch, counter, W32, sh,
+              blockIdx.x);
 }
 
 // k2f_fused with compile-time K (16 or 32; shared-memory scratch only)
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, c
   pdl_entry();
   if (ctl->stop) return;
   extern __shared__ double sh[];
-  k2f_body<KT>(ctl, gs, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode, nullptr, counter, W32, sh);
+  k2f_body<KT>(ctl, gs, gs + (size_t)(1 + blockIdx.x) * KT * KT, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode, nullptr, counter, W32, sh,
+               blockIdx.x);
 }
 
 // K2b (v2): A update. Every core is staged once in shared memory as fp32
@@ -602,27 +605,27 @@ inline int k2b_v4_rpt(int K, int64_t N) { return (K == 32 && N >= 2 * 148 * 64) 
 
 inline int k2b_v4_rb(int K, int64_t N) { return k2b_v4_rpt(K, N) * (256 / K); }
 
-template <int K, int RPT>
-__global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __restrict__ A64,
-                                              float* __restrict__ A32,
-                                              __nv_bfloat16* __restrict__ ATh,
-                                              __nv_bfloat16* __restrict__ ATl,
-                                              const float* __restrict__ P,
-                                              const float* __restrict__ Q,
-                                              const float* __restrict__ W32,
-                                              const double* __restrict__ Mm, int N, int M, int tg,
-                                              double eps_m) {
-  pdl_entry();
+// One row block `rbi` (also the last phase of the fused k-wide chain,
+// k2_chain.cuh, where P / Q / W32 were written earlier in the same launch:
+// COH = coherent L2 loads instead of the read-only path).
+template <typename T>
+RK_DEV T ld_pq(const T* p, bool coh) {
+  return coh ? __ldcg(p) : __ldg(p);
+}
+
+template <int K, int RPT, bool COH = false>
+RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float* __restrict__ A32,
+                         __nv_bfloat16* __restrict__ ATh, __nv_bfloat16* __restrict__ ATl,
+                         const float* __restrict__ P, const float* __restrict__ Q, const float* __restrict__ W32,
+                         const double* __restrict__ Mm, int N, int M, int tg, double eps_m, int rbi, float* shf) {
   static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
-  if (ctl->stop) return;
-  extern __shared__ float shf[];
   constexpr int TR = 256 / K;   // thread rows
   constexpr int RB = RPT * TR;  // rows per block
   constexpr int K4 = K / 4;
   float* Ws = shf;                                   // [tg][2][K][K]
   float* PQs = shf + (size_t)tg * 2 * K * K;         // [tg][2][RB][K]
   const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
-  const int rbase = blockIdx.x * RB;
+  const int rbase = rbi * RB;
   double nacc[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) nacc[j] = 0.0;
@@ -638,7 +641,7 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int e = e0 + q * blockDim.x;
-          v[q] = e < nw ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[q] = e < nw ? ld_pq(src + e, COH) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -660,7 +663,8 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
             const int r = rem2 / K4, qq = rem2 - r * K4;
             const int row = rbase + r;
             if (row < N)
-              v[q] = __ldg(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + qq);
+              v[q] = ld_pq(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + qq,
+                           COH);
           }
         }
 #pragma unroll
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
     if (i < N) {
       const double* Ai = A64 + (size_t)i * K;
       double deno = eps_m;
-      for (int d = 0; d < K; ++d) deno = fma(Ai[d], Mm[d * K + c], deno);
+      for (int d = 0; d < K; ++d) deno = fma(Ai[d], COH ? __ldcg(Mm + d * K + c) : Mm[d * K + c], deno);
       an[j] = Ai[c] * nacc[j] / deno;
       if (!isfinite(an[j])) bad = true;
     }
@@ -732,6 +736,22 @@ __global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __r
       ATl[(size_t)c * N + i] = lo;
     }
   }
+}
+
+template <int K, int RPT>
+__global__ void __launch_bounds__(256) k2b_v4(Ctl* __restrict__ ctl, double* __restrict__ A64,
+                                              float* __restrict__ A32,
+                                              __nv_bfloat16* __restrict__ ATh,
+                                              __nv_bfloat16* __restrict__ ATl,
+                                              const float* __restrict__ P,
+                                              const float* __restrict__ Q,
+                                              const float* __restrict__ W32,
+                                              const double* __restrict__ Mm, int N, int M, int tg,
+                                              double eps_m) {
+  pdl_entry();
+  if (ctl->stop) return;
+  extern __shared__ float shf[];
+  k2b_v4_block<K, RPT>(ctl, A64, A32, ATh, ATl, P, Q, W32, Mm, N, M, tg, eps_m, blockIdx.x, shf);
 }
 
 // Grid numerator (K in {16, 32}): U[row] = sum_t PQ_t[row] W_t with W_t =

@@ -307,23 +307,25 @@ struct SpGramTc {
 // KT = 32 (dense single GPU): each (slot, chunk) item is split into the four
 // 16 x 16 column quadrants of S (item-minor), each the K = 16 product above on
 // column slices of the 32-wide rows; quadrants write disjoint partial entries.
+// Body over the items bid, bid + nblk, ... (also phase 2 of the fused
+// k-wide chain, k2_chain.cuh); gts: the block's >= SpGramTc::smem bytes.
 template <int KT>
-__global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc_k(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
-                                                     const float* __restrict__ P, int n, int ldp, int M, int nchunk,
-                                                     double* __restrict__ part, int skip_if_stopped,
-                                                     const float* __restrict__ Aown = nullptr, int nown = 0) {
+RK_DEV void sp_gram_tc_body(const float* __restrict__ A32, const float* __restrict__ P, int n, int ldp, int M,
+                            int nchunk, double* __restrict__ part, const float* __restrict__ Aown, int nown,
+                            int bid, int nblk, float* gts) {
   // slot 0 (G) runs over Aown's nown rows when given (a grid rank's own piece
   // of A, rescal.py:124 with the grid's rank-ascending sum, dist_rescal.py:74-92)
   using C = SpGramTc;
   static_assert(KT == 16 || KT == 32, "sp_gram_tc_k: K = 16 or 32");
   constexpr int NQ1 = KT / 16, NQ = NQ1 * NQ1;
-  if (skip_if_stopped && ctl->stop) return;
-  extern __shared__ __align__(16) float gts[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int rows_per_chunk = (n + nchunk - 1) / nchunk;
+  // a block takes whole (slot, chunk) groups (all NQ quadrant items of the
+  // same rows): the fused chain reduces exactly those P rows just before
   const int nitems = (M + 1) * nchunk * NQ;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  for (int item0 = bid * NQ; item0 < nitems; item0 += nblk * NQ)
+  for (int item = item0; item < item0 + NQ; ++item) {
     const int q = item % NQ, sc = item / NQ;
     const int slot = sc / nchunk, chunk = sc - slot * nchunk;
     const int ca = (q / NQ1) * 16, cb = (q % NQ1) * 16;
@@ -428,6 +430,16 @@ __global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc_k(const Ctl* __rest
       part[((size_t)slot * nchunk + chunk) * KT * KT + (ca + (tid >> 4)) * KT + cb + (tid & 15)] = v;
     }
   }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc_k(const Ctl* __restrict__ ctl, const float* __restrict__ A32,
+                                                     const float* __restrict__ P, int n, int ldp, int M, int nchunk,
+                                                     double* __restrict__ part, int skip_if_stopped,
+                                                     const float* __restrict__ Aown = nullptr, int nown = 0) {
+  if (skip_if_stopped && ctl->stop) return;
+  extern __shared__ __align__(16) float gts[];
+  sp_gram_tc_body<KT>(A32, P, n, ldp, M, nchunk, part, Aown, nown, blockIdx.x, gridDim.x, gts);
 }
 
 __global__ void __launch_bounds__(256) sp_gram_reduce(const Ctl* __restrict__ ctl,
