@@ -506,9 +506,22 @@ constexpr uint32_t k1_smem_bytes() {  // same for both MQ variants
 // One float4 of P (row i of slice t, columns 4 q4 .. 4 q4 + 3): strips summed in order.
 RK_DEV void k1_reduce_p4(const float* __restrict__ Ppart, float* __restrict__ P, int NR, int K, int M,
                          int nstrips, int t, int i, int q4) {
+  // loads batched 4 at a time (independent, in flight together), sums kept in strip order
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = 0; s < nstrips; ++s) {
-    float4 v = reinterpret_cast<const float4*>(Ppart + ((((size_t)s * M + t) * NR) + i) * K)[q4];
+  const size_t sstride = (size_t)M * NR * K / 4;  // float4s between strips
+  const float4* src = reinterpret_cast<const float4*>(Ppart + (((size_t)t * NR) + i) * K) + q4;
+  int s = 0;
+  for (; s + 4 <= nstrips; s += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = src[(size_t)(s + u) * sstride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+    }
+  }
+  for (; s < nstrips; ++s) {
+    const float4 v = src[(size_t)s * sstride];
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
   }
   reinterpret_cast<float4*>(P + ((size_t)t * NR + i) * K)[q4] = acc;
@@ -523,8 +536,20 @@ RK_DEV void k1_reduce_q4(const float* __restrict__ Qpart, const int* __restrict_
   const int jl = j - s * W;
   const int f = slot_first[t * nstrips + s], nsl = slot_count[t * nstrips + s];
   float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int q = 0; q < nsl; ++q) {
-    float4 v = reinterpret_cast<const float4*>(Qpart + ((size_t)(f + q) * W + jl) * K)[q4];
+  const float4* src = reinterpret_cast<const float4*>(Qpart + ((size_t)f * W + jl) * K) + q4;
+  const size_t qstride = (size_t)W * K / 4;  // float4s between slots
+  int q = 0;
+  for (; q + 4 <= nsl; q += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = src[(size_t)(q + u) * qstride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      qa.x += v[u].x; qa.y += v[u].y; qa.z += v[u].z; qa.w += v[u].w;
+    }
+  }
+  for (; q < nsl; ++q) {
+    const float4 v = src[(size_t)q * qstride];
     qa.x += v.x; qa.y += v.y; qa.z += v.z; qa.w += v.w;
   }
   reinterpret_cast<float4*>(Q + ((size_t)t * NC + j) * K)[q4] = qa;

@@ -32,7 +32,6 @@
 
 #include "../../include/rescal_b200.h"
 #include "k1_tc.cuh"
-#include "k2_chain.cuh"
 #include <nvtx3/nvToolsExt.h>
 #include "peer.cuh"
 #include "rk_kernels.cuh"
@@ -262,12 +261,6 @@ struct rk_handle {
   // tcgen05 schedule
   int c = 0, nstrips = 0, grid_tc = 0, nslots = 0;
   bool k1_mq = true;  // K1 merges the Q hi/lo operands (always at K = 16; see k1_merge_q)
-  // fused k-wide chain (k2_chain.cuh): one cooperative launch after K1
-  bool chain = false, chain_on = true;
-  int chain_grid = 0;
-  size_t chain_smem = 0;
-  double* gsx = nullptr;
-  unsigned* chain_bar = nullptr;
   size_t smem_tc = 0;
   float *Ppart = nullptr, *Qpart = nullptr;
   int *d_cta_begin = nullptr, *d_cta_slot = nullptr, *d_slot_first = nullptr,
@@ -346,11 +339,6 @@ void free_factor_buffers(rk_handle* h) {
   h->gpart = nullptr;
   dfree(h->wfrag);
   h->wfrag = nullptr;
-  dfree(h->gsx);
-  dfree(h->chain_bar);
-  h->gsx = nullptr;
-  h->chain_bar = nullptr;
-  h->chain = false;
   void* ptrs[] = {h->Arow, h->A32row, h->ATh_row, h->ATl_row, h->R, h->Rnext, h->Mt, h->Mm, h->tt,
                   h->part, h->red, h->gscratch, h->counters, h->W32, h->d_simt_first,
                   h->d_simt_count, h->UI, h->UJ, h->regS, h->regG, h->regT,
@@ -468,30 +456,6 @@ void plan_tc(rk_handle* h) {
                                  (int)h->smem_tc));
 }
 
-template <int K, int RPT>
-void chain_attrs(rk_handle* h, int* occ) {
-  RK_CUDA(cudaFuncSetAttribute(rk::k2_chain<K, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)h->chain_smem));
-  RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, rk::k2_chain<K, RPT>, 256, h->chain_smem));
-}
-
-// The fused k-wide chain (single GPU, dense, K in {16, 32}): one CTA set that
-// stays co-resident (cooperative launch) -- up to 4 per SM.
-void setup_chain(rk_handle* h) {
-  const int K = h->K;
-  h->chain_smem = rk::k2_chain_smem(K, (int)h->m, h->NR);
-  int occ = 0;
-  const int rpt = rk::k2b_v4_rpt(K, h->NR);
-  if (K == 16) chain_attrs<16, 2>(h, &occ);
-  else if (rpt == 8) chain_attrs<32, 8>(h, &occ);
-  else chain_attrs<32, 2>(h, &occ);
-  if (occ < 1) return;
-  h->chain_grid = h->num_sms * std::min(occ, 4);
-  h->gsx = dalloc<double>((size_t)h->m * K * K);
-  h->chain_bar = dalloc<unsigned>(2);
-  h->chain = true;
-}
-
 void alloc_factor_buffers(rk_handle* h) {
   const int K = h->K;
   const int64_t M = h->m;
@@ -597,7 +561,6 @@ void alloc_factor_buffers(rk_handle* h) {
              "tcgen05 engine needs k_pad in {16, 32}");
   h->engine = eng;
   if (eng == RK_ENGINE_TC) plan_tc(h);
-  if (eng == RK_ENGINE_TC && h->fast && dense_gram_tc(h) && h->gpart) setup_chain(h);
   const size_t simt_smem = (size_t)(64 * 33 + 64 * K) * sizeof(float);
   RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
   RK_CUDA(cudaFuncSetAttribute(rk::k1_simt_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simt_smem));
@@ -783,7 +746,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 
 // ------------------------------- launches ----------------------------------
 
-void launch_k1(rk_handle* h, bool timed, bool with_reduce = true) {
+void launch_k1(rk_handle* h, bool timed) {
   cudaStream_t s = h->stream;
   const int K = h->K, M = (int)h->m;
   if (timed) {
@@ -831,7 +794,7 @@ void launch_k1(rk_handle* h, bool timed, bool with_reduce = true) {
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
-    if (with_reduce) {  // (else the fused k-wide chain reduces the partials)
+    {
       launch_pdl(rk::tc::k1_reduce, dim3(h->num_sms * 8), dim3(256), 0, s, (const Ctl*)h->ctl,
                  (const float*)h->Ppart, (const float*)h->Qpart, (const int*)h->d_slot_first,
                  (const int*)h->d_slot_count, h->P, h->Q, (int)h->NR, (int)h->NC, K, M, h->c, h->nstrips, 1);
@@ -1195,68 +1158,6 @@ void phase_mark(rk_handle* h, bool timed, int idx) {
   RK_CUDA(cudaEventRecord(h->ev_ph[i], h->stream));
 }
 
-template <int K, int RPT>
-void launch_chain_t(rk_handle* h, const rk::ChainArgs& a) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(h->chain_grid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = h->chain_smem;
-  cfg.stream = h->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  RK_CUDA(cudaLaunchKernelEx(&cfg, rk::k2_chain<K, RPT>, a));
-}
-
-// The k-wide chain of one iteration after K1 (k1_reduce + G/S + core update +
-// A update) as one cooperative launch (k2_chain.cuh).
-void launch_chain(rk_handle* h) {
-  const int K = h->K;
-  rk::ChainArgs a{};
-  a.ctl = h->ctl;
-  a.Ppart = h->Ppart;
-  a.Qpart = h->Qpart;
-  a.slot_first = h->d_slot_first;
-  a.slot_count = h->d_slot_count;
-  a.P = h->P;
-  a.Q = h->Q;
-  a.NR = (int)h->NR;
-  a.NC = (int)h->NC;
-  a.M = (int)h->m;
-  a.c = h->c;
-  a.nstrips = h->nstrips;
-  a.A32 = h->A32row;
-  a.rows_valid = (int)h->rows_valid;
-  a.gchunks = h->gchunks;
-  a.gpart = h->gpart;
-  a.red = h->red;
-  a.gsx = h->gsx;
-  a.R = h->R;
-  a.Rnext = h->Rnext;
-  a.Mt = h->Mt;
-  a.Mm = h->Mm;
-  a.tt = h->tt;
-  a.rres = h->rpart;
-  a.nres = h->nr;
-  a.trace = h->trace_dev;
-  a.eps = h->eps;
-  a.ticket = h->counters + h->m + 1;
-  a.W32 = h->W32;
-  a.A64 = h->Arow;
-  a.ATh = h->ATh_row;
-  a.ATl = h->ATl_row;
-  a.tg = rk::k2_chain_tg(K, (int)h->m, h->NR);
-  a.eps_m = h->eps * (double)h->m;
-  a.bar = h->chain_bar;
-  const int rpt = rk::k2b_v4_rpt(K, h->NR);
-  if (K == 16) launch_chain_t<16, 2>(h, a);
-  else if (rpt == 8) launch_chain_t<32, 8>(h, a);
-  else launch_chain_t<32, 2>(h, a);
-  h->launches += 1;
-}
-
 // NVTX ranges with the reference's phase names (grid.py:97-111 counted_mm
 // phases, perf.py:32-33) around the host enqueue of each phase; emitted only
 // in profile mode (per-phase events, no graph replay), so a timeline tool
@@ -1273,16 +1174,6 @@ struct NvtxPhase {
 
 // phases: 0 K1(+reduce) | 1 K5+K2a | 2 grid all-reduce | 3 K2f | 4 K2b/numerator (+RS) | 5 A update/gather
 void enqueue_iteration(rk_handle* h, bool timed, bool with_k5) {
-  if (h->chain && h->chain_on && !timed) {
-    // two launches per iteration: K1 (tcgen05 slice contraction) and the
-    // fused k-wide chain; the gated direct-residual pass K5 (tracked runs
-    // only) reads X and the old factors, so it goes between them. Profile
-    // mode keeps the separate kernels (per-phase events).
-    launch_k1(h, false, false);
-    if (with_k5) launch_k5(h, 1);
-    launch_chain(h);
-    return;
-  }
   phase_mark(h, timed, 0);
   {
     NvtxPhase r(timed, h->sparse ? "matrix_mul_sparse" : "matrix_mul");
@@ -2022,10 +1913,6 @@ int rk_set_option(rk_handle* h, int32_t key, int64_t value) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     if (key == 1) h->profile = value != 0;
-    else if (key == 5) {  // fused k-wide chain on / off (tests compare the two paths)
-      if (h->chain_on != (value != 0)) drop_graphs(h);
-      h->chain_on = value != 0;
-    }
     else if (key == 4) h->skip_comm = value != 0;
     else if (key == 2) {
       h->use_graph = value != 0;
@@ -2231,6 +2118,7 @@ int rk_run(rk_handle* h, int32_t iters, double eps, int32_t track_error, double 
         const int before = h->launches;
         for (int q = 0; q < (batched ? rk_handle::kGraphBatch : 1); ++q) enqueue_iteration(h, false, ti != 0);
         h->graph_launches[ti][batched] = h->launches - before;
+        h->launches = before;  // captured, not launched: counted when the graph runs
         RK_CUDA(cudaStreamEndCapture(h->stream, &g));
         RK_CUDA(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);

@@ -143,32 +143,3 @@ def test_dist_perturb_is_grid_independent(n, pr, pc):
         np.testing.assert_array_equal(blk.slices, block_of(whole, n, lay))
         sblk = rk.dist_perturb(rk.grid_block(xs, pr, pc, gi, gj), pcfg, (4, 2))
         np.testing.assert_array_equal(np.stack([q.toarray() for q in sblk.slices]), block_of(whole_s, n, lay))
-
-
-@pytest.mark.parametrize("n,m,k,track", [(1024, 4, 16, True), (640, 3, 32, True), (20000, 2, 32, False),
-                                         (256, 8, 4, True)])
-def test_fused_chain_is_bit_identical_to_separate_kernels(n, m, k, track):
-    """k2_chain.cuh (one cooperative launch after K1) runs the same phase
-    bodies in the same order as k1_reduce + sp_gram_tc_k + sp_gram_reduce +
-    k2f_fused_t + k2b_v4: factors and trace must match bit for bit."""
-    x = uniform_x(m, n, 4)
-    f0 = rk.random_init(n, k, m, 6)
-    out = []
-    for chain in (1, 0):
-        eng = _lib.Engine(n, m, k, device=0, engine="tc")
-        try:
-            eng.upload(x)
-            eng.set_option(5, chain)
-            eng.set_factors(f0.A, f0.R)
-            done, trace = eng.run(20, 1e-16, track_error=track)
-            a, r = eng.get_factors()
-            launches = eng.timing()["launches"]
-        finally:
-            eng.close()
-        out.append((a, r, trace, done, launches))
-    (a1, r1, t1, d1, l1), (a0, r0, t0, d0, l0) = out
-    assert d1 == d0 == 20
-    np.testing.assert_array_equal(a1, a0)
-    np.testing.assert_array_equal(r1, r0)
-    np.testing.assert_array_equal(t1, t0)
-    assert l1 <= (3 if track else 2) * 20 < l0, (l1, l0)  # K1 + chain (+ gated K5) per iteration

@@ -1,3 +1,18 @@
+// EXPERIMENT (not built into librescal_b200.so): measured slower than the
+// five separate kernels it replaces, so the product keeps those. Round-2 data
+// (B200, graph-replayed iterations, tools/experiments/chain_probe.py,
+// profiles/r02_chain_experiment.json):
+//   it/s chain vs separate: cfg1 27.4k vs 32.0k, cfg2 1325 vs 1338,
+//   cfg5 689 vs 695, n=2048/k=32 7.6k vs 9.1k, cfg3 78.1 vs 78.7.
+//   Phase edges of one launch (us from block 0's entry), cfg2:
+//   A end 30.7, barrier 1 exit 33.6, B end 50.5, barrier 2 exit 53.8,
+//   C end 72.2 -- each grid barrier costs ~2.5-3 us, more than a kernel
+//   boundary inside a CUDA graph, and every phase stays latency-bound with
+//   fewer co-resident warps than the standalone kernel it replaces.
+// It compiled against the phase bodies the standalone kernels share
+// (tc::k1_reduce_p4 / k1_reduce_q4, sp::sp_gram_tc_body, k2f_body,
+// k2b_v4_block) and was bit-identical to them (GPU test, round 2).
+//
 // k2_chain — the k-wide part of one MU iteration in ONE persistent launch
 // (single GPU, dense, K in {16, 32}), after the K1 slice contraction:
 //
@@ -65,11 +80,19 @@ struct ChainArgs {
   int tg;
   double eps_m;
   unsigned* bar;  // [2]: arrival count, generation (self-resetting)
+  int sleep_ns;   // barrier poll back-off
+  unsigned long long* stamps;  // diagnostics: [6] globaltimer at the phase edges (null: off)
 };
+
+RK_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Grid-wide barrier (all blocks co-resident): arrive on a counter, the last
 // arrival resets it and bumps the generation the others spin on.
-RK_DEV void chain_grid_sync(unsigned* bar, unsigned nblocks) {
+RK_DEV void chain_grid_sync(unsigned* bar, unsigned nblocks, int sleep_ns) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* vgen = bar + 1;
@@ -80,7 +103,8 @@ RK_DEV void chain_grid_sync(unsigned* bar, unsigned nblocks) {
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
-      while (*vgen == gen) __nanosleep(40);
+      while (*vgen == gen)
+        if (sleep_ns) __nanosleep(sleep_ns);
     }
     __threadfence();
   }
@@ -91,6 +115,7 @@ template <int K, int RPT>
 __global__ void __launch_bounds__(256) k2_chain(ChainArgs a) {
   static_assert(K == 16 || K == 32, "k2_chain: K in {16, 32}");
   if (a.ctl->stop) return;  // set before this launch: every block takes the same exit
+  if (a.stamps && threadIdx.x == 0 && blockIdx.x == 0) a.stamps[0] = globaltimer_ns();
   extern __shared__ __align__(16) float csm[];
   const int bid = blockIdx.x, nblk = gridDim.x, tid = threadIdx.x;
   const int M = a.M;
@@ -130,18 +155,17 @@ __global__ void __launch_bounds__(256) k2_chain(ChainArgs a) {
     // (c) G / S_t chunk partials (cp.async.cg reads of P go through L2)
     sp::sp_gram_tc_body<K>(a.A32, a.P, n, a.NR, M, nchunk, a.gpart, nullptr, 0, bid, nblk, csm);
   }
-  chain_grid_sync(a.bar, nblk);
+  if (a.stamps && tid == 0) atomicMax(a.stamps + 1 + 2 * 0, globaltimer_ns());
+  chain_grid_sync(a.bar, nblk, a.sleep_ns);
+  if (a.stamps && tid == 0 && bid == 0) a.stamps[2] = globaltimer_ns();
 
   // ---------------- phase B: per-slice core update, M, commit ---------------
   if (bid < M) {
     const int t = bid, nchunk = a.gchunks;
     double* gsG = a.gsx + (size_t)t * KK;
     for (int e = tid; e < KK; e += 256) {
-      double g = 0.0, s = 0.0;
-      for (int q = 0; q < nchunk; ++q) {
-        g += __ldcg(a.gpart + (size_t)q * KK + e);
-        s += __ldcg(a.gpart + ((size_t)(1 + t) * nchunk + q) * KK + e);
-      }
+      const double g = sp::sum_chunks(a.gpart + e, nchunk, KK);
+      const double s = sp::sum_chunks(a.gpart + (size_t)(1 + t) * nchunk * KK + e, nchunk, KK);
       gsG[e] = g;
       if (t == 0) a.red[e] = g;
       a.red[(size_t)(1 + t) * KK + e] = s;
@@ -150,7 +174,9 @@ __global__ void __launch_bounds__(256) k2_chain(ChainArgs a) {
     k2f_body<K>(a.ctl, gsG, a.red + (size_t)(1 + t) * KK, a.R, a.Rnext, a.Mt, a.Mm, a.tt, a.rres, a.nres,
                 a.trace, K, M, a.eps, 0, nullptr, a.ticket, a.W32, reinterpret_cast<double*>(csm), t);
   }
-  chain_grid_sync(a.bar, nblk);
+  if (a.stamps && tid == 0) atomicMax(a.stamps + 3, globaltimer_ns());
+  chain_grid_sync(a.bar, nblk, a.sleep_ns);
+  if (a.stamps && tid == 0 && bid == 0) a.stamps[4] = globaltimer_ns();
 
   // ---------------- phase C: A update + operand planes ----------------------
   if (*reinterpret_cast<volatile int*>(&a.ctl->stop)) return;  // tolerance / non-finite: same on every block
@@ -159,6 +185,7 @@ __global__ void __launch_bounds__(256) k2_chain(ChainArgs a) {
   for (int rbi = bid; rbi < nrb; rbi += nblk)
     k2b_v4_block<K, RPT, true>(a.ctl, a.A64, a.A32, a.ATh, a.ATl, a.P, a.Q, a.W32, a.Mm,
                                a.NR, M, a.tg, a.eps_m, rbi, csm);
+  if (a.stamps && tid == 0) atomicMax(a.stamps + 5, globaltimer_ns());
 }
 
 // fused-kernel k2b staging: slices per group so that its shared memory stays
