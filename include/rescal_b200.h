@@ -92,7 +92,11 @@ int rk_upload_csr_slices(rk_handle* h, const int64_t* const* indptrs, const int3
 int rk_upload_dense(rk_handle* h, const void* x, int32_t dtype);
 
 /* Same, but for one rank's block of a p_r x p_c grid: x is (m, rows, cols)
- * C-contiguous and lands in the top-left corner of the padded slices. */
+ * C-contiguous and lands in the top-left corner of the padded slices.
+ * sq_norm_global: ||X||^2 of the whole tensor, or < 0 to have the ranks sum
+ * the exact squares of their uploaded blocks on the device (all-reduced over
+ * the grid; the blocks partition X). Collective when < 0. Replaces
+ * dist_rescal.py:138-140 (_global_sum of _local_sq_norm). */
 int rk_upload_block(rk_handle* h, const void* x, int32_t dtype, int64_t rows, int64_t cols,
                     double sq_norm_global);
 

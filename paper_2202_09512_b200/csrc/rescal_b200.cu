@@ -1954,8 +1954,10 @@ int rk_upload_block(rk_handle* h, const void* x, int32_t dtype, int64_t rows, in
       upload_rows(h, static_cast<const float*>(x), rows, cols);
     else
       upload_rows(h, static_cast<const double*>(x), rows, cols);
-    finish_upload_norm(h, false);
-    h->norm2 = sq_norm_global;
+    // sq_norm_global < 0: the ranks' exact device sums of squares (all-reduced)
+    const bool dev_norm = sq_norm_global < 0.0;
+    finish_upload_norm(h, dev_norm);
+    if (!dev_norm) h->norm2 = sq_norm_global;
     h->have_x = true;
     h->perturbed = false;
     drop_base_copies(h);

@@ -357,20 +357,11 @@ def dist_rescal_solve(xblock, k: int, cfg: SolverConfig | None = None, ctx: Grid
         blk = src.block(lay)
         if src.sparse and not sparse:  # k > 32: the dense engine on the densified block
             blk = np.stack([np.asarray(s.toarray()) for s in blk])
-        if sparse:
-            if cfg.track_error and src.sq_norm is None:
-                local = sum(float(np.sum(np.asarray(s.data, dtype=np.float64) ** 2)) for s in blk)
-                if _sum_over_ranks(dist, local) == 0.0:
-                    raise DataError("cannot track relative error: tensor norm is zero")
+        if sparse:  # the CSR upload sums ||X||^2 on the device (all-reduced over the grid)
             eng.upload_csr(blk)
         else:
-            if src.sq_norm is not None:
-                sq = float(src.sq_norm)
-            else:
-                sq = _sum_over_ranks(dist, float(np.sum(np.asarray(blk, dtype=np.float64) ** 2)))
-            if cfg.track_error and sq == 0.0:
-                raise DataError("cannot track relative error: tensor norm is zero")
-            eng.upload_block(blk, sq)
+            # no norm given: the ranks sum their blocks' squares on the device
+            eng.upload_block(blk, float(src.sq_norm) if src.sq_norm is not None else -1.0)
         del blk
         eng.set_factors(f0.A.astype(dt).astype(np.float64), f0.R.astype(dt).astype(np.float64))
         _, trace = eng.run(cfg.max_iters, float(dt.type(cfg.epsilon)), cfg.track_error, cfg.tolerance)

@@ -22,7 +22,6 @@ for n, m, k in ((256, 3, 16), (384, 2, 32), (1664, 2, 32)):
     eng = _lib.Engine(n, m, k)
     eng.upload(x.slices)
     eng.set_factors(f.A, f.R)
-    eng.set_option(5, 0)  # separate k2 kernels too
     eng.run(3, 1e-16, track_error=True)
     eng.update_r(1e-16)
     eng.update_a(1e-16)
