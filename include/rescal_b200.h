@@ -190,6 +190,16 @@ int rk_positive_mean(rk_handle* h, double* mean);
  * cudaMalloc). This returns every cached block to the driver. */
 void rk_release_cached_memory(void);
 
+/* Diagnostics (the GPU pool has no compute-sanitizer): with guards on, every
+ * device block allocated afterwards is followed by a 64 KB band of a fixed
+ * byte pattern; rk_debug_check_guards reports how many band bytes of live
+ * and already-freed guarded blocks were overwritten (0 = no out-of-bounds
+ * write past any buffer end). Engine-private; no reference counterpart. */
+int rk_debug_guards(int32_t on);
+int rk_debug_check_guards(int64_t* damaged_bytes, int64_t* blocks_checked);
+/* Positive control: allocate 1000 bytes, write nbytes past the end, free. */
+int rk_debug_overrun(int64_t nbytes);
+
 /* Raw PCG64 draws u_{offset} .. u_{offset+count-1} (tests of the generator). */
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,
                    int64_t count, double* out);

@@ -94,6 +94,9 @@ SIGNATURES = {
     "rk_csr_copy": (ctypes.c_int, [_vp, _pi64, ctypes.POINTER(ctypes.c_int32), _pf]),
     "rk_fill_sparse_uniform": (ctypes.c_int, [_vp, _u64, _i64]),
     "rk_nnz": (ctypes.c_int, [_vp, _pi64]),
+    "rk_debug_guards": (ctypes.c_int, [_i32]),
+    "rk_debug_check_guards": (ctypes.c_int, [_pi64, _pi64]),
+    "rk_debug_overrun": (ctypes.c_int, [_i64]),
 }
 
 _LIB = None
@@ -437,6 +440,18 @@ def perturb_csr_values(entropy, delta, t: int, n: int, indptr, indices, values: 
                                        RK_F32 if values.dtype == np.float32 else RK_F64, int(t), int(n),
                                        ip.ctypes.data_as(_pi64), ix.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                        values.ctypes.data, int(values.size)))
+
+
+def debug_guards(on: bool) -> None:
+    """Guard bands after every later device allocation (diagnostics)."""
+    check(load().rk_debug_guards(1 if on else 0))
+
+
+def debug_check_guards():
+    """(overwritten guard bytes, guarded blocks live) -- 0 damaged = no overrun."""
+    bad, n = _i64(0), _i64(0)
+    check(load().rk_debug_check_guards(ctypes.byref(bad), ctypes.byref(n)))
+    return int(bad.value), int(n.value)
 
 
 def release_cached_memory() -> None:

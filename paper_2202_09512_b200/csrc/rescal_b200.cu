@@ -96,7 +96,15 @@ struct DevPool {
   std::mutex mu;
   std::unordered_map<void*, std::pair<int, size_t>> live;  // ptr -> (device, bytes)
   std::multimap<std::pair<int, size_t>, void*> idle;        // (device, bytes) -> ptr
+  // guard mode (rk_debug_guards; compute-sanitizer is not available on the
+  // GPU pool): every new block is followed by kGuard bytes of a fixed
+  // pattern, checked on free and by rk_debug_check_guards
+  bool guard = false;
+  std::unordered_map<void*, size_t> guarded;  // ptr -> requested bytes (guard starts there)
+  int64_t violations = 0;
 };
+constexpr size_t kGuard = 64 << 10;
+constexpr unsigned char kGuardByte = 0xA5;
 
 DevPool& dev_pool() {
   static DevPool* p = new DevPool();  // process lifetime (no teardown-order hazards)
@@ -124,11 +132,34 @@ void pool_release(int dev) {
   cudaSetDevice(cur);
 }
 
+// bytes of the guard band of block p that lost the pattern (caller holds mu)
+int64_t guard_damage(void* p, size_t req, int dev) {
+  std::vector<unsigned char> g(kGuard);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  cudaDeviceSynchronize();
+  cudaMemcpy(g.data(), static_cast<unsigned char*>(p) + req, kGuard, cudaMemcpyDeviceToHost);
+  cudaSetDevice(cur);
+  int64_t bad = 0;
+  for (unsigned char c : g) bad += c != kGuardByte;
+  return bad;
+}
+
 void* pool_alloc(size_t bytes) {
   DevPool& P = dev_pool();
   int dev = 0;
   RK_CUDA(cudaGetDevice(&dev));
   const size_t b = pool_class(bytes);
+  if (P.guard) {  // no reuse: a fresh block with the guard band right after the request
+    void* p = nullptr;
+    RK_CUDA(cudaMalloc(&p, bytes + kGuard));
+    RK_CUDA(cudaMemset(static_cast<unsigned char*>(p) + bytes, kGuardByte, kGuard));
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.live[p] = {dev, bytes};
+    P.guarded[p] = bytes;
+    return p;
+  }
   {
     std::lock_guard<std::mutex> lk(P.mu);
     // best fit within 12.5 % of the request
@@ -171,6 +202,14 @@ void dfree(void* p) {
   std::lock_guard<std::mutex> lk(P.mu);
   auto it = P.live.find(p);
   if (it == P.live.end()) {  // not from dalloc
+    cudaFree(p);
+    return;
+  }
+  auto g = P.guarded.find(p);
+  if (g != P.guarded.end()) {  // guard mode: check the band, give the block back to the driver
+    P.violations += guard_damage(p, g->second, it->second.first);
+    P.guarded.erase(g);
+    P.live.erase(it);
     cudaFree(p);
     return;
   }
@@ -2591,6 +2630,38 @@ int rk_positive_mean(rk_handle* h, double* mean) {
 }
 
 void rk_release_cached_memory(void) { pool_release(-1); }
+
+int rk_debug_guards(int32_t on) {
+  return guarded([&] {
+    pool_release(-1);  // later allocations come fresh (guarded or pooled)
+    DevPool& P = dev_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.guard = on != 0;
+  });
+}
+
+// positive control for the guard check: a 1000-byte block, then `nbytes`
+// bytes written right after its end (a deliberate overrun), then freed
+int rk_debug_overrun(int64_t nbytes) {
+  return guarded([&] {
+    RK_REQUIRE(nbytes >= 0 && nbytes <= (int64_t)kGuard, RK_ERR_DATA, "bad overrun size");
+    unsigned char* p = dalloc<unsigned char>(1000);
+    if (nbytes) RK_CUDA(cudaMemset(p + 1000, 0, (size_t)nbytes));
+    RK_CUDA(cudaDeviceSynchronize());
+    dfree(p);
+  });
+}
+
+int rk_debug_check_guards(int64_t* damaged_bytes, int64_t* blocks_checked) {
+  return guarded([&] {
+    DevPool& P = dev_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    int64_t bad = P.violations;
+    for (auto& kv : P.guarded) bad += guard_damage(kv.first, kv.second, P.live[kv.first].first);
+    if (damaged_bytes) *damaged_bytes = bad;
+    if (blocks_checked) *blocks_checked = (int64_t)P.guarded.size();
+  });
+}
 
 int rk_nccl_unique_id(void* out128) {
   return guarded([&] {
