@@ -547,6 +547,25 @@ def run_ours(args, dist, rank, world, local_rank):
                            "nnz": dd["nnz"] if "density" in cc else None}
             except Exception as exc:
                 sec[nm] = {"error": repr(exc)[:300]}
+        try:  # cfg5: the public rescalk() on k = 15..16 of the sweep (20 members x 200 iterations)
+            import paper_2202_09512_b200 as rk
+
+            c5 = CONFIGS["cfg5"]
+            xh = host_tensor(c5["m"], c5["n"], pinned=True)
+            x5 = rk.RelTensor(xh)
+            t0 = time.perf_counter()
+            rep = rk.rescalk(x5, c5["k_min"], c5["k_max"], c5["r"], cfg=rk.SolverConfig(max_iters=c5["iters"],
+                                                                                        device=local_rank),
+                             pcfg=rk.PerturbConfig(delta=0.02, base_seed=0))
+            secs = time.perf_counter() - t0
+            units5 = (c5["k_max"] - c5["k_min"] + 1) * c5["r"] * c5["iters"]
+            sec["cfg5"] = {"workload": f"cfg5: rescalk dense m={c5['m']} n={c5['n']} k={c5['k_min']}..{c5['k_max']} "
+                                       f"r={c5['r']} iters={c5['iters']} (public API, host tensor, incl. upload, "
+                                       "resampling, clustering, refit)",
+                           "value": units5 / secs, "unit": "member-it/s", "seconds": secs, "k_opt": rep.k_opt}
+            del x5, xh
+        except Exception as exc:
+            sec["cfg5"] = {"error": repr(exc)[:300]}
         line["secondary"] = sec
 
     # ---------------- CPU baseline (rank 0, N=1 only) -----------------------
