@@ -652,6 +652,7 @@ def e2e_leg(args, dist, rank, world, local_rank, units):
         t0 = time.perf_counter()
         f, tr, info = rk.solve_on_grid(src, k, cfg(args.steps), initial=f0)
         e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
+        phases = {kk: vv for kk, vv in info.timing.items() if kk.endswith("_s")}
         h2d = blk.nbytes + f0.A.nbytes + f0.R.nbytes
         d2h = f.A.nbytes + f.R.nbytes
         api = ("solve_on_grid(BlockSource(pinned fp32 host block of this rank), k, "

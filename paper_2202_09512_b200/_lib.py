@@ -151,6 +151,7 @@ class Engine:
             device = int(os.environ.get("LOCAL_RANK", "0"))
         self.n, self.m, self.k = int(n), int(m), int(k)
         self.sparse = bool(sparse)
+        self.device = int(device)
         self._h = _vp()
         if self.sparse:
             check(lib.rk_create_sparse(int(device), self.n, self.m, self.k, ctypes.byref(self._h)))

@@ -33,6 +33,7 @@ Launch with ``torchrun --nproc-per-node N`` (``--master-addr 127.0.0.1``).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -299,6 +300,43 @@ def _sum_over_ranks(dist, value: float) -> float:
     return float(sum(out[r] for r in range(len(out))))  # rank order: identical on every rank
 
 
+# One idle grid engine per process, kept for the next solve of the same
+# shape on the same grid: it owns the NCCL communicators and the mapped peer
+# arenas, whose setup (ncclCommInitRank + splits, CUDA IPC) costs seconds per
+# call. Kept while its tensor is <= 1/4 of the GPU's memory; dropped by
+# release_cached_memory().
+_GRID_CACHE = {}
+
+
+def _grid_key(n, m, k, pr, pc, cfg, sparse, rank):
+    return (n, m, k, pr, pc, cfg.device, cfg.engine, bool(sparse), rank)
+
+
+def release_grid_cache() -> None:
+    for eng, _ in list(_GRID_CACHE.values()):
+        eng.close()
+    _GRID_CACHE.clear()
+
+
+def _keep_grid_engine(key, eng, lay) -> bool:
+    try:
+        import torch
+
+        total = torch.cuda.get_device_properties(eng_device(eng)).total_memory
+    except Exception:  # noqa: BLE001
+        total = 180e9
+    dense = 4.0 * eng.m * lay["rows"] * lay["cols"]
+    if eng.sparse or dense > total / 4:
+        return False
+    release_grid_cache()
+    _GRID_CACHE[key] = (eng, lay)
+    return True
+
+
+def eng_device(eng) -> int:
+    return int(getattr(eng, "device", 0) or 0)
+
+
 def make_grid_engine(n, m, k, grid=None, cfg: SolverConfig | None = None, sparse=False):
     """Create this rank's engine (dense, or the CSR/CSC engine) and join the
     NCCL grid."""
@@ -351,10 +389,27 @@ def dist_rescal_solve(xblock, k: int, cfg: SolverConfig | None = None, ctx: Grid
     if f0.A.shape != (n, k) or f0.R.shape != (m, k, k):
         raise DataError("initial factors do not match tensor/k")
     sparse = src.sparse and k <= 32
-    eng, lay = make_grid_engine(n, m, k, grid, cfg, sparse=sparse)
+    t0 = time.perf_counter()
+    size = dist.get_world_size()
+    pr, pc = grid if grid is not None else grid_shape(size)
+    key = _grid_key(n, m, k, pr, pc, cfg, sparse, dist.get_rank())
+    cached = _GRID_CACHE.pop(key, None)
+    # every rank must agree on reusing (the engine's communicators are collective)
+    flags = [None] * size
+    dist.all_gather_object(flags, cached is not None)
+    if cached is not None and all(flags):
+        eng, lay = cached
+    else:
+        if cached is not None:
+            cached[0].close()
+        eng, lay = make_grid_engine(n, m, k, (pr, pc), cfg, sparse=sparse)
+    phases = {"create_s": time.perf_counter() - t0, "engine_reused": cached is not None and all(flags)}
     counters = ctx.counters if ctx is not None else None
     try:
+        t0 = time.perf_counter()
         blk = src.block(lay)
+        phases["block_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
         if src.sparse and not sparse:  # k > 32: the dense engine on the densified block
             blk = np.stack([np.asarray(s.toarray()) for s in blk])
         if sparse:  # the CSR upload sums ||X||^2 on the device (all-reduced over the grid)
@@ -363,12 +418,20 @@ def dist_rescal_solve(xblock, k: int, cfg: SolverConfig | None = None, ctx: Grid
             # no norm given: the ranks sum their blocks' squares on the device
             eng.upload_block(blk, float(src.sq_norm) if src.sq_norm is not None else -1.0)
         del blk
+        phases["upload_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
         eng.set_factors(f0.A.astype(dt).astype(np.float64), f0.R.astype(dt).astype(np.float64))
         _, trace = eng.run(cfg.max_iters, float(dt.type(cfg.epsilon)), cfg.track_error, cfg.tolerance)
+        phases["run_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
         a, r = eng.get_factors()
-        timing = eng.timing()
+        phases["get_factors_s"] = time.perf_counter() - t0
+        timing = dict(eng.timing(), **phases)
         exchange = "peer" if eng.info().get("peer_exchange") else "nccl"
-    finally:
+    except BaseException:
+        eng.close()
+        raise
+    if not _keep_grid_engine(key, eng, lay):
         eng.close()
     if counters is not None:
         counters.add_time("device_run", timing["run_ms"] / 1e3)
@@ -470,5 +533,7 @@ def solve_on_grid(x, k: int, cfg: SolverConfig | None = None, p: int | None = No
     ctx = GridContext(p=size, pr=pr, pc=pc, i=rank // pc, j=rank % pc,
                       counters=KernelCounters() if with_counters else None)
     df, trace = dist_rescal_solve(x, k, cfg, ctx, initial=initial, grid=(pr, pc))
+    t0 = time.perf_counter()
     factors = gather_factors(df, ctx)
+    ctx.timing["gather_s"] = time.perf_counter() - t0
     return factors, trace, ctx

@@ -196,11 +196,15 @@ def _release_engine(eng) -> None:
 
 
 def release_cached_memory() -> None:
-    """Close the kept engine and return the device allocator's cached blocks."""
+    """Close the kept engines (this thread's single-GPU engine, the process's
+    grid engine) and return the device allocator's cached blocks."""
     old = getattr(_CACHE, "entry", None)
     _CACHE.entry = None
     if old is not None:
         old[1].close()
+    from .multigpu import release_grid_cache
+
+    release_grid_cache()
     _lib.release_cached_memory()
 
 
