@@ -33,10 +33,6 @@ constexpr int kStages = 2;
 constexpr int kTile = 128;
 constexpr int kThreads = 192;
 constexpr uint32_t kXBox = 128 * 64 * 2;  // one 128-row x 64-col bf16 box = 16 KB
-#ifndef RK_EPI_SUSPEND_NS
-#define RK_EPI_SUSPEND_NS 0x100000
-#endif
-constexpr uint32_t kEpiSuspendNs = RK_EPI_SUSPEND_NS;  // try_wait suspend-time hint of the epilogue waits
 
 struct K1Args {
   int NR, NC, K, M;
@@ -81,28 +77,6 @@ RK_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
       "DONE_%=:\n"
       "}\n" ::"r"(bar),
       "r"(parity)
-      : "memory");
-}
-
-// Same, for waits that are long by design (the epilogue warps wait a whole
-// item for their accumulator): try_wait with a suspend-time hint parks the
-// warp instead of spinning, which frees issue slots and power for the
-// producer / MMA warps under the power cap.
-RK_DEV void mbar_wait_sleepy(uint32_t bar, uint32_t parity) {
-#ifdef RK_EPI_SPIN  // A/B builds only
-  mbar_wait(bar, parity);
-  return;
-#endif
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@P1 bra DONE_%=;\n"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity), "r"(kEpiSuspendNs)
       : "memory");
 }
 
@@ -459,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int idx = item - item_b;
       const int pb = idx & 1;
       const uint32_t pp = (idx >> 1) & 1;
-      mbar_wait_sleepy(smem_u32(&p_full[pb]), pp);
+      mbar_wait(smem_u32(&p_full[pb]), pp);
       tc_fence_after();
       float v[K];
 #pragma unroll
@@ -481,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int h = 0; h < K / 4; ++h) dst[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
       if (last_in_seg) {
-        mbar_wait_sleepy(smem_u32(q_full), qf_phase);
+        mbar_wait(smem_u32(q_full), qf_phase);
         qf_phase ^= 1;
         tc_fence_after();
         float* qdst = args.Qpart + (size_t)slot * c * kTile * K;
