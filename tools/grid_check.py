@@ -40,6 +40,32 @@ for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "aut
         results.append(dict(n=n, m=m, k=k, iters=iters, engine=engine, grid=[info["pr"], info["pc"]],
                             exchange=info.get("exchange"),
                             relA=rel_a, relR=rel_r, dErr=derr, R_replicated=same_r, ok=good))
+# the same solve again (the kept grid engine is reused: no NCCL / IPC setup),
+# and from a memory-mapped RSK1 file through BlockSource.from_file: the
+# factors must be byte-identical to the first solve of the list
+import tempfile
+n, m, k, iters = 1000, 2, 16, 20
+x = np.random.default_rng(n).random((m, n, n), dtype=np.float32).astype(np.float64)
+f0 = rk.random_init(n, k, m, 1)
+ref, _, _ = rk.solve_on_grid(rk.RelTensor(x), k, rk.SolverConfig(max_iters=iters), initial=f0, grid=GRID)
+again, _, ctx2 = rk.solve_on_grid(rk.RelTensor(x), k, rk.SolverConfig(max_iters=iters), initial=f0, grid=GRID)
+path = os.path.join(tempfile.gettempdir(), f"grid_check_{os.getpid() if rank == 0 else 0}.rsk")
+paths = [None] * world
+dist.all_gather_object(paths, path)
+if rank == 0:
+    rk.save_tensor(rk.RelTensor(x), paths[0])
+dist.barrier()
+ff, _, _ = rk.solve_on_grid(rk.BlockSource.from_file(paths[0]), k, rk.SolverConfig(max_iters=iters), initial=f0,
+                            grid=GRID)
+dist.barrier()
+if rank == 0:
+    os.remove(paths[0])
+    good = (np.array_equal(again.A, ref.A) and np.array_equal(again.R, ref.R) and np.array_equal(ff.A, ref.A)
+            and np.array_equal(ff.R, ref.R) and bool(ctx2.timing.get("engine_reused")))
+    ok = ok and good
+    results.append(dict(n=n, m=m, k=k, iters=iters, engine="reuse+file", exchange=ctx2.exchange,
+                        reused=bool(ctx2.timing.get("engine_reused")),
+                        grid=[ctx2.pr, ctx2.pc], ok=good))
 # sparse CSR/CSC grid engine
 import scipy.sparse as sp
 for (n, m, k, dens, iters) in [(600, 2, 8, 0.02, 20), (1000, 3, 16, 0.01, 15), (555, 2, 32, 0.03, 10)]:
