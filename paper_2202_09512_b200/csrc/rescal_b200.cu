@@ -864,7 +864,12 @@ void launch_k5(rk_handle* h, int gate) {
   h->launches += 1;
 }
 
-void launch_k2a(rk_handle* h, int skip) {
+// One GPU, tensor-core G / S (dense K in {16, 32}, sparse K = 16): k2f sums
+// the chunk partials itself (one launch less per iteration); regress_r and
+// the grid all-reduce need the reduced [G, S_t] in `red` first.
+bool k2f_reduces(const rk_handle* h) { return !h->grid() && h->gpart && (h->K == 16 || !h->sparse); }
+
+void launch_k2a(rk_handle* h, int skip, bool for_k2f = true) {
   const int K = h->K;
   if (h->sparse && (!h->grid() || K == 16)) {
     // G = A^T A, S_t = A^T P_t streamed from the stored P (sparse.cuh sp_gram);
@@ -882,10 +887,13 @@ void launch_k2a(rk_handle* h, int skip) {
     else
       rk::sp::sp_gram<32><<<grid, 256, rk::sp::SpGramCfg<32>::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip);
-    rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
-                                                                        h->red, skip);
+    if (!(for_k2f && k2f_reduces(h) && K == 16)) {
+      rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
+                                                                          h->red, skip);
+      h->launches += 1;
+    }
     RK_CUDA(cudaGetLastError());
-    h->launches += 2;
+    h->launches += 1;
     return;
   }
   if (dense_gram_tc(h) && h->gpart) {
@@ -900,10 +908,13 @@ void launch_k2a(rk_handle* h, int skip) {
       rk::sp::sp_gram_tc_k<32><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
           h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
           nown);
-    rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
-                                                                        h->red, skip);
+    if (!(for_k2f && k2f_reduces(h))) {
+      rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
+                                                                          h->red, skip);
+      h->launches += 1;
+    }
     RK_CUDA(cudaGetLastError());
-    h->launches += 2;
+    h->launches += 1;
     return;
   }
   if (h->fast || (h->grid() && (K == 16 || K == 32))) {
@@ -968,15 +979,18 @@ void launch_k2f(rk_handle* h, int mode) {
   const int len = (int)((h->m + 1) * K * K);
   const double* rres = h->grid() ? h->red + len : h->rpart;
   const int nres = h->grid() ? 1 : h->nr;
+  // after a launch_k2a(for_k2f) on a one-GPU tensor-core G / S path the
+  // chunk partials are still unreduced: k2f sums them
+  const double* gpart = k2f_reduces(h) ? h->gpart : nullptr;
   if (!h->gscratch && (K == 16 || K == 32)) {
     auto kern = K == 16 ? rk::k2f_fused_t<16> : rk::k2f_fused_t<32>;
-    launch_pdl(kern, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
-               (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, (int)h->m,
-               h->eps, mode, h->counters + h->m + 1, h->W32);
+    launch_pdl(kern, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl, h->red, h->R,
+               h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, (int)h->m, h->eps, mode,
+               h->counters + h->m + 1, h->W32, gpart, h->gchunks);
   } else {
-    launch_pdl(rk::k2f_fused, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl,
-               (const double*)h->red, h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K,
-               (int)h->m, h->eps, mode, h->gscratch, h->counters + h->m + 1, h->W32);
+    launch_pdl(rk::k2f_fused, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl, h->red,
+               h->R, h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, K, (int)h->m, h->eps, mode,
+               h->gscratch, h->counters + h->m + 1, h->W32, gpart, h->gchunks);
   }
   RK_CUDA(cudaGetLastError());
   h->launches += 1;
@@ -1416,7 +1430,7 @@ void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iter
   const int K = h->K;
   reset_ctl(h, 0, -1.0, 0);
   launch_k1(h, false);
-  launch_k2a(h, 0);
+  launch_k2a(h, 0, false);
   if (h->grid()) grid_allreduce_parts(h, false);
   rk::regress_loop<<<1, 1024, 0, h->stream>>>(h->red, 1, h->R, h->regS, h->regG, h->regT, h->regRn,
                                              K, (int)h->m, eps, max_iters, tol, h->d_iters);

@@ -326,34 +326,58 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
 }
 
 
-__global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl, const double* __restrict__ gs,
+// gpart != nullptr: the chunk partials of [G, S_1..S_m] (sp_gram_tc_k) are
+// summed here (sp_gram_reduce's order, bit-identical) instead of by a
+// separate launch: block t forms G in its scratch and S_t into its own slot
+// of gs (block 0 also writes G's slot).
+RK_DEV const double* k2f_reduce_parts(const double* __restrict__ gpart, int gchunks, double* __restrict__ gs,
+                                      double* Gdst, int KK, int t) {
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    const double g = sum_chunks(gpart + e, gchunks, KK);
+    Gdst[e] = g;
+    if (t == 0) gs[e] = g;
+    gs[(size_t)(1 + t) * KK + e] = sum_chunks(gpart + (size_t)(1 + t) * gchunks * KK + e, gchunks, KK);
+  }
+  __syncthreads();
+  return Gdst;
+}
+
+__global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl, double* __restrict__ gs,
                                                       double* __restrict__ R, double* __restrict__ Rnext,
                                                       double* __restrict__ Mt, double* __restrict__ Mout,
                                                       double* __restrict__ tt, const double* __restrict__ rres,
                                                       int nres, double* __restrict__ trace, int K, int M,
                                                       double eps, int mode, double* gscratch,
-                                                      unsigned* __restrict__ counter, float* __restrict__ W32) {
+                                                      unsigned* __restrict__ counter, float* __restrict__ W32,
+                                                      const double* __restrict__ gpart, int gchunks) {
   pdl_entry();
   if (ctl->stop) return;
   extern __shared__ double sh[];
-  k2f_body<0>(ctl, gs, gs + (size_t)(1 + blockIdx.x) * K * K, R, Rnext, Mt, Mout, tt, rres, nres, trace, K, M, eps, mode, gscratch, counter, W32, sh,
-              blockIdx.x);
+  const int t = blockIdx.x, KK = K * K;
+  const double* G = gpart ? k2f_reduce_parts(gpart, gchunks, gs, gscratch ? gscratch + (size_t)t * 5 * KK : sh, KK, t)
+                          : gs;
+  k2f_body<0>(ctl, G, gs + (size_t)(1 + t) * KK, R, Rnext, Mt, Mout, tt, rres, nres, trace, K, M, eps, mode,
+              gscratch, counter, W32, sh, t);
 }
 
 // k2f_fused with compile-time K (16 or 32; shared-memory scratch only)
 template <int KT>
-__global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, const double* __restrict__ gs,
+__global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, double* __restrict__ gs,
                                                         double* __restrict__ R, double* __restrict__ Rnext,
                                                         double* __restrict__ Mt, double* __restrict__ Mout,
                                                         double* __restrict__ tt, const double* __restrict__ rres,
                                                         int nres, double* __restrict__ trace, int M, double eps,
                                                         int mode, unsigned* __restrict__ counter,
-                                                        float* __restrict__ W32) {
+                                                        float* __restrict__ W32, const double* __restrict__ gpart,
+                                                        int gchunks) {
   pdl_entry();
   if (ctl->stop) return;
   extern __shared__ double sh[];
-  k2f_body<KT>(ctl, gs, gs + (size_t)(1 + blockIdx.x) * KT * KT, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode, nullptr, counter, W32, sh,
-               blockIdx.x);
+  const int t = blockIdx.x;
+  constexpr int KK = KT * KT;
+  const double* G = gpart ? k2f_reduce_parts(gpart, gchunks, gs, sh, KK, t) : gs;
+  k2f_body<KT>(ctl, G, gs + (size_t)(1 + t) * KK, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode,
+               nullptr, counter, W32, sh, t);
 }
 
 // K2b (v2): A update. Every core is staged once in shared memory as fp32

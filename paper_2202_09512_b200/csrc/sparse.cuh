@@ -442,23 +442,6 @@ __global__ void __launch_bounds__(256, RK_SG_CPS) sp_gram_tc_k(const Ctl* __rest
   sp_gram_tc_body<KT>(A32, P, n, ldp, M, nchunk, part, Aown, nown, blockIdx.x, gridDim.x, gts);
 }
 
-// sum_{c < nchunk} p[c * stride], added in chunk order; the loads go out
-// eight at a time (independent, in flight together) instead of one chained
-// L2 round trip per chunk (cfg3: 64 chunks).
-RK_DEV double sum_chunks(const double* __restrict__ p, int nchunk, int stride) {
-  double v = 0.0;
-  int c = 0;
-  for (; c + 8 <= nchunk; c += 8) {
-    double x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = __ldcg(p + (size_t)(c + u) * stride);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v += x[u];
-  }
-  for (; c < nchunk; ++c) v += __ldcg(p + (size_t)c * stride);
-  return v;
-}
-
 __global__ void __launch_bounds__(256) sp_gram_reduce(const Ctl* __restrict__ ctl,
                                                       const double* __restrict__ part, int nchunk,
                                                       int KK, double* __restrict__ gs,
