@@ -423,13 +423,18 @@ void plan_tc(rk_handle* h) {
   const int qw = K == 16 ? rk::tc::K1Cfg<16, true>::kQW
                          : (h->k1_mq ? rk::tc::K1Cfg<32, true>::kQW : rk::tc::K1Cfg<32, false>::kQW);
   const int cmax = (512 - 2 * pw) / qw;  // TMEM columns: c Q accumulators + 2 P buffers
+  const int M = (int)h->m;
   int c = std::min(cmax, ncb);
+  // small tensors (cfg1: 2 x 2 tiles per slice) have fewer items than SMs:
+  // narrower strips spread the tiles over more CTAs (each CTA's K1 latency is
+  // TMEM alloc + one TMA round trip + its MMAs), at the price of a few more
+  // (tiny) P partials
+  while (c > 1 && (int64_t)M * ((ncb + c - 1) / c) * nrb < h->num_sms) c = (c + 1) / 2;
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
   nstrips = (ncb + c - 1) / c;
   h->c = c;
   h->nstrips = nstrips;
-  const int M = (int)h->m;
   const int64_t n_items = (int64_t)M * nstrips * nrb;
   auto tiles_of = [&](int64_t item) {
     int s = (int)((item / nrb) % nstrips);
