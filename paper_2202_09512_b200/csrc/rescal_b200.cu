@@ -635,7 +635,8 @@ void alloc_factor_buffers(rk_handle* h) {
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
     const int rb = rk::k2b_v4_rb(K, h->NR);
     const int tg = rk::k2b_v4_tg(K, (int)M, h->NR);
-    const int smem = tg * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
+    const int smem = rk::kK2bStages * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
+    (void)tg;
     if (K == 16)
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     else if (rk::k2b_v4_rpt(K, h->NR) == 8)
@@ -1057,7 +1058,7 @@ void launch_k2b(rk_handle* h) {
   if (h->fast) {
     const int rb = rk::k2b_v4_rb(K, h->NR);
     const int tg = rk::k2b_v4_tg(K, (int)h->m, h->NR);
-    const size_t smem = (size_t)tg * (2 * K * K + 2 * rb * K) * sizeof(float);
+    const size_t smem = (size_t)rk::kK2bStages * (2 * K * K + 2 * rb * K) * sizeof(float);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
     if (K == 16)
       launch_pdl(rk::k2b_v4<16, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,

@@ -637,73 +637,70 @@ RK_DEV T ld_pq(const T* p, bool coh) {
   return coh ? __ldcg(p) : __ldg(p);
 }
 
+// Per slice t the block stages W_t = [R_t^T ; R_t] (fp32, 2K^2) and its RB
+// rows of P_t and Q_t (2 RB K floats) into one of kK2bStages shared-memory
+// stages with cp.async, kK2bStages - 1 slices ahead of the one it computes
+// (the loads of later slices overlap the FMAs of this one). The arithmetic --
+// per slice an fp32 sum over the 2K terms, added to fp64 per slice in slice
+// order -- does not depend on the staging.
+constexpr int kK2bStages = 3;
+
+template <int K, int RPT>
+__host__ __device__ constexpr int k2b_v4_stage_floats() {
+  return 2 * K * K + 2 * RPT * (256 / K) * K;
+}
+
+RK_DEV void k2b_cp16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
 template <int K, int RPT, bool COH = false>
 RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float* __restrict__ A32,
                          __nv_bfloat16* __restrict__ ATh, __nv_bfloat16* __restrict__ ATl,
                          const float* __restrict__ P, const float* __restrict__ Q, const float* __restrict__ W32,
                          const double* __restrict__ Mm, int N, int M, int tg, double eps_m, int rbi, float* shf) {
   static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
+  (void)tg;
   constexpr int TR = 256 / K;   // thread rows
   constexpr int RB = RPT * TR;  // rows per block
   constexpr int K4 = K / 4;
-  float* Ws = shf;                                   // [tg][2][K][K]
-  float* PQs = shf + (size_t)tg * 2 * K * K;         // [tg][2][RB][K]
+  constexpr int SF = k2b_v4_stage_floats<K, RPT>();  // [2][K][K] W, then [2][RB][K] P / Q rows
   const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
   const int rbase = rbi * RB;
+  auto issue = [&](int t) {
+    float* st = shf + (size_t)(t % kK2bStages) * SF;
+    const float* w = W32 + (size_t)t * 2 * K * K;
+    for (int e = threadIdx.x; e < 2 * K * K / 4; e += blockDim.x) k2b_cp16(st + 4 * e, w + 4 * e);
+    float* pq = st + 2 * K * K;
+    for (int e = threadIdx.x; e < 2 * RB * K4; e += blockDim.x) {
+      const int which = e / (RB * K4), rem = e - which * RB * K4;
+      const int r = rem / K4, qq = rem - r * K4;
+      const int row = min(rbase + r, N - 1);  // N is a multiple of RB on the dense engine
+      k2b_cp16(pq + 4 * e, (which ? Q : P) + ((size_t)t * N + row) * K + 4 * qq);
+    }
+  };
   double nacc[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) nacc[j] = 0.0;
-  for (int tb = 0; tb < M; tb += tg) {
-    const int nt = min(tg, M - tb);
+  __syncthreads();  // the previous row block's stages are consumed
+#pragma unroll
+  for (int t = 0; t < kK2bStages - 1; ++t) {
+    if (t < M) issue(t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int t = 0; t < M; ++t) {
+    if (t + kK2bStages - 1 < M) issue(t + kK2bStages - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kK2bStages - 1) : "memory");
     __syncthreads();
+    const float* WrT = shf + (size_t)(t % kK2bStages) * SF;  // [d][c] = R_t[c][d]
+    const float* Wr = WrT + K * K;                           // [d][c] = R_t[d][c]
+    const float* pr = WrT + 2 * K * K + (size_t)rl * K;      // row rl + j*TR at + j*TR*K
+    const float* qr = pr + (size_t)RB * K;
     {
-      const float4* src = reinterpret_cast<const float4*>(W32 + (size_t)tb * 2 * K * K);
-      float4* dst = reinterpret_cast<float4*>(Ws);
-      const int nw = nt * 2 * K * K / 4;
-      for (int e0 = threadIdx.x; e0 < nw; e0 += 4 * blockDim.x) {
-        float4 v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = e0 + q * blockDim.x;
-          v[q] = e < nw ? ld_pq(src + e, COH) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = e0 + q * blockDim.x;
-          if (e < nw) dst[e] = v[q];
-        }
-      }
-      float4* pq = reinterpret_cast<float4*>(PQs);
-      const int npq = nt * 2 * RB * K4;
-      for (int e0 = threadIdx.x; e0 < npq; e0 += 8 * blockDim.x) {
-        float4 v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = e0 + q * blockDim.x;
-          v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (e < npq) {
-            const int u = e / (2 * RB * K4), rem = e - u * 2 * RB * K4;
-            const int which = rem / (RB * K4), rem2 = rem - which * RB * K4;
-            const int r = rem2 / K4, qq = rem2 - r * K4;
-            const int row = rbase + r;
-            if (row < N)
-              v[q] = ld_pq(reinterpret_cast<const float4*>((which ? Q : P) + ((size_t)(tb + u) * N + row) * K) + qq,
-                           COH);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = e0 + q * blockDim.x;
-          if (e < npq) pq[e] = v[q];
-        }
-      }
-    }
-    __syncthreads();
-    for (int u = 0; u < nt; ++u) {
-      const float* WrT = Ws + (size_t)u * 2 * K * K;  // [d][c] = R_t[c][d]
-      const float* Wr = WrT + K * K;                  // [d][c] = R_t[d][c]
-      const float* pr = PQs + ((size_t)u * 2 * RB + rl) * K;       // row rl + j*TR at + j*TR*K
-      const float* qr = PQs + ((size_t)u * 2 * RB + RB + rl) * K;
       float sacc[RPT];
 #pragma unroll
       for (int j = 0; j < RPT; ++j) sacc[j] = 0.f;
@@ -728,7 +725,9 @@ RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float*
 #pragma unroll
       for (int j = 0; j < RPT; ++j) nacc[j] += (double)sacc[j];
     }
+    __syncthreads();  // stage t % kK2bStages is refilled by a later iteration
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   double an[RPT];
   bool bad = false;
 #pragma unroll
