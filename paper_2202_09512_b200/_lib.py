@@ -385,10 +385,10 @@ class Engine:
         return ms.value
 
     def info(self):
-        out = np.zeros(11, dtype=np.int64)
-        check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 11))
+        out = np.zeros(12, dtype=np.int64)
+        check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 12))
         keys = ["engine", "n_pad", "k_pad", "strip_tiles", "ctas", "smem", "strips", "slots", "k2a_blocks", "nc_pad",
-                "peer_exchange"]
+                "peer_exchange", "k1_merge_q"]
         return dict(zip(keys, (int(v) for v in out)))
 
     @property

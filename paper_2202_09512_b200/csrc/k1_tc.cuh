@@ -29,7 +29,6 @@
 namespace rk {
 namespace tc {
 
-constexpr int kStages = 2;
 constexpr int kTile = 128;
 constexpr int kThreads = 192;
 constexpr uint32_t kXBox = 128 * 64 * 2;  // one 128-row x 64-col bf16 box = 16 KB
@@ -201,6 +200,18 @@ struct K1Cfg {
   static constexpr int kQW = kMergeQ ? 2 * K : K;  // TMEM columns per Q accumulator
 };
 
+// Split stages: each 128 x 128 tile arrives as two sub-stages (the X hi
+// plane with A_col's hi + lo boxes, then the X lo plane with A_col's hi
+// boxes), so the shared memory holds 4 (K = 32) / 5 (K = 16) of them instead
+// of 2 whole-tile stages: more bytes in flight per SM (round 2: cfg2 K1 0.976
+// -> 0.997 of HBM, cfg3 11.90 -> 11.60-11.69 ms; profiles/r02_k1_split_stages).
+template <int K>
+struct K1Stages {
+  static constexpr uint32_t kABox = K * 128;
+  static constexpr int kNSt = K == 32 ? 4 : 5;
+  static constexpr uint32_t kSubBytes = 2 * kXBox + 4 * kABox;
+};
+
 template <int K, bool MQ>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -217,8 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
   // A operand tiles hold the boxes as [hi b0][lo b0][hi b1][lo b1] so that
   // the hi and lo rows of one 64-column K chunk are contiguous (N = 2K view)
-  constexpr uint32_t kStageX = 4 * kXBox;          // Xh0 Xh1 Xl0 Xl1
-  constexpr uint32_t kStageBytes = kStageX + 4 * kABox;
+  // sub-stage: X0 X1 (one plane) | A_col boxes [hi b0][lo b0][hi b1][lo b1]
+  constexpr int kNSt = K1Stages<K>::kNSt;
+  constexpr uint32_t kStageX = 2 * kXBox;
+  constexpr uint32_t kStageBytes = K1Stages<K>::kSubBytes;
   constexpr uint32_t kAIBytes = 4 * kABox;
 
   if (args.skip_if_stopped && args.ctl->stop) return;
@@ -226,19 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (of the shared-window address) for SWIZZLE_128B atoms
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* stage_base = smem;                                  // kStages * kStageBytes
-  uint8_t* ai_base = smem + kStages * kStageBytes;             // 2 * kAIBytes
+  uint8_t* stage_base = smem;                                  // kNSt * kStageBytes
+  uint8_t* ai_base = smem + kNSt * kStageBytes;                // 2 * kAIBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(ai_base + 2 * kAIBytes);
   // barrier slots
-  uint64_t* full = bars;             // [kStages]
-  uint64_t* empty = bars + 2;        // [kStages]
-  uint64_t* ai_full = bars + 4;      // [2]
-  uint64_t* ai_empty = bars + 6;     // [2]
-  uint64_t* p_full = bars + 8;       // [2]
-  uint64_t* p_empty = bars + 10;     // [2]
-  uint64_t* q_full = bars + 12;      // [1]
-  uint64_t* q_empty = bars + 13;     // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* full = bars;                     // [kNSt]
+  uint64_t* empty = bars + kNSt;             // [kNSt]
+  uint64_t* ai_full = bars + 2 * kNSt;       // [2]
+  uint64_t* ai_empty = ai_full + 2;          // [2]
+  uint64_t* p_full = ai_full + 4;            // [2]
+  uint64_t* p_empty = ai_full + 6;           // [2]
+  uint64_t* q_full = ai_full + 8;            // [1]
+  uint64_t* q_empty = ai_full + 9;           // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ai_full + 10);
 
   const int warp = warp_id_uniform();
   const int lane = threadIdx.x & 31;
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nstrips = args.nstrips, nrb = args.nrb, ncb = args.ncb, c = args.c, NR = args.NR;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kNSt; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
       mbar_init(smem_u32(&empty[i]), 1);
     }
@@ -303,22 +316,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(ai + 3 * kABox, &map_rl, rb * kTile + 64, 0, aib);
         const int xrow = t * NR + rb * kTile;
         for (int cb = 0; cb < ct; ++cb) {
-          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
-          const uint32_t fb = smem_u32(&full[stage]);
-          mbar_expect_tx(fb, kStageBytes);
           const int j0 = (s * c + cb) * kTile;
-          tma_load_2d(st + 0 * kXBox, &map_xh, j0, xrow, fb);
-          tma_load_2d(st + 1 * kXBox, &map_xh, j0 + 64, xrow, fb);
-          tma_load_2d(st + 2 * kXBox, &map_xl, j0, xrow, fb);
-          tma_load_2d(st + 3 * kXBox, &map_xl, j0 + 64, xrow, fb);
-          tma_load_2d(st + kStageX + 0 * kABox, &map_ch, j0, 0, fb);
-          tma_load_2d(st + kStageX + 1 * kABox, &map_cl, j0, 0, fb);
-          tma_load_2d(st + kStageX + 2 * kABox, &map_ch, j0 + 64, 0, fb);
-          tma_load_2d(st + kStageX + 3 * kABox, &map_cl, j0 + 64, 0, fb);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {  // 0: X hi + A_col hi / lo, 1: X lo + A_col hi
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+            const uint32_t fb = smem_u32(&full[stage]);
+            const CUtensorMap* mx = sub ? &map_xl : &map_xh;
+            mbar_expect_tx(fb, 2 * kXBox + (sub ? 2 : 4) * kABox);
+            tma_load_2d(st + 0 * kXBox, mx, j0, xrow, fb);
+            tma_load_2d(st + 1 * kXBox, mx, j0 + 64, xrow, fb);
+            tma_load_2d(st + kStageX + 0 * kABox, &map_ch, j0, 0, fb);
+            tma_load_2d(st + kStageX + 2 * kABox, &map_ch, j0 + 64, 0, fb);
+            if (!sub) {
+              tma_load_2d(st + kStageX + 1 * kABox, &map_cl, j0, 0, fb);
+              tma_load_2d(st + kStageX + 3 * kABox, &map_cl, j0 + 64, 0, fb);
+            }
+            if (++stage == kNSt) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -359,53 +376,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ai = smem_u32(ai_base + ab * kAIBytes);
         const uint32_t p_tmem = tmem + (uint32_t)(c * kQW + pb * kPW);
         for (int cb = 0; cb < ct; ++cb) {
-          mbar_wait(smem_u32(&full[stage]), phase);
-          tc_fence_after();
-          const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
-          const uint32_t xh = st, xl = st + 2 * kXBox;
-          const uint32_t aj = st + kStageX;
           const uint32_t q_tmem = tmem + (uint32_t)(cb * kQW);
-          {
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {  // 0: the X hi plane's products, 1: the X lo plane's
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            const uint32_t st = smem_u32(stage_base + stage * kStageBytes);
+            const uint32_t aj = st + kStageX;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-              // ---- P: rows i (M=128), K-dim j: 16 columns at a time ----
               const uint32_t xoff = (ks >> 2) * kXBox + (ks & 3) * 32;
-              const uint32_t hoff = (ks >> 2) * 2 * kABox + (ks & 3) * 32;  // hi box of this chunk
-              const uint32_t loff = hoff + kABox;                            // lo box
-              const uint64_t dxh = umma_desc(xh + xoff, 16, 1024);
-              const uint64_t dxl = umma_desc(xl + xoff, 16, 1024);
+              const uint32_t hoff = (ks >> 2) * 2 * kABox + (ks & 3) * 32;
+              const uint32_t loff = hoff + kABox;
+              const uint64_t dx = umma_desc(st + xoff, 16, 1024);
               const uint64_t dah = umma_desc(aj + hoff, 16, 1024);
-              const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
-              // ---- Q: rows j (M=128, MN-major), K-dim i: 16 rows at a time ----
-              const uint32_t roff = ks * 16 * 128;
-              const uint64_t qxh = umma_desc(xh + roff, kXBox, 1024);
-              const uint64_t qxl = umma_desc(xl + roff, kXBox, 1024);
+              const uint64_t qx = umma_desc(st + ks * 16 * 128, kXBox, 1024);
               const uint64_t qah = umma_desc(ai + hoff, 16, 1024);
-              const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
               if (elect_one()) {
-                if (kMergeP) {
-                  tc_mma(p_tmem, dxh, dah, id_p2, accp);  // [Xh Ah | Xh Al], N = 2K
+                if (sub == 0) {
+                  const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
+                  const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
+                  if (kMergeP) {
+                    tc_mma(p_tmem, dx, dah, id_p2, accp);  // [Xh Ah | Xh Al]
+                  } else {
+                    tc_mma(p_tmem, dx, dah, id_p, accp);
+                    tc_mma(p_tmem, dx, umma_desc(aj + loff, 16, 1024), id_p, 1u);
+                  }
+                  if (kMergeQ) {
+                    tc_mma(q_tmem, qx, qah, id_q2, accq);
+                  } else {
+                    tc_mma(q_tmem, qx, qah, id_q, accq);
+                    tc_mma(q_tmem, qx, umma_desc(ai + loff, 16, 1024), id_q, 1u);
+                  }
                 } else {
-                  tc_mma(p_tmem, dxh, dah, id_p, accp);
-                  tc_mma(p_tmem, dxh, umma_desc(aj + loff, 16, 1024), id_p, 1u);
+                  tc_mma(p_tmem, dx, dah, id_p, 1u);  // Xl Ah into P's first half
+                  tc_mma(q_tmem, qx, qah, id_q, 1u);  // Xl^T Ah_I
                 }
-                tc_mma(p_tmem, dxl, dah, id_p, 1u);  // Xl Ah into the first half
-                if (kMergeQ) {
-                  tc_mma(q_tmem, qxh, qah, id_q2, accq);
-                } else {
-                  tc_mma(q_tmem, qxh, qah, id_q, accq);
-                  tc_mma(q_tmem, qxh, umma_desc(ai + loff, 16, 1024), id_q, 1u);
-                }
-                tc_mma(q_tmem, qxl, qah, id_q, 1u);
               }
               __syncwarp();
             }
-          }
-          if (elect_one()) tc_commit(smem_u32(&empty[stage]));
-          __syncwarp();
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+            if (elect_one()) tc_commit(smem_u32(&empty[stage]));
+            __syncwarp();
+            if (++stage == kNSt) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
         if (elect_one()) {
@@ -495,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int K>
 constexpr uint32_t k1_smem_bytes() {  // same for both MQ variants
-  return 1024 /*align slack*/ + kStages * (4 * kXBox + 4 * K * 128) + 2 * (4 * K * 128) + 256;
+  return 1024 /*align slack*/ + K1Stages<K>::kNSt * K1Stages<K>::kSubBytes + 2 * (4 * K * 128) +
+         (2 * K1Stages<K>::kNSt + 10) * 8 + 16;
 }
 
 // Deterministic reduction of the partials:

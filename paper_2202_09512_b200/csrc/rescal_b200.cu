@@ -414,6 +414,15 @@ bool k1_merge_q(int K, int64_t NC) {
   return (ncb + 5) / 6 == (ncb + 11) / 12;
 }
 
+using K1Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                         rk::tc::K1Args);
+
+K1Kernel k1_kernel_of(const rk_handle* h) {
+  using namespace rk::tc;
+  if (h->K == 16) return k1_tc_kernel<16, true>;
+  return h->k1_mq ? k1_tc_kernel<32, true> : k1_tc_kernel<32, false>;
+}
+
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
 void plan_tc(rk_handle* h) {
   const int K = h->K;
@@ -489,15 +498,7 @@ void plan_tc(rk_handle* h) {
   h->maps[4] = make_map(h->ATh_col, h->NC, K, K);
   h->maps[5] = make_map(h->ATl_col, h->NC, K, K);
   h->smem_tc = K == 16 ? rk::tc::k1_smem_bytes<16>() : rk::tc::k1_smem_bytes<32>();
-  if (K == 16)
-    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)h->smem_tc));
-  else if (h->k1_mq)
-    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)h->smem_tc));
-  else
-    RK_CUDA(cudaFuncSetAttribute(rk::tc::k1_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)h->smem_tc));
+  RK_CUDA(cudaFuncSetAttribute(k1_kernel_of(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_tc));
 }
 
 void alloc_factor_buffers(rk_handle* h) {
@@ -832,9 +833,7 @@ void launch_k1(rk_handle* h, bool timed) {
     a.cta_slot = h->d_cta_slot;
     a.ctl = h->ctl;
     a.skip_if_stopped = 1;
-    auto kern = K == 16 ? rk::tc::k1_tc_kernel<16, true>
-                        : (h->k1_mq ? rk::tc::k1_tc_kernel<32, true> : rk::tc::k1_tc_kernel<32, false>);
-    launch_pdl(kern, dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0], h->maps[1], h->maps[2],
+    launch_pdl(k1_kernel_of(h), dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0], h->maps[1], h->maps[2],
                h->maps[3], h->maps[4], h->maps[5], a);
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
@@ -2861,9 +2860,9 @@ void* rk_stream(rk_handle* h) { return h ? (void*)h->stream : nullptr; }
 int rk_info(rk_handle* h, int64_t* out, int32_t n_out) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
-    int64_t v[11] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
-                     h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0};
-    for (int i = 0; i < n_out && i < 11; ++i) out[i] = v[i];
+    int64_t v[12] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
+                     h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0, h->k1_mq ? 1 : 0};
+    for (int i = 0; i < n_out && i < 12; ++i) out[i] = v[i];
   });
 }
 
