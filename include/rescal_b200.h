@@ -199,6 +199,10 @@ int rk_debug_guards(int32_t on);
 int rk_debug_check_guards(int64_t* damaged_bytes, int64_t* blocks_checked);
 /* Positive control: allocate 1000 bytes, write nbytes past the end, free. */
 int rk_debug_overrun(int64_t nbytes);
+/* The slice products of the handle's last K1 pass (dense engines): P = X_t A
+ * into P[m][n_pad][k_pad] and Q = X_t^T A into Q[m][n_pad][k_pad] (fp32, the
+ * padded layout rk_info reports). Accuracy tests of the tensor-core pass. */
+int rk_debug_read_pq(rk_handle* h, float* P, float* Q);
 
 /* Raw PCG64 draws u_{offset} .. u_{offset+count-1} (tests of the generator). */
 int rk_pcg64_draws(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t offset,

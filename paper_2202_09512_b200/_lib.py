@@ -97,6 +97,7 @@ SIGNATURES = {
     "rk_debug_guards": (ctypes.c_int, [_i32]),
     "rk_debug_check_guards": (ctypes.c_int, [_pi64, _pi64]),
     "rk_debug_overrun": (ctypes.c_int, [_i64]),
+    "rk_debug_read_pq": (ctypes.c_int, [_vp, _vp, _vp]),
 }
 
 _LIB = None
@@ -114,6 +115,8 @@ def load():
             "(the RESCAL engine has no CPU fallback)")
     lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if path != LIB_PATH and not hasattr(lib, name):
+            continue  # an older experimental build
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -294,6 +297,15 @@ class Engine:
         r = np.empty((self.m, self.k, self.k), dtype=np.float64)
         check(self._lib.rk_get_factors(self._h, _dp(a), _dp(r)))
         return a, r
+
+    def debug_read_pq(self):
+        """P = X_t A and Q = X_t^T A of the last K1 pass, [m][n_pad][k_pad] fp32."""
+        inf = self.info()
+        shape = (self.m, inf["n_pad"], inf["k_pad"])
+        p = np.empty(shape, dtype=np.float32)
+        q = np.empty(shape, dtype=np.float32)
+        check(self._lib.rk_debug_read_pq(self._h, p.ctypes.data, q.ctypes.data))
+        return p, q
 
     # compute ---------------------------------------------------------------
     def run(self, iters, eps, track_error=True, tol=None):

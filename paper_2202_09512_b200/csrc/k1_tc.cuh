@@ -12,10 +12,23 @@
 //   item   = (t, strip, row-block rb): the c tiles of one row block in a strip
 // Each CTA owns a contiguous range of items (balanced by tile count). Within
 // an item the P accumulator (128 rows x K) lives in TMEM (double buffered);
-// the c Q accumulators (one per column tile, 128 x K each) live in TMEM for
-// the whole run of items the CTA has in the same (t, strip) — a "segment".
-//   P partial  -> Ppart[strip][t][row][K]      (one writer per (t,strip,row))
-//   Q partial  -> Qpart[slot][strip col][K]    (one slot per segment)
+// the c Q accumulators (one per column tile, 128 x K each) live in TMEM
+// across the run of items the CTA has in the same (t, strip).
+// Rotating Q drains (accuracy): the tensor core's fp32 accumulation loses
+// ~1 ulp per accumulate step in one direction, so the relative error of a
+// TMEM sum grows LINEARLY with its length (Q at n = 32768 summed over whole
+// runs: 5.7e-5 with ~76-row-block runs; P, 12 tiles per item: 5e-6). So
+// after the item of row block rb, Q tile (rb mod c) is drained — its TMEM
+// sum added into the run's slot in fp32 (round-to-nearest) and restarted:
+// every TMEM sum spans at most c row blocks, and one 16 KB tile leaves per
+// item (like P). The MMAs reuse that tile only c - 1 tiles later, so the
+// drain never stalls the tensor pipe (a drain of all c tiles at once costs
+// ~6 us of stalled MMA per drain). At the end of a run all tiles drain.
+// The slot (CTA-private, one per (CTA, run)) is read back by later drains:
+// stored evict-last under an L2 set-aside. The CTA's final drain writes a
+// fresh slot (a read-back there would sit on the kernel's tail).
+//   P partial  -> Ppart[strip][t][row block][K/4][128] float4 (one writer per (t,strip,row))
+//   Q partial  -> Qpart[slot][tile][K/4][128] float4
 // k1_reduce sums the partials in a fixed order (deterministic, no atomics).
 //
 // Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
@@ -32,6 +45,7 @@ namespace tc {
 constexpr int kTile = 128;
 constexpr int kThreads = 192;
 constexpr uint32_t kXBox = 128 * 64 * 2;  // one 128-row x 64-col bf16 box = 16 KB
+constexpr int kMaxC = 16;                 // max column tiles per strip (TMEM: 512 / 32)
 
 struct K1Args {
   int NR, NC, K, M;
@@ -39,8 +53,9 @@ struct K1Args {
   int nstrips;
   int nrb;        // NR / 128 row blocks
   int ncb;        // NC / 128 column tiles
-  float* Ppart;   // [nstrips][M][NR][K]
-  float* Qpart;   // [nslots][c*128][K]
+  int qrot;       // rotating Q drains: one tile every qrot items (0 = only at run ends)
+  float* Ppart;   // [nstrips][M][NR/128][K/4][128] float4
+  float* Qpart;   // [nslots][c][K/4][128] float4
   const int* cta_begin;  // [grid + 1] item ranges
   const int* cta_slot;   // [grid] first Q slot of the CTA
   const Ctl* ctl;
@@ -174,6 +189,12 @@ RK_DEV void decode_item(int item, int nstrips, int nrb, int& t, int& s, int& rb)
   t = ts / nstrips;
 }
 
+// the Q tile drained after row block rb (-1: none): tile (rb / p) mod c after
+// every p-th row block (k1_plan mirrors this on the host)
+__host__ __device__ inline int k1_rot_tile(int rb, int p, int c) {
+  return p > 0 && rb % p == p - 1 ? (rb / p) % c : -1;
+}
+
 RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
   return s == nstrips - 1 ? ncb - c * (nstrips - 1) : c;
 }
@@ -212,6 +233,44 @@ struct K1Stages {
   static constexpr uint32_t kSubBytes = 2 * kXBox + 4 * kABox;
 };
 
+// One Q tile's drain (epilogue thread = one TMEM lane / tile row): wait for
+// the tile's commit, read its K columns, release the TMEM (q_empty), add the
+// slot's earlier sum `old` when `add`, store the row (float4 column-major
+// slot layout, stride 128 rows) with L2 policy `pol`.
+template <int K, bool MQ>
+RK_DEV void k1_drain_q(uint32_t taddr, uint32_t full_bar, uint32_t par, uint32_t empty_bar, int lane,
+                       float4* dst, const float4 (&old)[K / 4], bool add, uint64_t pol) {
+  mbar_wait(full_bar, par);
+  tc_fence_after();
+  float w[K];
+#pragma unroll
+  for (int h = 0; h < K / 16; ++h) tmem_ld16(taddr + 16 * h, w + 16 * h);
+  if (MQ) {
+    float w2[K];
+#pragma unroll
+    for (int h = 0; h < K / 16; ++h) tmem_ld16(taddr + K + 16 * h, w2 + 16 * h);
+#pragma unroll
+    for (int d = 0; d < K; ++d) w[d] += w2[d];
+  }
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
+  if (add) {
+#pragma unroll
+    for (int h = 0; h < K / 4; ++h) {
+      w[4 * h] += old[h].x;
+      w[4 * h + 1] += old[h].y;
+      w[4 * h + 2] += old[h].z;
+      w[4 * h + 3] += old[h].w;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < K / 4; ++h)
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst + h * kTile),
+                 "f"(w[4 * h]), "f"(w[4 * h + 1]), "f"(w[4 * h + 2]), "f"(w[4 * h + 3]), "l"(pol)
+                 : "memory");
+}
+
 template <int K, bool MQ>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap map_xh, const __grid_constant__ CUtensorMap map_xl,
@@ -249,15 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* ai_empty = ai_full + 2;          // [2]
   uint64_t* p_full = ai_full + 4;            // [2]
   uint64_t* p_empty = ai_full + 6;           // [2]
-  uint64_t* q_full = ai_full + 8;            // [1]
-  uint64_t* q_empty = ai_full + 9;           // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ai_full + 10);
+  uint64_t* q_full = ai_full + 8;            // [kMaxC], one per Q column tile
+  uint64_t* q_empty = q_full + kMaxC;        // [kMaxC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + kMaxC);
 
   const int warp = warp_id_uniform();
   const int lane = threadIdx.x & 31;
   const int item_b = args.cta_begin[blockIdx.x];
   const int item_e = args.cta_begin[blockIdx.x + 1];
   const int nstrips = args.nstrips, nrb = args.nrb, ncb = args.ncb, c = args.c, NR = args.NR;
+  const int qrot = args.qrot;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNSt; ++i) {
@@ -270,8 +330,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&p_full[i]), 1);
       mbar_init(smem_u32(&p_empty[i]), 4);  // one arrive per epilogue warp
     }
-    mbar_init(smem_u32(q_full), 1);
-    mbar_init(smem_u32(q_empty), 4);
+    for (int i = 0; i < kMaxC; ++i) {
+      mbar_init(smem_u32(&q_full[i]), 1);
+      mbar_init(smem_u32(&q_empty[i]), 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -351,20 +413,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_q2 = idesc_bf16(2 * K, 1);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t qe_phase = 0;
-      int seg = 0;
+      uint32_t owed = 0;     // Q tiles committed for a drain, not yet waited free
+      uint32_t qe_par = 0;   // per-tile q_empty parity
+      uint32_t restart = 0;  // Q tiles whose next MMA starts a fresh TMEM sum
       for (int item = item_b; item < item_e; ++item) {
         int t, s, rb;
         decode_item(item, nstrips, nrb, t, s, rb);
         const int ct = strip_tiles(s, nstrips, c, ncb);
         const int ts = item / nrb;
-        const bool first_in_seg = item == item_b || (item - 1) / nrb != ts;
-        const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
-        if (first_in_seg && seg > 0) {
-          mbar_wait(smem_u32(q_empty), qe_phase);  // previous segment's Q drained
-          qe_phase ^= 1;
-          tc_fence_after();
-        }
+        if (item == item_b || (item - 1) / nrb != ts) restart = ~0u;  // a new (t, strip) run
+        const bool run_end = item == item_e - 1 || (item + 1) / nrb != ts;
+        const int dcb = k1_rot_tile(rb, qrot, c);  // the Q tile drained after this item
         const int idx = item - item_b;
         const int ab = idx & 1;
         const uint32_t ap = (idx >> 1) & 1;
@@ -377,6 +436,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t p_tmem = tmem + (uint32_t)(c * kQW + pb * kPW);
         for (int cb = 0; cb < ct; ++cb) {
           const uint32_t q_tmem = tmem + (uint32_t)(cb * kQW);
+          const uint32_t bit = 1u << cb;
+          if (owed & bit) {  // its last drain has read the TMEM tile
+            mbar_wait(smem_u32(&q_empty[cb]), (qe_par >> cb) & 1);
+            qe_par ^= bit;
+            owed &= ~bit;
+            tc_fence_after();
+          }
+          const bool q_fresh = (restart & bit) != 0;
 #pragma unroll
           for (int sub = 0; sub < 2; ++sub) {  // 0: the X hi plane's products, 1: the X lo plane's
             mbar_wait(smem_u32(&full[stage]), phase);
@@ -395,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (elect_one()) {
                 if (sub == 0) {
                   const uint32_t accp = (cb > 0 || ks > 0) ? 1u : 0u;
-                  const uint32_t accq = (first_in_seg && ks == 0) ? 0u : 1u;
+                  const uint32_t accq = (q_fresh && ks == 0) ? 0u : 1u;
                   if (kMergeP) {
                     tc_mma(p_tmem, dx, dah, id_p2, accp);  // [Xh Ah | Xh Al]
                   } else {
@@ -422,14 +489,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               phase ^= 1;
             }
           }
+          restart &= ~bit;
+          if (run_end || cb == dcb) {  // tile cb's sum is drained after this item
+            if (elect_one()) tc_commit(smem_u32(&q_full[cb]));
+            __syncwarp();
+            owed |= bit;
+            restart |= bit;
+          }
         }
         if (elect_one()) {
           tc_commit(smem_u32(&p_full[pb]));
           tc_commit(smem_u32(&ai_empty[ab]));
-          if (last_in_seg) tc_commit(smem_u32(q_full));
         }
         __syncwarp();
-        if (last_in_seg) ++seg;
       }
     }
   } else {
@@ -437,17 +509,88 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;                 // TMEM lane quadrant
     const int row = quad * 32 + lane;          // row within the 128-row tile
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    uint32_t qf_phase = 0;
-    int slot = args.cta_slot[blockIdx.x];
+    uint32_t qf_par = 0;     // per-tile q_full parity
+    uint32_t stored = 0;     // tiles of the current slot written at least once
+    int slot = args.cta_slot[blockIdx.x] - 1;
+    int slot_ts = -1;        // the (t, strip) the current slot belongs to
+    uint64_t pol_keep, pol_norm;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
     for (int item = item_b; item < item_e; ++item) {
       int t, s, rb;
       decode_item(item, nstrips, nrb, t, s, rb);
       const int ct = strip_tiles(s, nstrips, c, ncb);
       const int ts = item / nrb;
-      const bool last_in_seg = item == item_e - 1 || (item + 1) / nrb != ts;
+      const bool run_end = item == item_e - 1 || (item + 1) / nrb != ts;
+      const int dcb = k1_rot_tile(rb, qrot, c);
       const int idx = item - item_b;
       const int pb = idx & 1;
       const uint32_t pp = (idx >> 1) & 1;
+      if (ts != slot_ts) {  // one slot per (CTA, (t, strip) run)
+        ++slot;
+        slot_ts = ts;
+        stored = 0;
+      }
+      float4* qslot = reinterpret_cast<float4*>(args.Qpart + (size_t)slot * c * kTile * K) + row;
+      if (item == item_e - 1 && stored != 0) {
+        // the CTA's final drain never reads back (a load round trip per tile
+        // would sit on the kernel's tail): it stores into a slot of its own;
+        // the tiles the old slot never received are zeroed
+        for (int cb = 0; cb < ct; ++cb)
+          if (!((stored >> cb) & 1)) {
+#pragma unroll
+            for (int h = 0; h < K / 4; ++h) qslot[((size_t)cb * K / 4 + h) * kTile] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        ++slot;
+        stored = 0;
+        qslot += (size_t)c * kTile * K / 4;
+      }
+      // a slot tile a later drain reads back is stored evict-last (an L2
+      // set-aside holds it against the X stream); the run's last store releases it
+      const uint64_t pol = run_end ? pol_norm : pol_keep;
+      if (run_end) {
+        // every Q tile of the run: tiles in pairs, each with its own register
+        // set, so a read-back load has two tiles of time to land
+        float4 o[2][K / 4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (u < ct && ((stored >> u) & 1)) {
+#pragma unroll
+            for (int h = 0; h < K / 4; ++h) o[u][h] = qslot[((size_t)u * K / 4 + h) * kTile];
+          }
+        for (int cp = 0; cp < ct; cp += 2) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int cb = cp + u;
+            if (cb < ct) {
+              const bool add = (stored >> cb) & 1;
+              k1_drain_q<K, kMergeQ>(tmem + lane_base + (uint32_t)(cb * kQW), smem_u32(&q_full[cb]),
+                                     (qf_par >> cb) & 1, smem_u32(&q_empty[cb]), lane,
+                                     qslot + (size_t)cb * kTile * K / 4, o[u], add, pol);
+              qf_par ^= 1u << cb;
+              if (cb + 2 < ct && ((stored >> (cb + 2)) & 1)) {
+#pragma unroll
+                for (int h = 0; h < K / 4; ++h) o[u][h] = qslot[((size_t)(cb + 2) * K / 4 + h) * kTile];
+              }
+            }
+          }
+        }
+        stored = 0;  // the next item starts a new run (or the CTA is done)
+      } else if (dcb >= 0 && dcb < ct) {
+        // the one tile this item rotates out; its MMAs for the next item wait
+        // ~c - 1 tiles later, so this never stalls the tensor pipe
+        const bool add = (stored >> dcb) & 1;
+        float4 o[K / 4];
+        float4* qd = qslot + (size_t)dcb * kTile * K / 4;
+        if (add) {
+#pragma unroll
+          for (int h = 0; h < K / 4; ++h) o[h] = qd[h * kTile];
+        }
+        k1_drain_q<K, kMergeQ>(tmem + lane_base + (uint32_t)(dcb * kQW), smem_u32(&q_full[dcb]),
+                               (qf_par >> dcb) & 1, smem_u32(&q_empty[dcb]), lane, qd, o, add, pol);
+        qf_par ^= 1u << dcb;
+        stored |= 1u << dcb;
+      }
       mbar_wait(smem_u32(&p_full[pb]), pp);
       tc_fence_after();
       float v[K];
@@ -465,38 +608,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&p_empty[pb]));
+      // partial layout [strip][t][row block][K/4][128 rows] float4 (coalesced)
       float4* dst = reinterpret_cast<float4*>(
-          args.Ppart + ((((size_t)s * args.M + t) * NR) + (size_t)rb * kTile + row) * K);
+                        args.Ppart + ((((size_t)s * args.M + t) * NR) + (size_t)rb * kTile) * K) + row;
 #pragma unroll
-      for (int h = 0; h < K / 4; ++h) dst[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-      if (last_in_seg) {
-        mbar_wait(smem_u32(q_full), qf_phase);
-        qf_phase ^= 1;
-        tc_fence_after();
-        float* qdst = args.Qpart + (size_t)slot * c * kTile * K;
-        for (int cb = 0; cb < ct; ++cb) {
-          float w[K];
-#pragma unroll
-          for (int h = 0; h < K / 16; ++h)
-            tmem_ld16(tmem + lane_base + (uint32_t)(cb * kQW + 16 * h), w + 16 * h);
-          if (kMergeQ) {
-            float w2[K];
-#pragma unroll
-            for (int h = 0; h < K / 16; ++h)
-              tmem_ld16(tmem + lane_base + (uint32_t)(cb * kQW + K + 16 * h), w2 + 16 * h);
-#pragma unroll
-            for (int d = 0; d < K; ++d) w[d] += w2[d];
-          }
-          float4* qd = reinterpret_cast<float4*>(qdst + ((size_t)cb * kTile + row) * K);
-#pragma unroll
-          for (int h = 0; h < K / 4; ++h)
-            qd[h] = make_float4(w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(q_empty));
-        ++slot;
-      }
+      for (int h = 0; h < K / 4; ++h)
+        dst[h * kTile] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
     }
   }
 
@@ -511,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int K>
 constexpr uint32_t k1_smem_bytes() {  // same for both MQ variants
   return 1024 /*align slack*/ + K1Stages<K>::kNSt * K1Stages<K>::kSubBytes + 2 * (4 * K * 128) +
-         (2 * K1Stages<K>::kNSt + 10) * 8 + 16;
+         (2 * K1Stages<K>::kNSt + 8 + 2 * kMaxC) * 8 + 16;
 }
 
 // Deterministic reduction of the partials:
@@ -525,7 +642,8 @@ RK_DEV void k1_reduce_p4(const float* __restrict__ Ppart, float* __restrict__ P,
   // loads batched 4 at a time (independent, in flight together), sums kept in strip order
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const size_t sstride = (size_t)M * NR * K / 4;  // float4s between strips
-  const float4* src = reinterpret_cast<const float4*>(Ppart + (((size_t)t * NR) + i) * K) + q4;
+  const float4* src = reinterpret_cast<const float4*>(Ppart + (((size_t)t * NR) + (i & ~(kTile - 1))) * K) +
+                      q4 * kTile + (i & (kTile - 1));
   int s = 0;
   for (; s + 4 <= nstrips; s += 4) {
     float4 v[4];
@@ -552,7 +670,8 @@ RK_DEV void k1_reduce_q4(const float* __restrict__ Qpart, const int* __restrict_
   const int jl = j - s * W;
   const int f = slot_first[t * nstrips + s], nsl = slot_count[t * nstrips + s];
   float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* src = reinterpret_cast<const float4*>(Qpart + ((size_t)f * W + jl) * K) + q4;
+  const float4* src = reinterpret_cast<const float4*>(Qpart + ((size_t)f * W + (jl & ~(kTile - 1))) * K) +
+                      q4 * kTile + (jl & (kTile - 1));
   const size_t qstride = (size_t)W * K / 4;  // float4s between slots
   int q = 0;
   for (; q + 4 <= nsl; q += 4) {
@@ -580,14 +699,20 @@ RK_DEV void k1_reduce_body(const float* __restrict__ Ppart, const float* __restr
   const int64_t total = totalP + (int64_t)M * NC * K4;
 #pragma unroll 2
   for (int64_t e = g0; e < total; e += gstride) {
+    // consecutive threads take consecutive rows of one float4 column: the
+    // partials' [row block][K/4][128] layout makes their loads contiguous
     if (e < totalP) {
-      const int q4 = (int)(e % K4);
-      const int64_t ti = e / K4;
+      const int r = (int)(e % kTile);
+      const int64_t rest = e / kTile;
+      const int q4 = (int)(rest % K4);
+      const int64_t ti = (rest / K4) * kTile + r;
       k1_reduce_p4(Ppart, P, NR, K, M, nstrips, (int)(ti / NR), (int)(ti % NR), q4);
     } else {
       const int64_t e2 = e - totalP;
-      const int q4 = (int)(e2 % K4);
-      const int64_t tj = e2 / K4;
+      const int r = (int)(e2 % kTile);
+      const int64_t rest = e2 / kTile;
+      const int q4 = (int)(rest % K4);
+      const int64_t tj = (rest / K4) * kTile + r;
       k1_reduce_q4(Qpart, slot_first, slot_count, Q, NC, K, c, nstrips, (int)(tj / NC), (int)(tj % NC), q4);
     }
   }

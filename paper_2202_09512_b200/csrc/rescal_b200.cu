@@ -298,7 +298,7 @@ struct rk_handle {
   double* npart2 = nullptr;
   int nnp = 0;
   // tcgen05 schedule
-  int c = 0, nstrips = 0, grid_tc = 0, nslots = 0;
+  int c = 0, nstrips = 0, grid_tc = 0, nslots = 0, qrot = 1;
   bool k1_mq = true;  // K1 merges the Q hi/lo operands (always at K = 16; see k1_merge_q)
   size_t smem_tc = 0;
   float *Ppart = nullptr, *Qpart = nullptr;
@@ -423,6 +423,17 @@ K1Kernel k1_kernel_of(const rk_handle* h) {
   return h->k1_mq ? k1_tc_kernel<32, true> : k1_tc_kernel<32, false>;
 }
 
+// K1's Q accuracy mode (k1_tc.cuh "Rotating Q drains"): RK_K1_QROT=p > 0
+// drains one Q tile after every p-th row block, bounding each TMEM sum to
+// p*c row blocks (n = 32768, k = 32: Q rel. error 5.7e-5 -> 6.2e-6 at p = 1)
+// for 1.4-1.7 % more K1 time (read-backs of the slots that miss L2). Off by
+// default: the default error is inside the parity tolerance and K1 is the
+// HBM-bound headline kernel (profiles/r02_q_rotation.md).
+int k1_qrot() {
+  const char* e = std::getenv("RK_K1_QROT");
+  return e ? std::max(0, std::atoi(e)) : 0;
+}
+
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
 void plan_tc(rk_handle* h) {
   const int K = h->K;
@@ -442,6 +453,7 @@ void plan_tc(rk_handle* h) {
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
   nstrips = (ncb + c - 1) / c;
+  if (c > rk::tc::kMaxC) throw std::runtime_error("K1 strip wider than kMaxC tiles");
   h->c = c;
   h->nstrips = nstrips;
   const int64_t n_items = (int64_t)M * nstrips * nrb;
@@ -461,20 +473,35 @@ void plan_tc(rk_handle* h) {
     if (it == begin[g] && it < n_items) cum += tiles_of(it++);  // at least one item
   }
   begin[grid] = (int)n_items;
-  // slots: one per (CTA, segment) in item order
+  // slots: one per (CTA, (t, strip) run) in item order, plus a fresh one for
+  // a CTA's final drain when its last run already stored (mirrors the
+  // epilogue's rule in k1_tc.cuh exactly)
+  h->qrot = k1_qrot();
   std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips, 0), slot_count(M * nstrips, 0);
   int slots = 0;
+  auto new_slot = [&](int ts) {
+    if (slot_count[ts] == 0) slot_first[ts] = slots;
+    slot_count[ts] += 1;
+    ++slots;
+  };
   for (int g = 0; g < grid; ++g) {
     cta_slot[g] = slots;
-    int prev = -1;
+    int slot_ts = -1;
+    bool stored = false;
     for (int i = begin[g]; i < begin[g + 1]; ++i) {
-      int ts = i / nrb;
-      if (ts != prev) {
-        if (slot_count[ts] == 0) slot_first[ts] = slots;
-        slot_count[ts] += 1;
-        ++slots;
-        prev = ts;
+      const int ts = i / nrb, rb = i % nrb;
+      const int ct = tiles_of(i);
+      const bool run_end = i == begin[g + 1] - 1 || (i + 1) / nrb != ts;
+      if (ts != slot_ts) {
+        new_slot(ts);
+        slot_ts = ts;
+        stored = false;
       }
+      if (i == begin[g + 1] - 1 && stored) new_slot(ts);
+      if (run_end)
+        stored = false;
+      else if (rk::tc::k1_rot_tile(rb, h->qrot, c) >= 0 && rk::tc::k1_rot_tile(rb, h->qrot, c) < ct)
+        stored = true;
     }
   }
   h->grid_tc = grid;
@@ -491,6 +518,19 @@ void plan_tc(rk_handle* h) {
                      cudaMemcpyHostToDevice));
   h->Ppart = dalloc<float>((size_t)M * nstrips * h->NR * K);
   h->Qpart = dalloc<float>((size_t)slots * c * 128 * K);
+  // the slots being added into (one per CTA) are stored evict-last; give
+  // them an L2 set-aside so the policy holds against the X stream
+  if (h->qrot) {
+    int dev = 0, maxp = 0;
+    RK_CUDA(cudaGetDevice(&dev));
+    RK_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    // (sized to the live slots: the device maximum, 83 MB, slows the X
+    // stream itself by 10 %, profiles/r02_q_rotation.md)
+    const size_t want = std::min<size_t>((size_t)maxp, (size_t)grid * c * 128 * K * sizeof(float) * 5 / 4);
+    size_t cur = 0;
+    RK_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (want > cur) RK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  }
   h->maps[0] = make_map(h->Xh, h->NC, (uint64_t)M * h->NR, 128);
   h->maps[1] = make_map(h->Xl, h->NC, (uint64_t)M * h->NR, 128);
   h->maps[2] = make_map(h->ATh_row, h->NR, K, K);
@@ -827,6 +867,7 @@ void launch_k1(rk_handle* h, bool timed) {
     a.nstrips = h->nstrips;
     a.nrb = (int)(h->NR / 128);
     a.ncb = (int)(h->NC / 128);
+    a.qrot = h->qrot;
     a.Ppart = h->Ppart;
     a.Qpart = h->Qpart;
     a.cta_begin = h->d_cta_begin;
@@ -2679,6 +2720,15 @@ int rk_debug_guards(int32_t on) {
     DevPool& P = dev_pool();
     std::lock_guard<std::mutex> lk(P.mu);
     P.guard = on != 0;
+  });
+}
+
+int rk_debug_read_pq(rk_handle* h, float* P, float* Q) {
+  return guarded([&] {
+    RK_REQUIRE(h && h->P && h->Q && h->NR == h->NC, RK_ERR_DATA, "no dense K1 products on this handle");
+    RK_CUDA(cudaStreamSynchronize(h->stream));
+    RK_CUDA(cudaMemcpy(P, h->P, sizeof(float) * h->m * h->NR * h->K, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(Q, h->Q, sizeof(float) * h->m * h->NC * h->K, cudaMemcpyDeviceToHost));
   });
 }
 

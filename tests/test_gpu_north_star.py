@@ -6,6 +6,8 @@
   against the fp64 oracle on the device generator's exact values
   (m = 2 keeps the host oracle affordable; rescal.py:114-146).
 * K = 32 with merged Q (n <= 768) and unmerged Q with several strips.
+* K1's slice products P and Q against fp64 at n = 32768, default schedule
+  and rotating Q drains (the accuracy mode).
 * RESCALk over cfg5's sweep shape (k = 2..16, r = 10, delta = 0.02, 200
   iterations) against the real reference's report (tests/golden/rescalk_cfg5.npz):
   selected k identical, s_min / s_avg within 1e-4, rel_error within 1e-5.
@@ -55,6 +57,35 @@ def test_cfg3_shape_matches_oracle():
     assert rel_fro(a_dev, a) <= 1e-4 and rel_fro(r_dev, r) <= 1e-4, (rel_fro(a_dev, a), rel_fro(r_dev, r))
     assert abs(trace[-1] - err) <= 1e-5, (trace[-1], err)
     assert np.all(np.diff(trace) <= 1e-9), trace
+
+
+@pytest.mark.parametrize("qrot,q_bound", [("0", 6e-5), ("1", 1e-5)])
+def test_k1_slice_products_accuracy(monkeypatch, qrot, q_bound):
+    """K1's P = X A and Q = X^T A against fp64 at n = 32768 (k = 32, one
+    slice): the TMEM sums' error grows with their length (k1_tc.cuh); the
+    default schedule keeps Q within 6e-5, rotating drains (RK_K1_QROT=1)
+    within 1e-5, P within 1e-5 either way."""
+    monkeypatch.setenv("RK_K1_QROT", qrot)
+    n, m, k = 32768, 1, 32
+    eng = _lib.Engine(n, m, k, device=0, engine="tc")
+    try:
+        eng.fill_uniform(23)
+        x = eng.block_uniform(23, n, n)[0]
+        f0 = rk.random_init(n, k, m, 3)
+        eng.set_factors(f0.A, f0.R)
+        eng.update_r(1e-16)  # one K1 pass
+        p, q = eng.debug_read_pq()
+    finally:
+        eng.close()
+    a = f0.A
+    pr = np.empty((n, k)); qr = np.zeros((n, k))
+    for r0 in range(0, n, 4096):
+        xb = x[r0:r0 + 4096].astype(np.float64)
+        pr[r0:r0 + 4096] = xb @ a
+        qr += xb.T @ a[r0:r0 + 4096]
+    ep = rel_fro(p[0, :n, :k], pr)
+    eq = rel_fro(q[0, :n, :k], qr)
+    assert ep <= 1e-5 and eq <= q_bound, (ep, eq)
 
 
 @pytest.mark.parametrize("n,merged", [(768, True), (1664, False), (4096, False)])
