@@ -226,10 +226,12 @@ struct K1Cfg {
 // boxes), so the shared memory holds 4 (K = 32) / 5 (K = 16) of them instead
 // of 2 whole-tile stages: more bytes in flight per SM (round 2: cfg2 K1 0.976
 // -> 0.997 of HBM, cfg3 11.90 -> 11.60-11.69 ms; profiles/r02_k1_split_stages).
+// K = 48 / 64 (k from 33 to 64): the A boxes grow with K, so 3 / 2
+// sub-stages fit next to the two A_row buffers (227 KB).
 template <int K>
 struct K1Stages {
   static constexpr uint32_t kABox = K * 128;
-  static constexpr int kNSt = K == 32 ? 4 : 5;
+  static constexpr int kNSt = K == 16 ? 5 : K == 32 ? 4 : K == 48 ? 3 : 2;
   static constexpr uint32_t kSubBytes = 2 * kXBox + 4 * kABox;
 };
 
@@ -281,7 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // map_x*: the block's slices as a (M*NR) x NC bf16 matrix (hi / lo planes)
   // map_r*: A_row^T (K x NR) — B operand of Q = X^T A_row (indexed by row i)
   // map_c*: A_col^T (K x NC) — B operand of P = X A_col (indexed by col j)
-  static_assert(K == 16 || K == 32, "tcgen05 path supports k_pad 16 or 32");
+  static_assert(K == 16 || K == 32 || K == 48 || K == 64, "tcgen05 path supports k_pad 16, 32, 48, 64");
+  // rotating Q drains (read-back registers) only at K <= 32 (k1_qrot())
+  constexpr bool kRot = K <= 32;
   constexpr bool kMergeP = K1Cfg<K, MQ>::kMergeP, kMergeQ = K1Cfg<K, MQ>::kMergeQ;
   constexpr int kPW = K1Cfg<K, MQ>::kPW, kQW = K1Cfg<K, MQ>::kQW;
   constexpr uint32_t kABox = K * 128;              // K rows x 64 bf16
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         stored = 0;
       }
       float4* qslot = reinterpret_cast<float4*>(args.Qpart + (size_t)slot * c * kTile * K) + row;
+      if (!kRot) stored = 0;  // (lets the compiler drop the read-back path)
       if (item == item_e - 1 && stored != 0) {
         // the CTA's final drain never reads back (a load round trip per tile
         // would sit on the kernel's tail): it stores into a slot of its own;
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         stored = 0;  // the next item starts a new run (or the CTA is done)
-      } else if (dcb >= 0 && dcb < ct) {
+      } else if (kRot && dcb >= 0 && dcb < ct) {
         // the one tile this item rotates out; its MMAs for the next item wait
         // ~c - 1 tiles later, so this never stalls the tensor pipe
         const bool add = (stored >> dcb) & 1;

@@ -363,7 +363,8 @@ void drop_graphs(rk_handle* h) {
 // (sparse.cuh sp_gram_tc_k, TF32 3-pass, fp64 per 32 rows) over the reduced
 // P instead of the SIMT cluster kernel k2a_v4 (cfg2 K2a 27 -> 16 us, cfg3
 // 197 -> 110 us).
-bool dense_gram_tc(const rk_handle* h) { return !h->sparse && (h->K == 16 || h->K == 32); }
+bool k1_tc_k(int K);
+bool dense_gram_tc(const rk_handle* h) { return !h->sparse && k1_tc_k(h->K); }
 
 size_t k2f_smem(int K) {
   size_t s = (size_t)5 * K * K * sizeof(double);
@@ -410,6 +411,7 @@ void free_factor_buffers(rk_handle* h) {
 // longer the bound once it runs warp-uniform; profiles/r02k1_*.json).
 bool k1_merge_q(int K, int64_t NC) {
   if (K == 16) return true;
+  if (K > 32) return false;
   const int64_t ncb = NC / 128;
   return (ncb + 5) / 6 == (ncb + 11) / 12;
 }
@@ -420,7 +422,51 @@ using K1Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CU
 K1Kernel k1_kernel_of(const rk_handle* h) {
   using namespace rk::tc;
   if (h->K == 16) return k1_tc_kernel<16, true>;
+  if (h->K == 48) return k1_tc_kernel<48, false>;
+  if (h->K == 64) return k1_tc_kernel<64, false>;
   return h->k1_mq ? k1_tc_kernel<32, true> : k1_tc_kernel<32, false>;
+}
+
+bool k1_tc_k(int K) { return K == 16 || K == 32 || K == 48 || K == 64; }
+
+using SpGramTcKernel = void (*)(const rk::Ctl*, const float*, const float*, int, int, int, int, double*, int,
+                                const float*, int);
+SpGramTcKernel sp_gram_tc_of(int K) {
+  switch (K) {
+    case 16: return rk::sp::sp_gram_tc_k<16>;
+    case 48: return rk::sp::sp_gram_tc_k<48>;
+    case 64: return rk::sp::sp_gram_tc_k<64>;
+    default: return rk::sp::sp_gram_tc_k<32>;
+  }
+}
+
+// TMEM columns of one P buffer / one Q accumulator of K1<K, MQ>
+int k1_pw(int K, bool mq) {
+  using namespace rk::tc;
+  switch (K) {
+    case 16: return K1Cfg<16, true>::kPW;
+    case 48: return K1Cfg<48, false>::kPW;
+    case 64: return K1Cfg<64, false>::kPW;
+    default: return mq ? K1Cfg<32, true>::kPW : K1Cfg<32, false>::kPW;
+  }
+}
+int k1_qw(int K, bool mq) {
+  using namespace rk::tc;
+  switch (K) {
+    case 16: return K1Cfg<16, true>::kQW;
+    case 48: return K1Cfg<48, false>::kQW;
+    case 64: return K1Cfg<64, false>::kQW;
+    default: return mq ? K1Cfg<32, true>::kQW : K1Cfg<32, false>::kQW;
+  }
+}
+size_t k1_smem(int K) {
+  using namespace rk::tc;
+  switch (K) {
+    case 16: return k1_smem_bytes<16>();
+    case 48: return k1_smem_bytes<48>();
+    case 64: return k1_smem_bytes<64>();
+    default: return k1_smem_bytes<32>();
+  }
 }
 
 // K1's Q accuracy mode (k1_tc.cuh "Rotating Q drains"): RK_K1_QROT=p > 0
@@ -439,9 +485,8 @@ void plan_tc(rk_handle* h) {
   const int K = h->K;
   const int nrb = (int)(h->NR / 128), ncb = (int)(h->NC / 128);
   h->k1_mq = k1_merge_q(K, h->NC);
-  const int pw = K == 16 ? rk::tc::K1Cfg<16, true>::kPW : rk::tc::K1Cfg<32, true>::kPW;
-  const int qw = K == 16 ? rk::tc::K1Cfg<16, true>::kQW
-                         : (h->k1_mq ? rk::tc::K1Cfg<32, true>::kQW : rk::tc::K1Cfg<32, false>::kQW);
+  const int pw = k1_pw(K, h->k1_mq);
+  const int qw = k1_qw(K, h->k1_mq);
   const int cmax = (512 - 2 * pw) / qw;  // TMEM columns: c Q accumulators + 2 P buffers
   const int M = (int)h->m;
   int c = std::min(cmax, ncb);
@@ -476,7 +521,7 @@ void plan_tc(rk_handle* h) {
   // slots: one per (CTA, (t, strip) run) in item order, plus a fresh one for
   // a CTA's final drain when its last run already stored (mirrors the
   // epilogue's rule in k1_tc.cuh exactly)
-  h->qrot = k1_qrot();
+  h->qrot = K <= 32 ? k1_qrot() : 0;
   std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips, 0), slot_count(M * nstrips, 0);
   int slots = 0;
   auto new_slot = [&](int ts) {
@@ -537,7 +582,7 @@ void plan_tc(rk_handle* h) {
   h->maps[3] = make_map(h->ATl_row, h->NR, K, K);
   h->maps[4] = make_map(h->ATh_col, h->NC, K, K);
   h->maps[5] = make_map(h->ATl_col, h->NC, K, K);
-  h->smem_tc = K == 16 ? rk::tc::k1_smem_bytes<16>() : rk::tc::k1_smem_bytes<32>();
+  h->smem_tc = k1_smem(K);
   RK_CUDA(cudaFuncSetAttribute(k1_kernel_of(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_tc));
 }
 
@@ -574,7 +619,8 @@ void alloc_factor_buffers(rk_handle* h) {
   h->part = dalloc<double>((size_t)h->nb * (M + 1) * KK);
   h->red = dalloc<double>((size_t)(M + 1) * KK + 8);
   h->counters = dalloc<unsigned>((size_t)M + 8);
-  h->fast = !h->grid() && (K == 16 || K == 32);
+  // one-GPU fast k-wide chain (tensor-core G / S, k2f_fused_t, k2b_v4)
+  h->fast = !h->grid() && k1_tc_k(K);
   const bool grid_fast = h->grid() && (K == 16 || K == 32);
   if (grid_fast) h->W32 = dalloc<float>((size_t)M * 2 * KK);
   if (dense_gram_tc(h)) {
@@ -582,12 +628,8 @@ void alloc_factor_buffers(rk_handle* h) {
     // the (m+1) x chunks items cover the GPU at cfg2-sized n
     h->gchunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (h->rows_valid + 511) / 512));
     h->gpart = dalloc<double>((size_t)(M + 1) * h->gchunks * KK);
-    if (K == 16)
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)rk::sp::SpGramTc::smem));
-    else
-      RK_CUDA(cudaFuncSetAttribute(rk::sp::sp_gram_tc_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)rk::sp::SpGramTc::smem));
+    RK_CUDA(cudaFuncSetAttribute(sp_gram_tc_of(K), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rk::sp::SpGramTc::smem));
   }
   if (h->sparse) {
     h->numer = dalloc<double>((size_t)h->NR * K);
@@ -641,9 +683,9 @@ void alloc_factor_buffers(rk_handle* h) {
   // engine
   int eng = h->requested_engine;
   if (h->sparse) eng = RK_ENGINE_SIMT;  // gather-bound CSR/CSC kernels (no GEMM reshaping)
-  if (eng == RK_ENGINE_AUTO) eng = (K == 16 || K == 32) ? RK_ENGINE_TC : RK_ENGINE_SIMT;
-  RK_REQUIRE(!(eng == RK_ENGINE_TC && !(K == 16 || K == 32)), RK_ERR_DATA,
-             "tcgen05 engine needs k_pad in {16, 32}");
+  if (eng == RK_ENGINE_AUTO) eng = k1_tc_k(K) ? RK_ENGINE_TC : RK_ENGINE_SIMT;
+  RK_REQUIRE(!(eng == RK_ENGINE_TC && !k1_tc_k(K)), RK_ERR_DATA,
+             "tcgen05 engine needs k_pad in {16, 32, 48, 64}");
   h->engine = eng;
   if (eng == RK_ENGINE_TC) plan_tc(h);
   const size_t simt_smem = (size_t)(64 * 33 + 64 * K) * sizeof(float);
@@ -684,6 +726,13 @@ void alloc_factor_buffers(rk_handle* h) {
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     else
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+  if (K == 48 || K == 64) {
+    const int smem = rk::kK2bStages * (2 * K * K + 2 * rk::k2b_v4_rb(K, h->NR) * K) * (int)sizeof(float);
+    RK_CUDA(cudaFuncSetAttribute(K == 48 ? rk::k2b_v4<48, 2> : rk::k2b_v4<64, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RK_CUDA(cudaFuncSetAttribute(K == 48 ? rk::k2f_fused_t<48> : rk::k2f_fused_t<64>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
   }
   const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
@@ -946,14 +995,8 @@ void launch_k2a(rk_handle* h, int skip, bool for_k2f = true) {
     // on a grid G runs over the rank's own piece of A (as k2a_v4's aown), S_t over its row set
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : nullptr;
     const int nown = h->grid() ? (int)h->piece : 0;
-    if (K == 16)
-      rk::sp::sp_gram_tc_k<16><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
-          nown);
-    else
-      rk::sp::sp_gram_tc_k<32><<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
-          h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown,
-          nown);
+    sp_gram_tc_of(K)<<<h->num_sms * rk::sp::SpGramTc::CPS, 256, rk::sp::SpGramTc::smem, h->stream>>>(
+        h->ctl, h->A32row, h->P, (int)h->rows_valid, (int)h->NR, (int)h->m, h->gchunks, h->gpart, skip, aown, nown);
     if (!(for_k2f && k2f_reduces(h))) {
       rk::sp::sp_gram_reduce<<<(unsigned)(h->m + 1), 256, 0, h->stream>>>(h->ctl, h->gpart, h->gchunks, K * K,
                                                                           h->red, skip);
@@ -963,7 +1006,7 @@ void launch_k2a(rk_handle* h, int skip, bool for_k2f = true) {
     h->launches += 1;
     return;
   }
-  if (h->fast || (h->grid() && (K == 16 || K == 32))) {
+  if ((h->fast && K <= 32) || (h->grid() && (K == 16 || K == 32))) {
     const float* aown = h->grid() ? h->A32row + (size_t)h->gj * h->piece * K : h->A32row;
     const int nown = h->grid() ? (int)h->piece : (int)h->NR;
     // P/Q already reduced (k1_reduce / SIMT K1 / sparse CSR pass)
@@ -1028,8 +1071,11 @@ void launch_k2f(rk_handle* h, int mode) {
   // after a launch_k2a(for_k2f) on a one-GPU tensor-core G / S path the
   // chunk partials are still unreduced: k2f sums them
   const double* gpart = k2f_reduces(h) ? h->gpart : nullptr;
-  if (!h->gscratch && (K == 16 || K == 32)) {
-    auto kern = K == 16 ? rk::k2f_fused_t<16> : rk::k2f_fused_t<32>;
+  if (!h->gscratch && k1_tc_k(K)) {
+    auto kern = K == 16 ? rk::k2f_fused_t<16>
+                : K == 32 ? rk::k2f_fused_t<32>
+                : K == 48 ? rk::k2f_fused_t<48>
+                          : rk::k2f_fused_t<64>;
     launch_pdl(kern, dim3((unsigned)h->m), dim3(rk::kThreads), k2f_smem(K), h->stream, h->ctl, h->red, h->R,
                h->Rnext, h->Mt, h->Mm, h->tt, rres, nres, h->trace_dev, (int)h->m, h->eps, mode,
                h->counters + h->m + 1, h->W32, gpart, h->gchunks);
@@ -1100,7 +1146,11 @@ void launch_k2b(rk_handle* h) {
     const int tg = rk::k2b_v4_tg(K, (int)h->m, h->NR);
     const size_t smem = (size_t)rk::kK2bStages * (2 * K * K + 2 * rb * K) * sizeof(float);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
-    if (K == 16)
+    if (K == 48 || K == 64) {  // (256 / K) thread rows of K columns: 240 threads at K = 48
+      launch_pdl(K == 48 ? rk::k2b_v4<48, 2> : rk::k2b_v4<64, 2>, dim3(blocks), dim3((256 / K) * K), smem,
+                 h->stream, h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, (const float*)h->P,
+                 (const float*)h->Q, (const float*)h->W32, (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+    } else if (K == 16)
       launch_pdl(rk::k2b_v4<16, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
                  h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
                  (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) k2f_fused(Ctl* __restrict__ ctl, dou
               gscratch, counter, W32, sh, t);
 }
 
-// k2f_fused with compile-time K (16 or 32; shared-memory scratch only)
+// k2f_fused with compile-time K (16, 32, 48, 64; shared-memory scratch only)
 template <int KT>
 __global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, double* __restrict__ gs,
                                                         double* __restrict__ R, double* __restrict__ Rnext,
@@ -615,7 +615,7 @@ inline size_t k2a_v4_smem(int K) {
   return (size_t)2 * warps * kBatchRows * K * sizeof(float);
 }
 
-// k2b_v4: A update for K in {16, 32}; P, Q plain. Per group of tg slices the
+// k2b_v4: A update for K in {16, 32, 48, 64}; P, Q plain. Per group of tg slices the
 // block stages W32 = [R_t^T ; R_t] (fp32, written by the K2f commit) and its
 // RB rows of P_t / Q_t in shared memory with coalesced float4 loads (one
 // latency per group); thread = (RPT rows, column c) then runs from shared
@@ -662,9 +662,9 @@ RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float*
                          __nv_bfloat16* __restrict__ ATh, __nv_bfloat16* __restrict__ ATl,
                          const float* __restrict__ P, const float* __restrict__ Q, const float* __restrict__ W32,
                          const double* __restrict__ Mm, int N, int M, int tg, double eps_m, int rbi, float* shf) {
-  static_assert(K == 16 || K == 32, "k2b_v4: K in {16, 32}");
+  static_assert(K == 16 || K == 32 || K == 48 || K == 64, "k2b_v4: K in {16, 32, 48, 64}");
   (void)tg;
-  constexpr int TR = 256 / K;   // thread rows
+  constexpr int TR = 256 / K;   // thread rows (launched with TR * K threads: 240 at K = 48)
   constexpr int RB = RPT * TR;  // rows per block
   constexpr int K4 = K / 4;
   constexpr int SF = k2b_v4_stage_floats<K, RPT>();  // [2][K][K] W, then [2][RB][K] P / Q rows

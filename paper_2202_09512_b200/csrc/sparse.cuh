@@ -304,9 +304,10 @@ struct SpGramTc {
   static constexpr size_t smem = (size_t)NS * 2 * ARR * sizeof(float);  // 48 KB (>= 8 warps x 256 doubles)
 };
 
-// KT = 32 (dense single GPU): each (slot, chunk) item is split into the four
-// 16 x 16 column quadrants of S (item-minor), each the K = 16 product above on
-// column slices of the 32-wide rows; quadrants write disjoint partial entries.
+// KT = 32 / 48 / 64 (dense): each (slot, chunk) item is split into the
+// (KT/16)^2 16 x 16 column blocks of S (item-minor), each the K = 16 product
+// above on column slices of the KT-wide rows; blocks write disjoint partial
+// entries.
 // Body over the items bid, bid + nblk, ... (also phase 2 of the fused
 // k-wide chain, k2_chain.cuh); gts: the block's >= SpGramTc::smem bytes.
 template <int KT>
@@ -316,7 +317,7 @@ RK_DEV void sp_gram_tc_body(const float* __restrict__ A32, const float* __restri
   // slot 0 (G) runs over Aown's nown rows when given (a grid rank's own piece
   // of A, rescal.py:124 with the grid's rank-ascending sum, dist_rescal.py:74-92)
   using C = SpGramTc;
-  static_assert(KT == 16 || KT == 32, "sp_gram_tc_k: K = 16 or 32");
+  static_assert(KT == 16 || KT == 32 || KT == 48 || KT == 64, "sp_gram_tc_k: K in {16, 32, 48, 64}");
   constexpr int NQ1 = KT / 16, NQ = NQ1 * NQ1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;

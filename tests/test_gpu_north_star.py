@@ -59,6 +59,16 @@ def test_cfg3_shape_matches_oracle():
     assert np.all(np.diff(trace) <= 1e-9), trace
 
 
+@pytest.mark.parametrize("k,k_pad,strip_tiles", [(40, 48, 6), (64, 64, 4), (20, 32, 11)])
+def test_auto_engine_uses_tensor_cores_up_to_k64(k, k_pad, strip_tiles):
+    eng = _lib.Engine(4096, 2, k, device=0)
+    try:
+        info = eng.info()
+    finally:
+        eng.close()
+    assert info["engine"] == 1 and info["k_pad"] == k_pad and info["strip_tiles"] == strip_tiles, info
+
+
 @pytest.mark.parametrize("qrot,q_bound", [("0", 6e-5), ("1", 1e-5)])
 def test_k1_slice_products_accuracy(monkeypatch, qrot, q_bound):
     """K1's P = X A and Q = X^T A against fp64 at n = 32768 (k = 32, one

@@ -136,14 +136,18 @@ def test_rescalk_selects_reference_k():
 
 
 @pytest.mark.parametrize("n,m,k,iters", [(1024, 4, 16, 20), (640, 3, 32, 15), (1100, 2, 27, 10), (200, 2, 5, 30),
-                                         (300, 2, 40, 8), (400, 2, 130, 4)])
+                                         (300, 2, 40, 8), (1300, 3, 48, 6), (700, 2, 64, 8), (2200, 2, 57, 4),
+                                         (400, 2, 130, 4)])
 def test_engines_match_oracle_midsize(n, m, k, iters):
+    """k_pad 48 / 64 (k = 33..64) run K1 on tensor cores too (K1<48> with 6,
+    K1<64> with 4 column tiles per strip; several strips here); k = 130 is
+    SIMT only."""
     x = uniform_x(m, n, 7).astype(np.float64)
     a0, r0 = oracle.random_init(n, k, m, 3)
     ao, ro, tro = oracle.solve([x[t] for t in range(m)], k, oracle.OracleConfig(max_iters=iters),
                                initial=(a0, r0))
     for engine in ("tc", "simt"):
-        if engine == "tc" and k > 32:
+        if engine == "tc" and k > 64:
             continue
         f, tr = _solve(x, k, iters, a0, r0, engine=engine)
         assert rel_fro(f.A, ao) <= TOL_F, engine

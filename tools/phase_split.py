@@ -8,7 +8,7 @@ from paper_2202_09512_b200 import _lib
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n, m, k, sparse = {"cfg1": (256, 8, 4, False), "cfg5": (16384, 8, 16, False),
-                   "cfg2": (8192, 16, 16, False), "cfg3": (32768, 16, 32, False), "k32m": (16384, 16, 32, False),
+                   "cfg2": (8192, 16, 16, False), "k48": (8192, 16, 48, False), "k64": (8192, 16, 64, False), "cfg3": (32768, 16, 32, False), "k32m": (16384, 16, 32, False),
                    "cfg4": (1 << 20, 32, 16, True), "cfg4k32": (1 << 20, 32, 32, True)}[cfg]
 eng = _lib.Engine(n, m, k, device=0, sparse=sparse)
 if sparse:
