@@ -367,7 +367,7 @@ bool k1_tc_k(int K);
 bool dense_gram_tc(const rk_handle* h) { return !h->sparse && k1_tc_k(h->K); }
 
 size_t k2f_smem(int K) {
-  size_t s = (size_t)5 * K * K * sizeof(double);
+  size_t s = (size_t)5 * K * (K + 1) * sizeof(double);  // row stride K + 1 (mm_kk_t)
   return s <= 200 * 1024 ? s : 0;
 }
 

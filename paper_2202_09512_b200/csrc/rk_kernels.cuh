@@ -39,22 +39,45 @@ RK_DEV void mm_kk(double* __restrict__ C, const double* __restrict__ A, bool ta,
   }
 }
 
-// C = op(A) op(B) for compile-time K (shared-memory operands); the same
-// ascending-l fma chain as mm_kk, so the results are bit-identical to it.
+// C = op(A) op(B) for compile-time K in {16, 32, 48, 64} on shared-memory
+// operands stored with row stride K + 1 doubles (odd: a warp reading down a
+// column hits 16 distinct banks, so op = transpose costs no conflicts). The
+// 256 threads form a 16 x 16 grid; thread (ti, tj) owns the T x T outputs
+// (ti + 16 a, tj + 16 b), T = K / 16, as T^2 independent fma chains. Each
+// output is the same ascending-l fma chain as mm_kk: bit-identical results.
 template <int K>
 RK_DEV void mm_kk_t(double* __restrict__ C, const double* __restrict__ A, bool ta,
                     const double* __restrict__ B, bool tb) {
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, j = e % K;
-    double s = 0.0;
+  static_assert(K % 16 == 0 && K <= 64, "mm_kk_t: K in {16, 32, 48, 64}");
+  constexpr int LD = K + 1, T = K / 16;
+  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+  double s[T][T];
 #pragma unroll
-    for (int l = 0; l < K; ++l) {
-      const double a = ta ? A[l * K + i] : A[i * K + l];
-      const double bb = tb ? B[j * K + l] : B[l * K + j];
-      s = fma(a, bb, s);
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = 0; b < T; ++b) s[a][b] = 0.0;
+#pragma unroll 4
+  for (int l = 0; l < K; ++l) {
+    double av[T], bv[T];
+#pragma unroll
+    for (int a = 0; a < T; ++a) {
+      const int i = ti + 16 * a;
+      av[a] = ta ? A[l * LD + i] : A[i * LD + l];
     }
-    C[e] = s;
+#pragma unroll
+    for (int b = 0; b < T; ++b) {
+      const int j = tj + 16 * b;
+      bv[b] = tb ? B[j * LD + l] : B[l * LD + j];
+    }
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+      for (int b = 0; b < T; ++b) s[a][b] = fma(av[a], bv[b], s[a][b]);
   }
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int b = 0; b < T; ++b) C[(ti + 16 * a) * LD + tj + 16 * b] = s[a][b];
 }
 
 RK_DEV double block_sum(double v, double* scratch) {
@@ -193,16 +216,21 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
     else mm_kk(C, A, ta, B, tb, K);
   };
   const int KK = K * K;
+  // the five K x K scratch matrices; compile-time K stores them with row
+  // stride K + 1 (mm_kk_t), at(e) maps a row-major index e into them
+  const int LD = KT ? KT + 1 : K;
+  const int AS = K * LD;
+  auto at = [&](int e) { return KT ? (e / KT) * LD + (e - (e / KT) * KT) : e; };
   double* base = gscratch ? gscratch + (size_t)t * 5 * KK : sh;
   double* G = base;
-  double* Rt = base + KK;
-  double* T1 = base + 2 * KK;
-  double* T2 = base + 3 * KK;
-  double* Rn = base + 4 * KK;
+  double* Rt = base + AS;
+  double* T1 = base + 2 * AS;
+  double* T2 = base + 3 * AS;
+  double* Rn = base + 4 * AS;
   const double* S = gsS;  // S_t (gs + (1 + t) K^2 of the reduced [G, S_1..S_m])
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    G[e] = gsG[e];
-    Rt[e] = R[(size_t)t * KK + e];
+    G[at(e)] = gsG[e];
+    Rt[at(e)] = R[(size_t)t * KK + e];
   }
   __syncthreads();
   mm(T1, Rt, false, G, false);  // R G
@@ -211,8 +239,8 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
   __syncthreads();
   double rs = 0.0, rgrg = 0.0;
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    rs += Rt[e] * S[e];
-    rgrg += Rt[e] * T2[e];
+    rs += Rt[at(e)] * S[e];
+    rgrg += Rt[at(e)] * T2[at(e)];
   }
   rs = block_sum(rs, red);
   rgrg = block_sum(rgrg, red);
@@ -222,8 +250,8 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
   }
   if (mode != 1) {
     for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-      double v = mode == 3 ? Rt[e] : Rt[e] * S[e] / (T2[e] + eps);
-      Rn[e] = v;
+      double v = mode == 3 ? Rt[at(e)] : Rt[at(e)] * S[e] / (T2[at(e)] + eps);
+      Rn[at(e)] = v;
       Rnext[(size_t)t * KK + e] = v;
     }
     __syncthreads();
@@ -235,7 +263,7 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
     __syncthreads();
     mm(Rt, Rn, false, T1, false);  // R' G R'^T
     __syncthreads();
-    for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[e] + Rt[e];
+    for (int e = threadIdx.x; e < KK; e += blockDim.x) Mt[(size_t)t * KK + e] = T2[at(e)] + Rt[at(e)];
   }
   // ---- last block: trace / stop / commit (former K2m) ----
   __threadfence();
@@ -375,7 +403,8 @@ __global__ void __launch_bounds__(kThreads) k2f_fused_t(Ctl* __restrict__ ctl, d
   extern __shared__ double sh[];
   const int t = blockIdx.x;
   constexpr int KK = KT * KT;
-  const double* G = gpart ? k2f_reduce_parts(gpart, gchunks, gs, sh, KK, t) : gs;
+  // the chunk sums of G go to T2's scratch (free until after G is copied in)
+  const double* G = gpart ? k2f_reduce_parts(gpart, gchunks, gs, sh + 3 * KT * (KT + 1), KK, t) : gs;
   k2f_body<KT>(ctl, G, gs + (size_t)(1 + t) * KK, R, Rnext, Mt, Mout, tt, rres, nres, trace, KT, M, eps, mode,
                nullptr, counter, W32, sh, t);
 }

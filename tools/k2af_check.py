@@ -13,7 +13,7 @@ from paper_2202_09512_b200 import _lib
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n, m, k = {"cfg1": (256, 8, 4), "cfg5": (16384, 8, 16), "cfg2": (8192, 16, 16),
            "cfg3": (32768, 16, 32), "k32s": (4096, 8, 32), "k20": (2048, 4, 20),
-           "k32m": (16384, 16, 32)}[cfg]
+           "k32m": (16384, 16, 32), "k48": (8192, 16, 48), "k64": (8192, 16, 64)}[cfg]
 eng = _lib.Engine(n, m, k, device=0)
 eng.fill_uniform(1)
 f0 = rk.random_init(n, k, m, 0)
