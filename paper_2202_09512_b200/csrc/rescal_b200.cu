@@ -429,6 +429,18 @@ K1Kernel k1_kernel_of(const rk_handle* h) {
 
 bool k1_tc_k(int K) { return K == 16 || K == 32 || K == 48 || K == 64; }
 
+using K2bKernel = void (*)(rk::Ctl*, double*, float*, __nv_bfloat16*, __nv_bfloat16*, const float*, const float*,
+                          const float*, const double*, int, int, int, double);
+K2bKernel k2b_v4_of(int K, int rpt) {
+  using namespace rk;
+  switch (K) {
+    case 16: return rpt > 1 ? k2b_v4<16, 2> : k2b_v4<16, 1>;
+    case 48: return rpt > 1 ? k2b_v4<48, 3> : k2b_v4<48, 1>;
+    case 64: return rpt > 1 ? k2b_v4<64, 4> : k2b_v4<64, 1>;
+    default: return rpt > 1 ? k2b_v4<32, 2> : k2b_v4<32, 1>;
+  }
+}
+
 using SpGramTcKernel = void (*)(const rk::Ctl*, const float*, const float*, int, int, int, int, double*, int,
                                 const float*, int);
 SpGramTcKernel sp_gram_tc_of(int K) {
@@ -716,24 +728,13 @@ void alloc_factor_buffers(rk_handle* h) {
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
     else
       RK_CUDA(cudaFuncSetAttribute(rk::k2b_u4<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smu));
-    const int rb = rk::k2b_v4_rb(K, h->NR);
-    const int tg = rk::k2b_v4_tg(K, (int)M, h->NR);
-    const int smem = rk::kK2bStages * (2 * K * K + 2 * rb * K) * (int)sizeof(float);
-    (void)tg;
-    if (K == 16)
-      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    else if (rk::k2b_v4_rpt(K, h->NR) == 8)
-      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    else
-      RK_CUDA(cudaFuncSetAttribute(rk::k2b_v4<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
-  if (K == 48 || K == 64) {
-    const int smem = rk::kK2bStages * (2 * K * K + 2 * rk::k2b_v4_rb(K, h->NR) * K) * (int)sizeof(float);
-    RK_CUDA(cudaFuncSetAttribute(K == 48 ? rk::k2b_v4<48, 2> : rk::k2b_v4<64, 2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (h->fast)
+    RK_CUDA(cudaFuncSetAttribute(k2b_v4_of(K, rk::k2b_v4_rpt(K, h->NR)), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rk::k2b_v4_smem(K, h->NR)));
+  if (K == 48 || K == 64)
     RK_CUDA(cudaFuncSetAttribute(K == 48 ? rk::k2f_fused_t<48> : rk::k2f_fused_t<64>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2f_smem(K)));
-  }
   const size_t k2bs = (size_t)(K <= 128 ? K * (K + 1) : 0) * 8 + 2 * (256 / K) * K * 4;
   RK_CUDA(cudaFuncSetAttribute(rk::k2b_update_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2bs));
   const size_t k2ps = (size_t)K * (K + 1) * 8 + (256 / K) * K * 4;
@@ -1143,25 +1144,11 @@ void launch_k2b(rk_handle* h) {
   }
   if (h->fast) {
     const int rb = rk::k2b_v4_rb(K, h->NR);
-    const int tg = rk::k2b_v4_tg(K, (int)h->m, h->NR);
-    const size_t smem = (size_t)rk::kK2bStages * (2 * K * K + 2 * rb * K) * sizeof(float);
     const unsigned blocks = (unsigned)((h->NR + rb - 1) / rb);
-    if (K == 48 || K == 64) {  // (256 / K) thread rows of K columns: 240 threads at K = 48
-      launch_pdl(K == 48 ? rk::k2b_v4<48, 2> : rk::k2b_v4<64, 2>, dim3(blocks), dim3((256 / K) * K), smem,
-                 h->stream, h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row, (const float*)h->P,
-                 (const float*)h->Q, (const float*)h->W32, (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
-    } else if (K == 16)
-      launch_pdl(rk::k2b_v4<16, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
-                 h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
-                 (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
-    else if (rk::k2b_v4_rpt(K, h->NR) == 8)
-      launch_pdl(rk::k2b_v4<32, 8>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
-                 h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
-                 (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
-    else
-      launch_pdl(rk::k2b_v4<32, 2>, dim3(blocks), dim3(256), smem, h->stream, h->ctl, h->Arow, h->A32row,
-                 h->ATh_row, h->ATl_row, (const float*)h->P, (const float*)h->Q, (const float*)h->W32,
-                 (const double*)h->Mm, (int)h->NR, (int)h->m, tg, eps_m);
+    launch_pdl(k2b_v4_of(K, rk::k2b_v4_rpt(K, h->NR)), dim3(blocks), dim3(rk::k2b_v4_threads(K)),
+               rk::k2b_v4_smem(K, h->NR), h->stream, h->ctl, h->Arow, h->A32row, h->ATh_row, h->ATl_row,
+               (const float*)h->P, (const float*)h->Q, (const float*)h->W32, (const double*)h->Mm, (int)h->NR,
+               (int)h->m, 0, eps_m);
     RK_CUDA(cudaGetLastError());
     h->launches += 1;
     return;

@@ -59,6 +59,32 @@ RK_DEV double sum_chunks(const double* __restrict__ p, int nchunk, int stride) {
   return v;
 }
 
+// sum_chunks for NG elements at once (p[i], valid[i]): the same per-element
+// order (bit-identical), with the 8-chunk batches of all NG elements in
+// flight together (latency-bound reductions: NG x more loads per round trip).
+template <int NG>
+RK_DEV void sum_chunks_group(const double* const (&p)[NG], const bool (&valid)[NG], int nchunk, int stride,
+                             double (&out)[NG]) {
+#pragma unroll
+  for (int i = 0; i < NG; ++i) out[i] = 0.0;
+  int c = 0;
+  for (; c + 8 <= nchunk; c += 8) {
+    double x[NG][8];
+#pragma unroll
+    for (int i = 0; i < NG; ++i)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[i][u] = valid[i] ? __ldcg(p[i] + (size_t)(c + u) * stride) : 0.0;
+#pragma unroll
+    for (int i = 0; i < NG; ++i)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) out[i] += x[i][u];
+  }
+  for (; c < nchunk; ++c)
+#pragma unroll
+    for (int i = 0; i < NG; ++i)
+      if (valid[i]) out[i] += __ldcg(p[i] + (size_t)c * stride);
+}
+
 RK_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -360,11 +360,30 @@ RK_DEV void k2f_body(Ctl* __restrict__ ctl,
 // of gs (block 0 also writes G's slot).
 RK_DEV const double* k2f_reduce_parts(const double* __restrict__ gpart, int gchunks, double* __restrict__ gs,
                                       double* Gdst, int KK, int t) {
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    const double g = sum_chunks(gpart + e, gchunks, KK);
-    Gdst[e] = g;
-    if (t == 0) gs[e] = g;
-    gs[(size_t)(1 + t) * KK + e] = sum_chunks(gpart + (size_t)(1 + t) * gchunks * KK + e, gchunks, KK);
+  // 4 entries of G and the same 4 of S_t per thread and round: 64 loads in
+  // flight per thread (sum_chunks_group; sum_chunks' order, bit-identical)
+  const double* sbase = gpart + (size_t)(1 + t) * gchunks * KK;
+  for (int e0 = threadIdx.x; e0 < KK; e0 += 4 * blockDim.x) {
+    const double* p[8];
+    bool ok[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q * blockDim.x;
+      ok[q] = ok[4 + q] = e < KK;
+      p[q] = gpart + (ok[q] ? e : 0);
+      p[4 + q] = sbase + (ok[q] ? e : 0);
+    }
+    double v[8];
+    sum_chunks_group<8>(p, ok, gchunks, KK, v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q * blockDim.x;
+      if (e < KK) {
+        Gdst[e] = v[q];
+        if (t == 0) gs[e] = v[q];
+        gs[(size_t)(1 + t) * KK + e] = v[4 + q];
+      }
+    }
   }
   __syncthreads();
   return Gdst;
@@ -644,19 +663,41 @@ inline size_t k2a_v4_smem(int K) {
   return (size_t)2 * warps * kBatchRows * K * sizeof(float);
 }
 
-// k2b_v4: A update for K in {16, 32, 48, 64}; P, Q plain. Per group of tg slices the
-// block stages W32 = [R_t^T ; R_t] (fp32, written by the K2f commit) and its
-// RB rows of P_t / Q_t in shared memory with coalesced float4 loads (one
-// latency per group); thread = (RPT rows, column c) then runs from shared
-// memory: every W value feeds RPT rows, P/Q reads are broadcasts. RPT = 8 at
-// K = 32 (64-row blocks) so the 8 KB-per-slice W is staged once per 64 rows,
-// not per 16 (the 16-row version was L1/shared-memory bound on W staging).
-// The per-row arithmetic (order of every fma and add) does not depend on RPT.
-// RPT = 8 only pays while the 64-row blocks still fill two waves of the GPU
-// (n >= 2 * 148 * 64); smaller K = 32 blocks keep RPT = 2 (16-row blocks).
-inline int k2b_v4_rpt(int K, int64_t N) { return (K == 32 && N >= 2 * 148 * 64) ? 8 : 2; }
+// k2b_v4: A update for K in {16, 32, 48, 64}; P, Q plain.
+//   num_i = sum_t P_t[i] R_t^T + Q_t[i] R_t,  A_i <- A_i * num_i / (A_i M + m eps)
+// Thread = (4 consecutive columns 4cg .. 4cg + 3, RPT rows rl + j TRW) with
+// cg = tid mod K/4 fastest, so a warp reads few P/Q rows (K/4 lanes share one
+// float4) and its W = [R_t^T ; R_t] float4 loads are distinct lanes of one
+// row: per 16 columns x k-step, 2 RPT + 8 shared-memory wavefronts feed
+// 32 RPT FFMAs (the one-column mapping of round 1 was LSU-bound: 24 per 64).
+// P/Q rows sit in shared memory with stride K + 4 floats (conflict-free).
+// Per slice t the block stages W_t and its RB rows of P_t and Q_t into one of
+// kK2bStages stages with cp.async, kK2bStages - 1 slices ahead. The per-output
+// arithmetic -- per slice an fp32 fma chain over the 2K terms in d order,
+// added to fp64 per slice in slice order; the fp64 denominator chain over d --
+// is the same for every mapping (bit-identical factors across versions).
+constexpr int kK2bStages = 3;
 
-inline int k2b_v4_rb(int K, int64_t N) { return k2b_v4_rpt(K, N) * (256 / K); }
+// thread rows TR x column groups CG: 32 x 4 (128 threads) at K = 16,
+// 32 x 8 at 32, 20 x 12 (240) at 48, 16 x 16 at 64
+__host__ __device__ constexpr int k2b_v4_tr(int K) { return K == 48 ? 20 : K == 64 ? 16 : 32; }
+
+template <int K>
+struct K2bMap {
+  static constexpr int CG = K / 4;                 // column groups (4 columns each)
+  static constexpr int TR = k2b_v4_tr(K);          // thread rows
+  static constexpr int LDP = K + 4;                // P/Q row stride in shared memory
+};
+
+inline int k2b_v4_threads(int K) { return k2b_v4_tr(K) * K / 4; }
+
+// rows per thread: the ~64-row blocks only while they still fill two waves
+inline int k2b_v4_rpt(int K, int64_t N) {
+  const int big = K == 48 ? 3 : 64 / k2b_v4_tr(K);
+  return N >= (int64_t)2 * 148 * k2b_v4_tr(K) * big ? big : 1;
+}
+
+inline int k2b_v4_rb(int K, int64_t N) { return k2b_v4_rpt(K, N) * k2b_v4_tr(K); }
 
 // One row block `rbi` (also the last phase of the fused k-wide chain,
 // k2_chain.cuh, where P / Q / W32 were written earlier in the same launch:
@@ -666,17 +707,14 @@ RK_DEV T ld_pq(const T* p, bool coh) {
   return coh ? __ldcg(p) : __ldg(p);
 }
 
-// Per slice t the block stages W_t = [R_t^T ; R_t] (fp32, 2K^2) and its RB
-// rows of P_t and Q_t (2 RB K floats) into one of kK2bStages shared-memory
-// stages with cp.async, kK2bStages - 1 slices ahead of the one it computes
-// (the loads of later slices overlap the FMAs of this one). The arithmetic --
-// per slice an fp32 sum over the 2K terms, added to fp64 per slice in slice
-// order -- does not depend on the staging.
-constexpr int kK2bStages = 3;
-
 template <int K, int RPT>
 __host__ __device__ constexpr int k2b_v4_stage_floats() {
-  return 2 * K * K + 2 * RPT * (256 / K) * K;
+  return 2 * K * K + 2 * RPT * K2bMap<K>::TR * K2bMap<K>::LDP;
+}
+
+inline size_t k2b_v4_smem(int K, int64_t N) {
+  const int rb = k2b_v4_rb(K, N);
+  return (size_t)kK2bStages * (2 * K * K + 2 * rb * (K + 4)) * sizeof(float);
 }
 
 RK_DEV void k2b_cp16(float* dst, const float* src) {
@@ -693,27 +731,32 @@ RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float*
                          const double* __restrict__ Mm, int N, int M, int tg, double eps_m, int rbi, float* shf) {
   static_assert(K == 16 || K == 32 || K == 48 || K == 64, "k2b_v4: K in {16, 32, 48, 64}");
   (void)tg;
-  constexpr int TR = 256 / K;   // thread rows (launched with TR * K threads: 240 at K = 48)
+  using Map = K2bMap<K>;
+  constexpr int CG = Map::CG, TR = Map::TR, LDP = Map::LDP;
   constexpr int RB = RPT * TR;  // rows per block
   constexpr int K4 = K / 4;
-  constexpr int SF = k2b_v4_stage_floats<K, RPT>();  // [2][K][K] W, then [2][RB][K] P / Q rows
-  const int rl = threadIdx.x / K, c = threadIdx.x - rl * K;
+  constexpr int SF = k2b_v4_stage_floats<K, RPT>();  // [2][K][K] W, then [2][RB][LDP] P / Q rows
+  const int tid = threadIdx.x;
+  const int cg = tid % CG, rl = tid / CG;
+  const bool active = rl < TR;
   const int rbase = rbi * RB;
   auto issue = [&](int t) {
     float* st = shf + (size_t)(t % kK2bStages) * SF;
     const float* w = W32 + (size_t)t * 2 * K * K;
-    for (int e = threadIdx.x; e < 2 * K * K / 4; e += blockDim.x) k2b_cp16(st + 4 * e, w + 4 * e);
+    for (int e = tid; e < 2 * K * K / 4; e += blockDim.x) k2b_cp16(st + 4 * e, w + 4 * e);
     float* pq = st + 2 * K * K;
-    for (int e = threadIdx.x; e < 2 * RB * K4; e += blockDim.x) {
+    for (int e = tid; e < 2 * RB * K4; e += blockDim.x) {
       const int which = e / (RB * K4), rem = e - which * RB * K4;
       const int r = rem / K4, qq = rem - r * K4;
-      const int row = min(rbase + r, N - 1);  // N is a multiple of RB on the dense engine
-      k2b_cp16(pq + 4 * e, (which ? Q : P) + ((size_t)t * N + row) * K + 4 * qq);
+      const int row = min(rbase + r, N - 1);  // rows >= N are discarded below
+      k2b_cp16(pq + (which * RB + r) * LDP + 4 * qq, (which ? Q : P) + ((size_t)t * N + row) * K + 4 * qq);
     }
   };
-  double nacc[RPT];
+  double nacc[RPT][4];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) nacc[j] = 0.0;
+  for (int j = 0; j < RPT; ++j)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) nacc[j][u] = 0.0;
   __syncthreads();  // the previous row block's stages are consumed
 #pragma unroll
   for (int t = 0; t < kK2bStages - 1; ++t) {
@@ -727,48 +770,66 @@ RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float*
     __syncthreads();
     const float* WrT = shf + (size_t)(t % kK2bStages) * SF;  // [d][c] = R_t[c][d]
     const float* Wr = WrT + K * K;                           // [d][c] = R_t[d][c]
-    const float* pr = WrT + 2 * K * K + (size_t)rl * K;      // row rl + j*TR at + j*TR*K
-    const float* qr = pr + (size_t)RB * K;
-    {
-      float sacc[RPT];
+    const float* pr = WrT + 2 * K * K + (size_t)rl * LDP;    // row rl + j TR at + j TR LDP
+    const float* qr = pr + (size_t)RB * LDP;
+    if (active) {
+      float sacc[RPT][4];
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) sacc[j] = 0.f;
+      for (int j = 0; j < RPT; ++j)
 #pragma unroll
+        for (int u = 0; u < 4; ++u) sacc[j][u] = 0.f;
+#pragma unroll 2
       for (int d4 = 0; d4 < K4; ++d4) {
-        float wr[4], wq[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          wr[q] = WrT[(d4 * 4 + q) * K + c];
-          wq[q] = Wr[(d4 * 4 + q) * K + c];
-        }
+        float4 p4[RPT], q4[RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-          const float4 a = *reinterpret_cast<const float4*>(pr + (size_t)j * TR * K + 4 * d4);
-          const float4 b = *reinterpret_cast<const float4*>(qr + (size_t)j * TR * K + 4 * d4);
-          const float pa[4] = {a.x, a.y, a.z, a.w};
-          const float qa[4] = {b.x, b.y, b.z, b.w};
+          p4[j] = *reinterpret_cast<const float4*>(pr + (size_t)j * TR * LDP + 4 * d4);
+          q4[j] = *reinterpret_cast<const float4*>(qr + (size_t)j * TR * LDP + 4 * d4);
+        }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) sacc[j] = fmaf(pa[q], wr[q], fmaf(qa[q], wq[q], sacc[j]));
+        for (int q = 0; q < 4; ++q) {
+          const float4 wr4 = *reinterpret_cast<const float4*>(WrT + (d4 * 4 + q) * K + 4 * cg);
+          const float4 wq4 = *reinterpret_cast<const float4*>(Wr + (d4 * 4 + q) * K + 4 * cg);
+          const float wr[4] = {wr4.x, wr4.y, wr4.z, wr4.w};
+          const float wq[4] = {wq4.x, wq4.y, wq4.z, wq4.w};
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const float pa = q == 0 ? p4[j].x : q == 1 ? p4[j].y : q == 2 ? p4[j].z : p4[j].w;
+            const float qa = q == 0 ? q4[j].x : q == 1 ? q4[j].y : q == 2 ? q4[j].z : q4[j].w;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sacc[j][u] = fmaf(pa, wr[u], fmaf(qa, wq[u], sacc[j][u]));
+          }
         }
       }
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) nacc[j] += (double)sacc[j];
+      for (int j = 0; j < RPT; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) nacc[j][u] += (double)sacc[j][u];
     }
     __syncthreads();  // stage t % kK2bStages is refilled by a later iteration
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  double an[RPT];
+  double an[RPT][4];
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int i = rbase + rl + j * TR;
-    an[j] = 0.0;
-    if (i < N) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) an[j][u] = 0.0;
+    if (active && i < N) {
       const double* Ai = A64 + (size_t)i * K;
-      double deno = eps_m;
-      for (int d = 0; d < K; ++d) deno = fma(Ai[d], COH ? __ldcg(Mm + d * K + c) : Mm[d * K + c], deno);
-      an[j] = Ai[c] * nacc[j] / deno;
-      if (!isfinite(an[j])) bad = true;
+      double deno[4] = {eps_m, eps_m, eps_m, eps_m};
+      for (int d = 0; d < K; ++d) {
+        const double a = Ai[d];
+        const double* mrow = Mm + d * K + 4 * cg;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) deno[u] = fma(a, COH ? __ldcg(mrow + u) : mrow[u], deno[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        an[j][u] = Ai[4 * cg + u] * nacc[j][u] / deno[u];
+        if (!isfinite(an[j][u])) bad = true;
+      }
     }
   }
   if (bad) {
@@ -779,13 +840,17 @@ RK_DEV void k2b_v4_block(Ctl* __restrict__ ctl, double* __restrict__ A64, float*
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int i = rbase + rl + j * TR;
-    if (i < N) {
-      A64[(size_t)i * K + c] = an[j];
-      A32[(size_t)i * K + c] = (float)an[j];
-      __nv_bfloat16 hi, lo;
-      split_bf16(an[j], hi, lo);
-      ATh[(size_t)c * N + i] = hi;
-      ATl[(size_t)c * N + i] = lo;
+    if (active && i < N) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = 4 * cg + u;
+        A64[(size_t)i * K + c] = an[j][u];
+        A32[(size_t)i * K + c] = (float)an[j][u];
+        __nv_bfloat16 hi, lo;
+        split_bf16(an[j][u], hi, lo);
+        ATh[(size_t)c * N + i] = hi;
+        ATl[(size_t)c * N + i] = lo;
+      }
     }
   }
 }
@@ -896,11 +961,6 @@ inline int k2b_u4_tg(int K, int M) {
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (48 * 1024) / per));
 }
 
-inline int k2b_v4_tg(int K, int M, int64_t N) {
-  const int RB = k2b_v4_rb(K, N);
-  const size_t per = (size_t)(2 * K * K + 2 * RB * K) * sizeof(float);
-  return (int)std::max<size_t>(1, std::min<size_t>((size_t)M, (96 * 1024) / per));
-}
 
 // ---------------------------------------------------------------------------
 // K2b: accumulated A update (rescal.py:133-145), one thread per (row, column):
