@@ -21,7 +21,8 @@ GRID = tuple(int(v) for v in _gs.lower().split("x")) if _gs else None
 results = []
 ok = True
 for (n, m, k, iters, engine) in [(300, 3, 5, 30, "auto"), (1000, 2, 16, 20, "auto"), (700, 2, 32, 12, "auto"),
-                                 (257, 2, 4, 25, "simt"), (300, 2, 40, 8, "auto")]:
+                                 (257, 2, 4, 25, "simt"), (300, 2, 40, 8, "auto"),
+                                 (600, 2, 64, 6, "auto")]:
     x = np.random.default_rng(n).random((m, n, n), dtype=np.float32).astype(np.float64)
     f0 = rk.random_init(n, k, m, 1)
     f, tr, info = rk.solve_on_grid(rk.RelTensor(x), k, rk.SolverConfig(max_iters=iters, engine=engine),
