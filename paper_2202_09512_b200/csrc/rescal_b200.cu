@@ -299,6 +299,10 @@ struct rk_handle {
   int nnp = 0;
   // tcgen05 schedule
   int c = 0, nstrips = 0, grid_tc = 0, nslots = 0, qrot = 1;
+  int sw = 0;           // K1 column tiles per strip (c, or up to 2c with paired strips)
+  bool k1_pair = false; // K1 paired strips
+  float* Pscr = nullptr;      // paired strips: the odd CTAs' P tiles
+  unsigned* pflag = nullptr;  // paired strips: produced / consumed counters
   bool k1_mq = true;  // K1 merges the Q hi/lo operands (always at K = 16; see k1_merge_q)
   size_t smem_tc = 0;
   float *Ppart = nullptr, *Qpart = nullptr;
@@ -383,8 +387,10 @@ void free_factor_buffers(rk_handle* h) {
                   h->part, h->red, h->gscratch, h->counters, h->W32, h->d_simt_first,
                   h->d_simt_count, h->UI, h->UJ, h->regS, h->regG, h->regT,
                   h->regRn, h->P, h->Q, h->rpart, h->Ppart, h->Qpart, h->d_cta_begin,
-                  h->d_cta_slot, h->d_slot_first, h->d_slot_count};
+                  h->d_cta_slot, h->d_slot_first, h->d_slot_count, h->Pscr, h->pflag};
   for (void* p : ptrs) dfree(p);
+  h->Pscr = nullptr;
+  h->pflag = nullptr;
   if (h->Acol != h->Arow) dfree(h->Acol);
   if (h->A32col != h->A32row) dfree(h->A32col);
   if (h->ATh_col != h->ATh_row) dfree(h->ATh_col);
@@ -492,6 +498,13 @@ int k1_qrot() {
   return e ? std::max(0, std::atoi(e)) : 0;
 }
 
+// Paired strips in K1 (RK_K1_PAIR=0 turns them off: measurement only).
+constexpr int kPairMinStrips = 16;
+bool k1_pair_on() {
+  const char* e = std::getenv("RK_K1_PAIR");
+  return e ? std::atoi(e) != 0 : true;
+}
+
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
 void plan_tc(rk_handle* h) {
   const int K = h->K;
@@ -510,69 +523,96 @@ void plan_tc(rk_handle* h) {
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
   nstrips = (ncb + c - 1) / c;
+  // Paired strips (k1_tc.cuh): for wide tensors (>= 16 strips) two CTAs
+  // share a strip of up to 2 c tiles and write ONE P partial for it (half
+  // the partial traffic). On narrower ones the pair coupling costs more K1
+  // time than the partials save (cfg2: K1 +7 %, profiles/r02_pairs.md).
+  const bool pair = nstrips >= kPairMinStrips && k1_pair_on();
+  int sw = c;
+  if (pair) {
+    nstrips = (ncb + 2 * cmax - 1) / (2 * cmax);
+    sw = (ncb + nstrips - 1) / nstrips;
+    nstrips = (ncb + sw - 1) / sw;
+    c = (sw + 1) / 2;
+  }
   if (c > rk::tc::kMaxC) throw std::runtime_error("K1 strip wider than kMaxC tiles");
   h->c = c;
+  h->sw = sw;
+  h->k1_pair = pair;
   h->nstrips = nstrips;
   const int64_t n_items = (int64_t)M * nstrips * nrb;
-  auto tiles_of = [&](int64_t item) {
-    int s = (int)((item / nrb) % nstrips);
-    return s == nstrips - 1 ? ncb - c * (nstrips - 1) : c;
+  auto tiles_of = [&](int64_t item, int half) {
+    int ct, toff;
+    rk::tc::k1_half_tiles((int)((item / nrb) % nstrips), nstrips, sw, ncb, pair ? 1 : 0, half, ct, toff);
+    return ct;
   };
   int64_t total = 0;
-  for (int64_t it = 0; it < n_items; ++it) total += tiles_of(it);
-  const int grid = (int)std::min<int64_t>(h->num_sms, n_items);
-  std::vector<int> begin(grid + 1, 0);
+  for (int64_t it = 0; it < n_items; ++it) total += tiles_of(it, 0);
+  // item ranges: one per CTA, or one per CTA pair (both CTAs walk it)
+  const int ranges = (int)std::min<int64_t>(pair ? h->num_sms / 2 : h->num_sms, n_items);
+  const int grid = pair ? 2 * ranges : ranges;
+  std::vector<int> begin(ranges + 1, 0);
   int64_t cum = 0, it = 0;
-  for (int g = 0; g < grid; ++g) {
+  for (int g = 0; g < ranges; ++g) {
     begin[g] = (int)it;
-    const int64_t target = total * (g + 1) / grid;
-    while (it < n_items && cum + tiles_of(it) <= target) cum += tiles_of(it++);
-    if (it == begin[g] && it < n_items) cum += tiles_of(it++);  // at least one item
+    const int64_t target = total * (g + 1) / ranges;
+    while (it < n_items && cum + tiles_of(it, 0) <= target) cum += tiles_of(it++, 0);
+    if (it == begin[g] && it < n_items) cum += tiles_of(it++, 0);  // at least one item
   }
-  begin[grid] = (int)n_items;
+  begin[ranges] = (int)n_items;
   // slots: one per (CTA, (t, strip) run) in item order, plus a fresh one for
   // a CTA's final drain when its last run already stored (mirrors the
-  // epilogue's rule in k1_tc.cuh exactly)
+  // epilogue's rule in k1_tc.cuh exactly). Keys (t, strip[, half]); with
+  // pairs all even CTAs are numbered first, so every key's slots are
+  // consecutive (k1_reduce_q4).
   h->qrot = K <= 32 ? k1_qrot() : 0;
-  std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips, 0), slot_count(M * nstrips, 0);
+  const int halves = pair ? 2 : 1;
+  std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips * halves, 0), slot_count(M * nstrips * halves, 0);
   int slots = 0;
-  auto new_slot = [&](int ts) {
-    if (slot_count[ts] == 0) slot_first[ts] = slots;
-    slot_count[ts] += 1;
+  auto new_slot = [&](int key) {
+    if (slot_count[key] == 0) slot_first[key] = slots;
+    slot_count[key] += 1;
     ++slots;
   };
-  for (int g = 0; g < grid; ++g) {
-    cta_slot[g] = slots;
-    int slot_ts = -1;
-    bool stored = false;
-    for (int i = begin[g]; i < begin[g + 1]; ++i) {
-      const int ts = i / nrb, rb = i % nrb;
-      const int ct = tiles_of(i);
-      const bool run_end = i == begin[g + 1] - 1 || (i + 1) / nrb != ts;
-      if (ts != slot_ts) {
-        new_slot(ts);
-        slot_ts = ts;
-        stored = false;
+  for (int half = 0; half < halves; ++half)
+    for (int r = 0; r < ranges; ++r) {
+      const int g = pair ? 2 * r + half : r;
+      cta_slot[g] = slots;
+      int slot_ts = -1;
+      bool stored = false;
+      for (int i = begin[r]; i < begin[r + 1]; ++i) {
+        const int ts = i / nrb, rb = i % nrb;
+        const int key = ts * halves + half;
+        const int ct = tiles_of(i, half);
+        const bool run_end = i == begin[r + 1] - 1 || (i + 1) / nrb != ts;
+        if (ts != slot_ts) {
+          new_slot(key);
+          slot_ts = ts;
+          stored = false;
+        }
+        if (i == begin[r + 1] - 1 && stored) new_slot(key);
+        if (run_end)
+          stored = false;
+        else if (rk::tc::k1_rot_tile(rb, h->qrot, c) >= 0 && rk::tc::k1_rot_tile(rb, h->qrot, c) < ct)
+          stored = true;
       }
-      if (i == begin[g + 1] - 1 && stored) new_slot(ts);
-      if (run_end)
-        stored = false;
-      else if (rk::tc::k1_rot_tile(rb, h->qrot, c) >= 0 && rk::tc::k1_rot_tile(rb, h->qrot, c) < ct)
-        stored = true;
     }
+  if (pair) {
+    h->Pscr = dalloc<float>((size_t)ranges * rk::tc::kPairSlots * 128 * K);
+    h->pflag = dalloc<unsigned>((size_t)ranges * rk::tc::kPairWords);
+    RK_CUDA(cudaMemset(h->pflag, 0, sizeof(unsigned) * ranges * rk::tc::kPairWords));
   }
   h->grid_tc = grid;
   h->nslots = slots;
-  h->d_cta_begin = dalloc<int>(grid + 1);
+  const int nkeys = M * nstrips * halves;
+  h->d_cta_begin = dalloc<int>(ranges + 1);
   h->d_cta_slot = dalloc<int>(grid);
-  h->d_slot_first = dalloc<int>(M * nstrips);
-  h->d_slot_count = dalloc<int>(M * nstrips);
-  RK_CUDA(cudaMemcpy(h->d_cta_begin, begin.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice));
+  h->d_slot_first = dalloc<int>(nkeys);
+  h->d_slot_count = dalloc<int>(nkeys);
+  RK_CUDA(cudaMemcpy(h->d_cta_begin, begin.data(), sizeof(int) * (ranges + 1), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(h->d_cta_slot, cta_slot.data(), sizeof(int) * grid, cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(h->d_slot_first, slot_first.data(), sizeof(int) * M * nstrips,
-                     cudaMemcpyHostToDevice));
-  RK_CUDA(cudaMemcpy(h->d_slot_count, slot_count.data(), sizeof(int) * M * nstrips,
-                     cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(h->d_slot_first, slot_first.data(), sizeof(int) * nkeys, cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(h->d_slot_count, slot_count.data(), sizeof(int) * nkeys, cudaMemcpyHostToDevice));
   h->Ppart = dalloc<float>((size_t)M * nstrips * h->NR * K);
   h->Qpart = dalloc<float>((size_t)slots * c * 128 * K);
   // the slots being added into (one per CTA) are stored evict-last; give
@@ -918,6 +958,10 @@ void launch_k1(rk_handle* h, bool timed) {
     a.nrb = (int)(h->NR / 128);
     a.ncb = (int)(h->NC / 128);
     a.qrot = h->qrot;
+    a.pair = h->k1_pair ? 1 : 0;
+    a.sw = h->sw;
+    a.Pscr = h->Pscr;
+    a.pflag = h->pflag;
     a.Ppart = h->Ppart;
     a.Qpart = h->Qpart;
     a.cta_begin = h->d_cta_begin;
@@ -932,7 +976,8 @@ void launch_k1(rk_handle* h, bool timed) {
     {
       launch_pdl(rk::tc::k1_reduce, dim3(h->num_sms * 8), dim3(256), 0, s, (const Ctl*)h->ctl,
                  (const float*)h->Ppart, (const float*)h->Qpart, (const int*)h->d_slot_first,
-                 (const int*)h->d_slot_count, h->P, h->Q, (int)h->NR, (int)h->NC, K, M, h->c, h->nstrips, 1);
+                 (const int*)h->d_slot_count, h->P, h->Q, (int)h->NR, (int)h->NC, K, M, h->c, h->nstrips, 1,
+                 h->sw, h->k1_pair ? 1 : 0);
       h->launches += 1;
     }
   } else {
@@ -2947,9 +2992,10 @@ void* rk_stream(rk_handle* h) { return h ? (void*)h->stream : nullptr; }
 int rk_info(rk_handle* h, int64_t* out, int32_t n_out) {
   return guarded([&] {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
-    int64_t v[12] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
-                     h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0, h->k1_mq ? 1 : 0};
-    for (int i = 0; i < n_out && i < 12; ++i) out[i] = v[i];
+    int64_t v[14] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
+                     h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0, h->k1_mq ? 1 : 0,
+                     h->k1_pair ? 1 : 0, h->sw};
+    for (int i = 0; i < n_out && i < 14; ++i) out[i] = v[i];
   });
 }
 

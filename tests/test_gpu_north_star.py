@@ -53,7 +53,9 @@ def _device_vs_oracle(n, m, k, iters, seed):
 def test_cfg3_shape_matches_oracle():
     n, m, k, iters = 32768, 2, 32, 3
     a_dev, r_dev, trace, a, r, err, info = _device_vs_oracle(n, m, k, iters, 13)
-    assert info["engine"] == 1 and info["strip_tiles"] == 12 and info["strips"] == 22, info
+    # paired strips: 11 strips of 24 column tiles, 12 per CTA of a pair
+    assert info["engine"] == 1 and info["strip_tiles"] == 12 and info["strips"] == 11, info
+    assert info["k1_pair"] == 1 and info["strip_width"] == 24 and info["ctas"] == 148, info
     assert rel_fro(a_dev, a) <= 1e-4 and rel_fro(r_dev, r) <= 1e-4, (rel_fro(a_dev, a), rel_fro(r_dev, r))
     assert abs(trace[-1] - err) <= 1e-5, (trace[-1], err)
     assert np.all(np.diff(trace) <= 1e-9), trace
