@@ -1509,7 +1509,10 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 template <typename T>
 void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
   // chunks of host rows through a pinned staging ring when the host buffer is
-  // pageable; straight async copies when it is already pinned.
+  // pageable; straight async copies when it is already pinned. The copies run
+  // on their own stream, the split kernels on the handle's: the split of
+  // chunk i overlaps the copy of chunk i + 1 (a copy-bound upload), ordered
+  // by events per staging slot, without host waits for a pinned source.
   cudaPointerAttributes attr;
   bool pinned = cudaPointerGetAttributes(&attr, x) == cudaSuccess &&
                 (attr.type == cudaMemoryTypeHost);
@@ -1521,36 +1524,48 @@ void upload_rows(rk_handle* h, const T* x, int64_t rows, int64_t cols) {
   T* hstage[2] = {nullptr, nullptr};
   if (!pinned)
     for (int i = 0; i < 2; ++i) RK_CUDA(cudaMallocHost(&hstage[i], (size_t)rows_per * row_bytes));
-  cudaEvent_t done[2];
-  for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+  cudaStream_t cs;
+  RK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaEvent_t copied[2], split[2];
+  for (int i = 0; i < 2; ++i) {
+    RK_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&split[i], cudaEventDisableTiming));
+  }
+  RK_CUDA(cudaEventRecord(split[0], h->stream));  // the upload starts after the handle's pending work
+  RK_CUDA(cudaStreamWaitEvent(cs, split[0], 0));
   bool used[2] = {false, false};
   int slot = 0;
   for (int64_t t = 0; t < h->m; ++t) {
     for (int64_t r0 = 0; r0 < rows; r0 += rows_per) {
       const int64_t nrow = std::min(rows_per, rows - r0);
       const T* src = x + ((size_t)t * rows + r0) * cols;
-      if (used[slot]) RK_CUDA(cudaEventSynchronize(done[slot]));
       const T* from = src;
       if (!pinned) {
+        if (used[slot]) RK_CUDA(cudaEventSynchronize(copied[slot]));  // host staging slot free
         parallel_memcpy(hstage[slot], src, (size_t)nrow * row_bytes);
         from = hstage[slot];
       }
-      RK_CUDA(cudaMemcpyAsync(dstage[slot], from, (size_t)nrow * row_bytes, cudaMemcpyHostToDevice,
-                              h->stream));
+      if (used[slot]) RK_CUDA(cudaStreamWaitEvent(cs, split[slot], 0));  // device staging slot free
+      RK_CUDA(cudaMemcpyAsync(dstage[slot], from, (size_t)nrow * row_bytes, cudaMemcpyHostToDevice, cs));
+      RK_CUDA(cudaEventRecord(copied[slot], cs));
+      RK_CUDA(cudaStreamWaitEvent(h->stream, copied[slot], 0));
       rk::split_chunk<T><<<h->nnp, rk::kThreads, 0, h->stream>>>(
           dstage[slot], nrow, cols, h->Xh, h->Xl, h->NR, h->NC, (int)t, r0, h->npart, h->npart2);
       RK_CUDA(cudaGetLastError());
-      RK_CUDA(cudaEventRecord(done[slot], h->stream));
+      RK_CUDA(cudaEventRecord(split[slot], h->stream));
       used[slot] = true;
       slot ^= 1;
     }
   }
   RK_CUDA(cudaStreamSynchronize(h->stream));
+  RK_CUDA(cudaStreamSynchronize(cs));
   for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(done[i]);
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(split[i]);
     dfree(dstage[i]);
     if (hstage[i]) cudaFreeHost(hstage[i]);
   }
+  cudaStreamDestroy(cs);
 }
 
 void regress_core(rk_handle* h, int max_iters, double tol, double eps, int* iters_done) {
