@@ -499,10 +499,14 @@ int k1_qrot() {
 }
 
 // Paired strips in K1 (RK_K1_PAIR=0 turns them off: measurement only).
-constexpr int kPairMinStrips = 16;
+constexpr int kPairMinStrips = 8;
 bool k1_pair_on() {
   const char* e = std::getenv("RK_K1_PAIR");
   return e ? std::atoi(e) != 0 : true;
+}
+bool k1_pair_force() {  // RK_K1_PAIR=2: pairs below kPairMinStrips too (measurement)
+  const char* e = std::getenv("RK_K1_PAIR");
+  return e && std::atoi(e) == 2;
 }
 
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
@@ -523,11 +527,11 @@ void plan_tc(rk_handle* h) {
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
   nstrips = (ncb + c - 1) / c;
-  // Paired strips (k1_tc.cuh): for wide tensors (>= 16 strips) two CTAs
-  // share a strip of up to 2 c tiles and write ONE P partial for it (half
-  // the partial traffic). On narrower ones the pair coupling costs more K1
-  // time than the partials save (cfg2: K1 +7 %, profiles/r02_pairs.md).
-  const bool pair = nstrips >= kPairMinStrips && k1_pair_on();
+  // Paired strips (k1_tc.cuh): from 8 strips on two CTAs share a strip of up
+  // to 2 c tiles and write ONE P partial for it (half the partial traffic):
+  // K1 + k1_reduce -3 % at 10-22 strips; neutral at cfg2's 5 (ncb 64, K 16),
+  // which stays unpaired (profiles/r02_pairs.md).
+  const bool pair = (nstrips >= kPairMinStrips || k1_pair_force()) && nstrips >= 2 && k1_pair_on();
   int sw = c;
   if (pair) {
     nstrips = (ncb + 2 * cmax - 1) / (2 * cmax);
