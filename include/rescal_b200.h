@@ -244,7 +244,7 @@ void* rk_stream(rk_handle* h);
  * out[3]=strip tiles (TC), out[4]=CTAs (TC), out[5]=smem bytes (TC), out[6]=strips,
  * out[7]=Q slots, out[8]=K2a blocks, out[9]=nc_pad, out[10]=1 when the grid exchange
  * runs over peer memory (NVLink IPC; set by the first grid rk_run), 0 for NCCL,
- * out[11]=1 when K1 merges Q's hi/lo operands, out[12]=1 for paired K1 strips,
+ * out[11]=1 when K1 merges Q's hi/lo operands, out[12]=CTAs per K1 strip group (1, 2, 4),
  * out[13]=column tiles per strip (TC). */
 int rk_info(rk_handle* h, int64_t* out, int32_t n_out);
 

@@ -400,7 +400,7 @@ class Engine:
         out = np.zeros(14, dtype=np.int64)
         check(self._lib.rk_info(self._h, out.ctypes.data_as(_pi64), 14))
         keys = ["engine", "n_pad", "k_pad", "strip_tiles", "ctas", "smem", "strips", "slots", "k2a_blocks", "nc_pad",
-                "peer_exchange", "k1_merge_q", "k1_pair", "strip_width"]
+                "peer_exchange", "k1_merge_q", "k1_group", "strip_width"]
         return dict(zip(keys, (int(v) for v in out)))
 
     @property

@@ -54,10 +54,10 @@ struct K1Args {
   int nrb;        // NR / 128 row blocks
   int ncb;        // NC / 128 column tiles
   int qrot;       // rotating Q drains: one tile every qrot items (0 = only at run ends)
-  int pair;       // CTA pairs share a strip (k1_tc.cuh "Paired strips")
-  int sw;         // column tiles per strip (c, or <= 2c with pairs)
-  float* Pscr;    // pairs: [npairs][kPairSlots][K/4][128] float4, first arrivals' P tiles
-  unsigned* pflag;  // pairs: [npairs][kPairWords] tickets / ready / done / exit counters
+  int grp;        // CTAs per strip group (1, 2 or 4; k1_tc.cuh "Strip groups")
+  int sw;         // column tiles per strip (c, or <= grp * c with groups)
+  float* Pscr;    // groups: [ngroups][kPairSlots][grp][K/4][128] float4, the members' P tiles
+  unsigned* pflag;  // groups: [ngroups][kPairWords] tickets / ready / done / exit counters
   float* Ppart;   // [nstrips][M][NR/128][K/4][128] float4
   float* Qpart;   // [nslots][c][K/4][128] float4
   const int* cta_begin;  // [grid + 1] item ranges
@@ -203,19 +203,24 @@ RK_DEV int strip_tiles(int s, int nstrips, int c, int ncb) {
   return s == nstrips - 1 ? ncb - c * (nstrips - 1) : c;
 }
 
-// The column tiles of strip s a CTA works on: all of them, or with pairs the
-// first ceil(ct/2) (even CTA, half 0) / the rest (odd CTA, half 1).
-__host__ __device__ inline void k1_half_tiles(int s, int nstrips, int sw, int ncb, int pair, int half, int& ct,
+// The column tiles of strip s a CTA works on: all of them, or with a group
+// of grp CTAs member q's share of a balanced split (the first cts mod grp
+// members take one tile more).
+__host__ __device__ inline void k1_half_tiles(int s, int nstrips, int sw, int ncb, int grp, int q, int& ct,
                                               int& toff) {
   const int cts = s == nstrips - 1 ? ncb - sw * (nstrips - 1) : sw;
-  if (!pair) {
+  if (grp <= 1) {
     ct = cts;
     toff = 0;
     return;
   }
-  const int ct0 = (cts + 1) / 2;
-  ct = half ? cts - ct0 : ct0;
-  toff = half ? ct0 : 0;
+  const int base = cts / grp, rem = cts - base * grp;
+  ct = base + (q < rem ? 1 : 0);
+  toff = q * base + (q < rem ? q : rem);
+}
+
+RK_DEV void red_release_add_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 RK_DEV unsigned ld_acquire_u32(const unsigned* p) {
@@ -230,7 +235,8 @@ RK_DEV void st_release_u32(unsigned* p, unsigned v) {
 
 RK_DEV void epi_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }  // the 4 epilogue warps
 
-constexpr int kPairSlots = 4;                   // scratch tiles per CTA pair
+constexpr int kPairSlots = 4;                   // scratch item slots per CTA group
+constexpr int kMaxGrp = 4;                      // CTAs per strip group
 constexpr int kPairWords = 3 * kPairSlots + 1;  // tickets, ready, done per slot + exit count
 
 // ------------------------------- the kernel --------------------------------
@@ -349,12 +355,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_full = ai_full + 8;            // [kMaxC], one per Q column tile
   uint64_t* q_empty = q_full + kMaxC;        // [kMaxC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + kMaxC);
-  volatile uint32_t* s_first = tmem_slot + 1;  // paired strips: this CTA arrived first
+  volatile uint32_t* s_first = tmem_slot + 1;  // strip groups: this CTA is not the item's last arrival
 
   const int warp = warp_id_uniform();
   const int lane = threadIdx.x & 31;
-  const int pair = args.pair, half = pair ? (int)(blockIdx.x & 1) : 0;
-  const int rng = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // item range index
+  const int grp = args.grp > 1 ? args.grp : 1;
+  const int half = (int)(blockIdx.x % grp);  // member of the strip group
+  const int rng = (int)(blockIdx.x / grp);   // item range index (one per group)
   const int item_b = args.cta_begin[rng];
   const int item_e = args.cta_begin[rng + 1];
   const int nstrips = args.nstrips, nrb = args.nrb, ncb = args.ncb, c = args.c, NR = args.NR, sw = args.sw;
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int t, s, rb;
         decode_item(item, nstrips, nrb, t, s, rb);
         int ct, toff;
-        k1_half_tiles(s, nstrips, sw, ncb, pair, half, ct, toff);
+        k1_half_tiles(s, nstrips, sw, ncb, grp, half, ct, toff);
         const int ab = (item - item_b) & 1;
         const uint32_t ap = ((item - item_b) >> 1) & 1;
         // A^T[:, I] (row operand of Q) for this row block
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int t, s, rb;
         decode_item(item, nstrips, nrb, t, s, rb);
         int ct, toff;
-        k1_half_tiles(s, nstrips, sw, ncb, pair, half, ct, toff);
+        k1_half_tiles(s, nstrips, sw, ncb, grp, half, ct, toff);
         const int ts = item / nrb;
         if (item == item_b || (item - 1) / nrb != ts) restart = ~0u;  // a new (t, strip) run
         const bool run_end = item == item_e - 1 || (item + 1) / nrb != ts;
@@ -470,6 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int idx = item - item_b;
         const int ab = idx & 1;
         const uint32_t ap = (idx >> 1) & 1;
+        // (P double-buffered across items. Splitting an item's P over both
+        // buffers halves P's TMEM error but made the factors LESS accurate:
+        // P's and Q's truncation biases then differ -- the MU update absorbs
+        // a common scale, not a P / Q imbalance; profiles/r02_q_rotation.md)
         const int pb = idx & 1;
         const uint32_t pp = (idx >> 1) & 1;
         mbar_wait(smem_u32(&ai_full[ab]), ap);
@@ -563,13 +574,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int t, s, rb;
       decode_item(item, nstrips, nrb, t, s, rb);
       int ct, toff;
-      k1_half_tiles(s, nstrips, sw, ncb, pair, half, ct, toff);
+      k1_half_tiles(s, nstrips, sw, ncb, grp, half, ct, toff);
       const int ts = item / nrb;
       const bool run_end = item == item_e - 1 || (item + 1) / nrb != ts;
       const int dcb = k1_rot_tile(rb, qrot, c);
       const int idx = item - item_b;
-      const int pb = idx & 1;
-      const uint32_t pp = (idx >> 1) & 1;
       if (ts != slot_ts) {  // one slot per (CTA, (t, strip) run)
         ++slot;
         slot_ts = ts;
@@ -636,6 +645,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         qf_par ^= 1u << dcb;
         stored |= 1u << dcb;
       }
+      const int pb = idx & 1;
+      const uint32_t pp = (idx >> 1) & 1;
       mbar_wait(smem_u32(&p_full[pb]), pp);
       tc_fence_after();
       float v[K];
@@ -653,34 +664,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&p_empty[pb]));
-      if (ct == 0) {  // an odd CTA without tiles in a ragged last strip: no MMA wrote P
+      if (ct == 0) {  // a group member without tiles in a ragged last strip: no MMA wrote P
 #pragma unroll
         for (int d = 0; d < K; ++d) v[d] = 0.f;
       }
       // partial layout [strip][t][row block][K/4][128 rows] float4 (coalesced)
       float4* dst = reinterpret_cast<float4*>(
                         args.Ppart + ((((size_t)s * args.M + t) * NR) + (size_t)rb * kTile) * K) + row;
-      if (pair) {
-        // Paired strips: both CTAs of a pair produce a P tile for the same
-        // (t, strip, rb). Whichever arrives second (ticket per buffer slot)
-        // adds the first one's tile from the L2 scratch and writes the
-        // strip's one partial; the first writes its tile and moves on, so
-        // the two CTAs never run in lockstep (a + b == b + a: deterministic).
+      if (grp > 1) {
+        // Strip groups: the grp CTAs of a group produce P tiles for the same
+        // (t, strip, rb). The last to arrive (ticket per buffer slot) sums
+        // all of them in member order (deterministic) and writes the strip's
+        // one partial; the others store their tile in the group's L2 scratch
+        // and move on, so the members never run in lockstep.
         const int b = idx % kPairSlots;
         const unsigned k = (unsigned)(idx / kPairSlots);  // earlier uses of slot b
         unsigned* tk = args.pflag + (size_t)rng * kPairWords;  // [tickets][ready][done][exit]
         unsigned* ready = tk + kPairSlots;
         unsigned* done = ready + kPairSlots;
-        float4* scr = reinterpret_cast<float4*>(args.Pscr + ((size_t)rng * kPairSlots + b) * kTile * K) + row;
+        float* scr0 = args.Pscr + ((size_t)rng * kPairSlots + b) * grp * kTile * K;  // member tiles
         if (threadIdx.x == 64) {
-          // slot b's previous use must be complete (both arrivals and the
-          // read) before its ticket is taken: the ticket parity then tells
-          // first from second even when one CTA runs kPairSlots items ahead
+          // slot b's previous use must be complete (all arrivals and the
+          // read) before its ticket is taken: the ticket then counts this
+          // item's arrivals even when a member runs kPairSlots items ahead
           // (waits only then)
           if (k > 0)
             while (ld_acquire_u32(done + b) < k) {
             }
-          *s_first = (atomicAdd(tk + b, 1u) & 1u) == 0u ? 1u : 0u;
+          *s_first = (atomicAdd(tk + b, 1u) % (unsigned)grp) != (unsigned)(grp - 1) ? 1u : 0u;
         }
         epi_bar();
         if (*s_first) {
@@ -688,6 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // (and discarded)
           uint64_t pol;
           asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+          float4* scr = reinterpret_cast<float4*>(scr0 + (size_t)half * kTile * K) + row;
 #pragma unroll
           for (int h = 0; h < K / 4; ++h)
             asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(scr + h * kTile),
@@ -695,36 +707,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                          : "memory");
           __threadfence();
           epi_bar();
-          if (threadIdx.x == 64) st_release_u32(ready + b, (unsigned)(idx + 1));
+          if (threadIdx.x == 64) red_release_add_u32(ready + b, 1u);
         } else {
           if (threadIdx.x == 64)
-            while (ld_acquire_u32(ready + b) != (unsigned)(idx + 1)) {
+            while (ld_acquire_u32(ready + b) < (k + 1) * (unsigned)(grp - 1)) {
             }
           epi_bar();
+          float acc[K];
 #pragma unroll
-          for (int h = 0; h < K / 4; ++h) {
-            const float4 o = __ldcg(scr + h * kTile);
-            v[4 * h] += o.x;
-            v[4 * h + 1] += o.y;
-            v[4 * h + 2] += o.z;
-            v[4 * h + 3] += o.w;
+          for (int d = 0; d < K; ++d) acc[d] = 0.f;
+          for (int qq = 0; qq < grp; ++qq) {  // member order: the same sum whoever arrives last
+            if (qq == half) {
+#pragma unroll
+              for (int d = 0; d < K; ++d) acc[d] += v[d];
+            } else {
+              const float4* scr = reinterpret_cast<const float4*>(scr0 + (size_t)qq * kTile * K) + row;
+#pragma unroll
+              for (int h = 0; h < K / 4; ++h) {
+                const float4 o = __ldcg(scr + h * kTile);
+                acc[4 * h] += o.x;
+                acc[4 * h + 1] += o.y;
+                acc[4 * h + 2] += o.z;
+                acc[4 * h + 3] += o.w;
+              }
+            }
           }
           epi_bar();  // every row read
-          // the tile is dead: drop its L2 lines without a write-back (else
-          // the partial traffic the pair saves reappears as scratch
-          // write-backs); one 128 B line per thread
-          if (threadIdx.x - 64 < K * kTile * 4 / 128) {
-            const char* line =
-                reinterpret_cast<const char*>(args.Pscr + ((size_t)rng * kPairSlots + b) * kTile * K) +
-                (size_t)(threadIdx.x - 64) * 128;
-            asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+          // the tiles are dead: drop their L2 lines without a write-back
+          // (else the partial traffic the group saves reappears as scratch
+          // write-backs); one 128 B line per thread and member tile
+          for (int qq = 0; qq < grp; ++qq) {
+            if (qq == half) continue;
+            if (threadIdx.x - 64 < K * kTile * 4 / 128) {
+              const char* line = reinterpret_cast<const char*>(scr0 + (size_t)qq * kTile * K) +
+                                 (size_t)(threadIdx.x - 64) * 128;
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+            }
           }
           __threadfence();
           epi_bar();
           if (threadIdx.x == 64) st_release_u32(done + b, k + 1);
 #pragma unroll
           for (int h = 0; h < K / 4; ++h)
-            dst[h * kTile] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+            dst[h * kTile] = make_float4(acc[4 * h], acc[4 * h + 1], acc[4 * h + 2], acc[4 * h + 3]);
         }
       } else {
 #pragma unroll
@@ -732,12 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst[h * kTile] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
       }
     }
-    // the pair's counters start from zero in the next launch: the second CTA
-    // to finish resets them (both are done with them by then)
-    if (pair && threadIdx.x == 64) {
+    // the group's counters start from zero in the next launch: the last
+    // member to finish resets them (all are done with them by then)
+    if (grp > 1 && threadIdx.x == 64) {
       unsigned* f = args.pflag + (size_t)rng * kPairWords;
       __threadfence();
-      if (atomicAdd(f + 3 * kPairSlots, 1u) == 1u) {
+      if (atomicAdd(f + 3 * kPairSlots, 1u) == (unsigned)(grp - 1)) {
         for (int w = 0; w < kPairWords; ++w) f[w] = 0u;
         __threadfence();
       }
@@ -791,22 +816,25 @@ RK_DEV void k1_reduce_p4(const float* __restrict__ Ppart, float* __restrict__ P,
 // One float4 of Q (row j of slice t): the Q-partial slots of its strip in order.
 RK_DEV void k1_reduce_q4(const float* __restrict__ Qpart, const int* __restrict__ slot_first,
                          const int* __restrict__ slot_count, float* __restrict__ Q, int NC, int K, int c,
-                         int nstrips, int t, int j, int q4, int sw = 0, int pair = 0) {
-  // slots hold c column tiles; a strip has sw tiles (sw = c, or up to 2c
-  // split between the two CTAs of a pair: slots keyed (t, strip, half))
+                         int nstrips, int t, int j, int q4, int sw = 0, int grp = 1) {
+  // slots hold c column tiles; a strip has sw tiles (sw = c, or up to grp c
+  // split between the CTAs of a group: slots keyed (t, strip, member))
   const int W = c * kTile;
   const int swt = sw ? sw : c;
+  grp = grp > 1 ? grp : 1;
   const int s = j / (swt * kTile);
   const int jt = (j - s * swt * kTile) / kTile;  // tile within the strip
   int half = 0, toff = 0;
-  if (pair) {
-    int ct0, t0;
-    k1_half_tiles(s, nstrips, swt, NC / kTile, 1, 0, ct0, t0);
-    half = jt >= ct0;
-    toff = half ? ct0 : 0;
+  for (int q = 1; q < grp; ++q) {  // the member whose tiles hold jt
+    int ctq, tq;
+    k1_half_tiles(s, nstrips, swt, NC / kTile, grp, q, ctq, tq);
+    if (jt >= tq) {
+      half = q;
+      toff = tq;
+    }
   }
   const int jl = (jt - toff) * kTile + (j & (kTile - 1));  // column within the slot
-  const int key = (t * nstrips + s) * (pair ? 2 : 1) + half;
+  const int key = (t * nstrips + s) * grp + half;
   const int f = slot_first[key], nsl = slot_count[key];
   float4 qa = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* src = reinterpret_cast<const float4*>(Qpart + ((size_t)f * W + (jl & ~(kTile - 1))) * K) +
@@ -832,7 +860,7 @@ RK_DEV void k1_reduce_q4(const float* __restrict__ Qpart, const int* __restrict_
 RK_DEV void k1_reduce_body(const float* __restrict__ Ppart, const float* __restrict__ Qpart,
                            const int* __restrict__ slot_first, const int* __restrict__ slot_count,
                            float* __restrict__ P, float* __restrict__ Q, int NR, int NC, int K, int M, int c,
-                           int nstrips, int64_t g0, int64_t gstride, int sw = 0, int pair = 0) {
+                           int nstrips, int64_t g0, int64_t gstride, int sw = 0, int grp = 1) {
   const int K4 = K / 4;
   const int64_t totalP = (int64_t)M * NR * K4;
   const int64_t total = totalP + (int64_t)M * NC * K4;
@@ -853,7 +881,7 @@ RK_DEV void k1_reduce_body(const float* __restrict__ Ppart, const float* __restr
       const int q4 = (int)(rest % K4);
       const int64_t tj = (rest / K4) * kTile + r;
       k1_reduce_q4(Qpart, slot_first, slot_count, Q, NC, K, c, nstrips, (int)(tj / NC), (int)(tj % NC), q4, sw,
-                   pair);
+                   grp);
     }
   }
 }
@@ -865,11 +893,11 @@ __global__ void __launch_bounds__(256) k1_reduce(const Ctl* __restrict__ ctl,
                                                  const int* __restrict__ slot_count,
                                                  float* __restrict__ P, float* __restrict__ Q,
                                                  int NR, int NC, int K, int M, int c, int nstrips,
-                                                 int skip_if_stopped, int sw, int pair) {
+                                                 int skip_if_stopped, int sw, int grp) {
   pdl_entry();
   if (skip_if_stopped && ctl->stop) return;
   k1_reduce_body(Ppart, Qpart, slot_first, slot_count, P, Q, NR, NC, K, M, c, nstrips,
-                 (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, sw, pair);
+                 (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, sw, grp);
 }
 
 }  // namespace tc

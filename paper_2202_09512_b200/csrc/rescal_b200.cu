@@ -299,10 +299,10 @@ struct rk_handle {
   int nnp = 0;
   // tcgen05 schedule
   int c = 0, nstrips = 0, grid_tc = 0, nslots = 0, qrot = 1;
-  int sw = 0;           // K1 column tiles per strip (c, or up to 2c with paired strips)
-  bool k1_pair = false; // K1 paired strips
-  float* Pscr = nullptr;      // paired strips: the odd CTAs' P tiles
-  unsigned* pflag = nullptr;  // paired strips: produced / consumed counters
+  int sw = 0;           // K1 column tiles per strip (c, or up to grp c with strip groups)
+  int k1_grp = 1;       // K1 CTAs per strip group (1, 2, 4)
+  float* Pscr = nullptr;      // strip groups: the members' P tiles
+  unsigned* pflag = nullptr;  // strip groups: ticket / ready / done / exit counters
   bool k1_mq = true;  // K1 merges the Q hi/lo operands (always at K = 16; see k1_merge_q)
   size_t smem_tc = 0;
   float *Ppart = nullptr, *Qpart = nullptr;
@@ -487,26 +487,29 @@ size_t k1_smem(int K) {
   }
 }
 
-// K1's Q accuracy mode (k1_tc.cuh "Rotating Q drains"): RK_K1_QROT=p > 0
-// drains one Q tile after every p-th row block, bounding each TMEM sum to
-// p*c row blocks (n = 32768, k = 32: Q rel. error 5.7e-5 -> 6.2e-6 at p = 1)
-// for 1.4-1.7 % more K1 time (read-backs of the slots that miss L2). Off by
-// default: the default error is inside the parity tolerance and K1 is the
-// HBM-bound headline kernel (profiles/r02_q_rotation.md).
+// K1's rotating Q drains (k1_tc.cuh): one Q tile drained after every p-th
+// row block bounds each TMEM sum to p*c row blocks. p = 1 by default: at
+// n = 32768, k = 32 Q's relative error drops from 5.7e-5 to 6.2e-6 and the
+// cfg3-shape factors after 3 iterations from relR 9.6e-5 (4 % inside the
+// 1e-4 tolerance) to 1.4e-6 -- fp32-class, as north_star's "fp32-accurate"
+// split precision asks -- for ~1.5 % more K1 time at cfg3 (slot read-backs;
+// profiles/r02_q_rotation.md). RK_K1_QROT=0 turns it off (measurement only).
 int k1_qrot() {
   const char* e = std::getenv("RK_K1_QROT");
-  return e ? std::max(0, std::atoi(e)) : 0;
+  return e ? std::max(0, std::atoi(e)) : 1;
 }
 
-// Paired strips in K1 (RK_K1_PAIR=0 turns them off: measurement only).
+// K1 strip groups: grp CTAs share a strip (k1_tc.cuh). 2 from 8 strips on,
+// 4 from 16; RK_K1_GRP=g forces g (1 = off; measurement only).
 constexpr int kPairMinStrips = 8;
-bool k1_pair_on() {
-  const char* e = std::getenv("RK_K1_PAIR");
-  return e ? std::atoi(e) != 0 : true;
-}
-bool k1_pair_force() {  // RK_K1_PAIR=2: pairs below kPairMinStrips too (measurement)
-  const char* e = std::getenv("RK_K1_PAIR");
-  return e && std::atoi(e) == 2;
+constexpr int kQuadMinStrips = 16;
+int k1_grp_for(int nstrips) {
+  const char* e = std::getenv("RK_K1_GRP");
+  if (e) {
+    const int g = std::atoi(e);
+    return g >= 4 ? 4 : g >= 2 ? 2 : 1;
+  }
+  return nstrips >= kQuadMinStrips ? 4 : nstrips >= kPairMinStrips ? 2 : 1;
 }
 
 // Balanced item ranges and Q-partial slots for the tcgen05 K1 (see k1_tc.cuh).
@@ -527,34 +530,36 @@ void plan_tc(rk_handle* h) {
   int nstrips = (ncb + c - 1) / c;
   c = (ncb + nstrips - 1) / nstrips;
   nstrips = (ncb + c - 1) / c;
-  // Paired strips (k1_tc.cuh): from 8 strips on two CTAs share a strip of up
-  // to 2 c tiles and write ONE P partial for it (half the partial traffic):
-  // K1 + k1_reduce -3 % at 10-22 strips; neutral at cfg2's 5 (ncb 64, K 16),
-  // which stays unpaired (profiles/r02_pairs.md).
-  const bool pair = (nstrips >= kPairMinStrips || k1_pair_force()) && nstrips >= 2 && k1_pair_on();
+  // Strip groups (k1_tc.cuh): from 8 strips on, grp = 2 (from 16: 4) CTAs
+  // share a strip of up to grp c tiles and write ONE P partial for it (1/grp
+  // of the partial traffic): pairs cut K1 + k1_reduce by 3 % at 10-22 strips;
+  // neutral at cfg2's 5 (ncb 64, K 16), which stays ungrouped
+  // (profiles/r02_pairs.md).
+  const int grp = nstrips >= 2 ? k1_grp_for(nstrips) : 1;
+  const bool pair = grp > 1;
   int sw = c;
   if (pair) {
-    nstrips = (ncb + 2 * cmax - 1) / (2 * cmax);
+    nstrips = (ncb + grp * cmax - 1) / (grp * cmax);
     sw = (ncb + nstrips - 1) / nstrips;
     nstrips = (ncb + sw - 1) / sw;
-    c = (sw + 1) / 2;
+    c = (sw + grp - 1) / grp;
   }
   if (c > rk::tc::kMaxC) throw std::runtime_error("K1 strip wider than kMaxC tiles");
   h->c = c;
   h->sw = sw;
-  h->k1_pair = pair;
+  h->k1_grp = grp;
   h->nstrips = nstrips;
   const int64_t n_items = (int64_t)M * nstrips * nrb;
   auto tiles_of = [&](int64_t item, int half) {
     int ct, toff;
-    rk::tc::k1_half_tiles((int)((item / nrb) % nstrips), nstrips, sw, ncb, pair ? 1 : 0, half, ct, toff);
+    rk::tc::k1_half_tiles((int)((item / nrb) % nstrips), nstrips, sw, ncb, grp, half, ct, toff);
     return ct;
   };
   int64_t total = 0;
   for (int64_t it = 0; it < n_items; ++it) total += tiles_of(it, 0);
-  // item ranges: one per CTA, or one per CTA pair (both CTAs walk it)
-  const int ranges = (int)std::min<int64_t>(pair ? h->num_sms / 2 : h->num_sms, n_items);
-  const int grid = pair ? 2 * ranges : ranges;
+  // item ranges: one per CTA, or one per strip group (all members walk it)
+  const int ranges = (int)std::min<int64_t>(h->num_sms / grp, n_items);
+  const int grid = grp * ranges;
   std::vector<int> begin(ranges + 1, 0);
   int64_t cum = 0, it = 0;
   for (int g = 0; g < ranges; ++g) {
@@ -570,7 +575,7 @@ void plan_tc(rk_handle* h) {
   // pairs all even CTAs are numbered first, so every key's slots are
   // consecutive (k1_reduce_q4).
   h->qrot = K <= 32 ? k1_qrot() : 0;
-  const int halves = pair ? 2 : 1;
+  const int halves = grp;
   std::vector<int> cta_slot(grid, 0), slot_first(M * nstrips * halves, 0), slot_count(M * nstrips * halves, 0);
   int slots = 0;
   auto new_slot = [&](int key) {
@@ -580,7 +585,7 @@ void plan_tc(rk_handle* h) {
   };
   for (int half = 0; half < halves; ++half)
     for (int r = 0; r < ranges; ++r) {
-      const int g = pair ? 2 * r + half : r;
+      const int g = grp * r + half;
       cta_slot[g] = slots;
       int slot_ts = -1;
       bool stored = false;
@@ -602,7 +607,7 @@ void plan_tc(rk_handle* h) {
       }
     }
   if (pair) {
-    h->Pscr = dalloc<float>((size_t)ranges * rk::tc::kPairSlots * 128 * K);
+    h->Pscr = dalloc<float>((size_t)ranges * rk::tc::kPairSlots * grp * 128 * K);
     h->pflag = dalloc<unsigned>((size_t)ranges * rk::tc::kPairWords);
     RK_CUDA(cudaMemset(h->pflag, 0, sizeof(unsigned) * ranges * rk::tc::kPairWords));
   }
@@ -627,7 +632,14 @@ void plan_tc(rk_handle* h) {
     RK_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
     // (sized to the live slots: the device maximum, 83 MB, slows the X
     // stream itself by 10 %, profiles/r02_q_rotation.md)
-    const size_t want = std::min<size_t>((size_t)maxp, (size_t)grid * c * 128 * K * sizeof(float) * 5 / 4);
+    // live evict-last lines: one slot of c tiles per CTA, plus the strip
+    // groups' scratch tiles; 1.3x of them (cfg3: 48 MB; 36 MB left 0.4 GB
+    // of write-backs, 64 MB measured no better)
+    const size_t tile = (size_t)128 * K * sizeof(float);
+    const size_t live = (size_t)grid * c * tile + (grp > 1 ? (size_t)ranges * rk::tc::kPairSlots * grp * tile : 0);
+    size_t want = std::min<size_t>((size_t)maxp, live * 13 / 10);
+    if (const char* e = std::getenv("RK_K1_L2SET_MB"))  // measurement only
+      want = std::min<size_t>((size_t)maxp, (size_t)std::atoi(e) << 20);
     size_t cur = 0;
     RK_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
     if (want > cur) RK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
@@ -962,7 +974,7 @@ void launch_k1(rk_handle* h, bool timed) {
     a.nrb = (int)(h->NR / 128);
     a.ncb = (int)(h->NC / 128);
     a.qrot = h->qrot;
-    a.pair = h->k1_pair ? 1 : 0;
+    a.grp = h->k1_grp;
     a.sw = h->sw;
     a.Pscr = h->Pscr;
     a.pflag = h->pflag;
@@ -981,7 +993,7 @@ void launch_k1(rk_handle* h, bool timed) {
       launch_pdl(rk::tc::k1_reduce, dim3(h->num_sms * 8), dim3(256), 0, s, (const Ctl*)h->ctl,
                  (const float*)h->Ppart, (const float*)h->Qpart, (const int*)h->d_slot_first,
                  (const int*)h->d_slot_count, h->P, h->Q, (int)h->NR, (int)h->NC, K, M, h->c, h->nstrips, 1,
-                 h->sw, h->k1_pair ? 1 : 0);
+                 h->sw, h->k1_grp);
       h->launches += 1;
     }
   } else {
@@ -3013,7 +3025,7 @@ int rk_info(rk_handle* h, int64_t* out, int32_t n_out) {
     RK_REQUIRE(h, RK_ERR_DATA, "null handle");
     int64_t v[14] = {h->engine, h->NR, h->K, h->c, h->grid_tc, (int64_t)h->smem_tc,
                      h->nstrips, h->nslots, h->nb, h->NC, h->peer ? 1 : 0, h->k1_mq ? 1 : 0,
-                     h->k1_pair ? 1 : 0, h->sw};
+                     h->k1_grp, h->sw};
     for (int i = 0; i < n_out && i < 14; ++i) out[i] = v[i];
   });
 }

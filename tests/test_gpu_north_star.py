@@ -1,7 +1,8 @@
 """North-star shapes and the round-2 drop-in names on the device (GPU suite).
 
-* cfg3 shape (n = 32768, k = 32): K1<32> with its strip / segment / slot
-  schedule at full n (unmerged Q: 22 strips of 12 column tiles), the K = 32
+* cfg3 shape (n = 32768, k = 32), 10 iterations: K1<32> with its strip /
+  group / slot schedule at full n (unmerged Q: 6 strips of 43 column tiles
+  shared by groups of 4 CTAs, rotating Q drains), the K = 32
   tensor-core G / S kernel and k2b_v4<32, 8> (selected from n = 18944 on),
   against the fp64 oracle on the device generator's exact values
   (m = 2 keeps the host oracle affordable; rescal.py:114-146).
@@ -51,11 +52,14 @@ def _device_vs_oracle(n, m, k, iters, seed):
 
 
 def test_cfg3_shape_matches_oracle():
-    n, m, k, iters = 32768, 2, 32, 3
+    # 10 iterations: MU amplifies K1's accumulation error over iterations;
+    # with rotating Q drains (default) relR is 6.6e-6 here, without them
+    # 5.1e-4 (profiles/r02_q_rotation.md)
+    n, m, k, iters = 32768, 2, 32, 10
     a_dev, r_dev, trace, a, r, err, info = _device_vs_oracle(n, m, k, iters, 13)
-    # paired strips: 11 strips of 24 column tiles, 12 per CTA of a pair
-    assert info["engine"] == 1 and info["strip_tiles"] == 12 and info["strips"] == 11, info
-    assert info["k1_pair"] == 1 and info["strip_width"] == 24 and info["ctas"] == 148, info
+    # strip groups of 4 CTAs: 6 strips of up to 43 column tiles, <= 11 per CTA
+    assert info["engine"] == 1 and info["strip_tiles"] == 11 and info["strips"] == 6, info
+    assert info["k1_group"] == 4 and info["strip_width"] == 43 and info["ctas"] == 148, info
     assert rel_fro(a_dev, a) <= 1e-4 and rel_fro(r_dev, r) <= 1e-4, (rel_fro(a_dev, a), rel_fro(r_dev, r))
     assert abs(trace[-1] - err) <= 1e-5, (trace[-1], err)
     assert np.all(np.diff(trace) <= 1e-9), trace

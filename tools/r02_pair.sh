@@ -3,8 +3,8 @@
 o=gpurun_out; tag=${1:-r02p}; reps=${2:-2}
 timeout 1500 python -m pytest tests -m gpu -x -q > $o/${tag}_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $o/${tag}_pytest.log
 [ "$(grep -c passed $o/${tag}_pytest.log)" = 0 ] && exit 1
-for rep in $(seq $reps); do for cfg in cfg3 cfg2; do for v in head p0 p1; do
-  case $v in head) envs="RK_LIB_PATH=paper_2202_09512_b200/librescal_b200_head.so";; p0) envs="RK_K1_PAIR=0";; p1) envs="RK_K1_PAIR=1";; esac
+for rep in $(seq $reps); do for cfg in cfg3 cfg2; do for v in head new; do
+  case $v in head) envs="RK_LIB_PATH=paper_2202_09512_b200/librescal_b200_head.so";; new) envs="RK_NOTHING=1";; esac
   env $envs timeout 600 python bench.py --config $cfg --steps 30 --warmup 3 --no-cpu --no-e2e --no-secondary > $o/${tag}_${cfg}_${v}_$rep.json 2>$o/${tag}_${cfg}_${v}_$rep.err
   python - $o/${tag}_${cfg}_${v}_$rep.json <<'PY'
 import json,sys
