@@ -418,6 +418,7 @@ void free_factor_buffers(rk_handle* h) {
 bool k1_merge_q(int K, int64_t NC) {
   if (K == 16) return true;
   if (K > 32) return false;
+  if (const char* e = std::getenv("RK_K1_MERGEQ")) return std::atoi(e) != 0;  // measurement only
   const int64_t ncb = NC / 128;
   return (ncb + 5) / 6 == (ncb + 11) / 12;
 }
