@@ -418,7 +418,6 @@ void free_factor_buffers(rk_handle* h) {
 bool k1_merge_q(int K, int64_t NC) {
   if (K == 16) return true;
   if (K > 32) return false;
-  if (const char* e = std::getenv("RK_K1_MERGEQ")) return std::atoi(e) != 0;  // measurement only
   const int64_t ncb = NC / 128;
   return (ncb + 5) / 6 == (ncb + 11) / 12;
 }
@@ -638,9 +637,7 @@ void plan_tc(rk_handle* h) {
     // of write-backs, 64 MB measured no better)
     const size_t tile = (size_t)128 * K * sizeof(float);
     const size_t live = (size_t)grid * c * tile + (grp > 1 ? (size_t)ranges * rk::tc::kPairSlots * grp * tile : 0);
-    size_t want = std::min<size_t>((size_t)maxp, live * 13 / 10);
-    if (const char* e = std::getenv("RK_K1_L2SET_MB"))  // measurement only
-      want = std::min<size_t>((size_t)maxp, (size_t)std::atoi(e) << 20);
+    const size_t want = std::min<size_t>((size_t)maxp, live * 13 / 10);
     size_t cur = 0;
     RK_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
     if (want > cur) RK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
