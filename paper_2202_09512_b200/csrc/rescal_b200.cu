@@ -934,6 +934,28 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   RK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// Launch as a cooperative grid: every CTA co-resident. K1 with strip groups
+// needs it -- group members wait for each other's P tiles, which is only safe
+// when all of them run at once, also next to another engine's kernels on the
+// same GPU (a grid of one CTA per SM always fits an otherwise idle GPU).
+template <typename... KArgs, typename... Args>
+void launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                 Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
+  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 // ------------------------------- launches ----------------------------------
 
 void launch_k1(rk_handle* h, bool timed) {
@@ -982,8 +1004,12 @@ void launch_k1(rk_handle* h, bool timed) {
     a.cta_slot = h->d_cta_slot;
     a.ctl = h->ctl;
     a.skip_if_stopped = 1;
-    launch_pdl(k1_kernel_of(h), dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0], h->maps[1], h->maps[2],
-               h->maps[3], h->maps[4], h->maps[5], a);
+    if (h->k1_grp > 1)  // strip-group members wait for each other: co-resident grid
+      launch_coop(k1_kernel_of(h), dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0],
+                  h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
+    else
+      launch_pdl(k1_kernel_of(h), dim3(h->grid_tc), dim3(rk::tc::kThreads), h->smem_tc, s, h->maps[0],
+                 h->maps[1], h->maps[2], h->maps[3], h->maps[4], h->maps[5], a);
     RK_CUDA(cudaGetLastError());
     if (timed) RK_CUDA(cudaEventRecord(h->ev_k1[(size_t)h->k1_count * 2 + 1], s));
     h->launches += 1;
