@@ -1,7 +1,7 @@
 #!/bin/bash
 # Paired K1 strips: GPU tests, then cfg3 / cfg2 step and K1 time (HEAD build vs pairs off / on), interleaved.
 o=gpurun_out; tag=${1:-r02p}; reps=${2:-2}
-timeout 1500 python -m pytest tests -m gpu -x -q > $o/${tag}_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $o/${tag}_pytest.log
+timeout 900 python -m pytest tests/test_gpu_north_star.py tests/test_gpu_parity.py tests/test_gpu_guards.py -x -q > $o/${tag}_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $o/${tag}_pytest.log
 [ "$(grep -c passed $o/${tag}_pytest.log)" = 0 ] && exit 1
 for rep in $(seq $reps); do for cfg in cfg3 cfg2; do for v in head new; do
   case $v in head) envs="RK_LIB_PATH=paper_2202_09512_b200/librescal_b200_head.so";; new) envs="RK_NOTHING=1";; esac
