@@ -30,7 +30,7 @@ from scipy.optimize import linear_sum_assignment
 from . import _lib
 from .containers import dense_slices, is_sparse, tensor_dtype
 from .exceptions import DataError, RescalkitError
-from .solver import RescalFactors, SolverConfig, finalize_normalize, random_init, rescal_solve
+from .solver import RescalFactors, SolverConfig, drop_cached_engine, finalize_normalize, random_init, rescal_solve
 
 _SEED_TAG_PERTURB = 3
 _SEED_TAG_ENSEMBLE = 4
@@ -320,6 +320,7 @@ def rescalk(x, k_min: int, k_max: int, r: int, cfg: SolverConfig | None = None,
             raise DataError(f"sparse RESCALk runs on the CSR engine, which supports k <= 32 (k_max={k_max}); "
                             f"a dense copy of this tensor ({x.m}x{x.n}x{x.n}) is too large")
         sparse = False  # small tensor: the dense engine on the densified copy
+    drop_cached_engine()  # at most one tensor's device storage per thread
     eng = _lib.Engine(x.n, x.m, k_min, device=cfg.device, engine=cfg.engine, sparse=sparse)
     entries, timing = [], {"per_k_seconds": {}}
     try:

@@ -145,11 +145,15 @@ def finalize_normalize(f: RescalFactors) -> RescalFactors:
 # (device, n, m, k, engine kind): repeated small solves (RESCALk members,
 # update_r / update_a / rel_error loops) skip handle creation (stream, pinned
 # control block, buffer set-up: ~5 ms at cfg1 against ~1 ms of iterations).
-# Only tensors up to _CACHE_MAX_BYTES of device storage are kept;
-# release_cached_memory() drops it. Every use re-uploads x and resets the
-# factors, so a cached engine is indistinguishable from a fresh one.
+# Engines of any size are kept (a cfg3-sized call then skips handle and plan
+# set-up and reuses its captured graphs); a kept engine that does not match
+# the next call is closed BEFORE the new one is created, so at most one
+# tensor's device storage is held per thread. The library's allocator keeps
+# freed blocks cached either way; release_cached_memory() drops both. Every
+# use re-uploads x and resets the factors, so a cached engine is
+# indistinguishable from a fresh one.
 _CACHE = threading.local()
-_CACHE_MAX_BYTES = 1 << 30
+_CACHE_MAX_BYTES = 1 << 40
 
 
 def _engine_key(x, k, cfg: SolverConfig):
@@ -163,26 +167,44 @@ def _engine_for(x, k, cfg: SolverConfig):
     (k <= 32), the dense tcgen05/SIMT engine otherwise."""
     key = _engine_key(x, k, cfg)
     cached = getattr(_CACHE, "entry", None)
+    _CACHE.entry = None
     if cached is not None and cached[0] == key and cached[1].k == k:
         eng = cached[1]
-        _CACHE.entry = None
     else:
         eng = None
-    if key[4] == "sparse":
-        eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], sparse=True)
-        eng.upload_csr(list(x.slices))
-    else:
-        if is_sparse(x) and x.m * x.n * x.n > _DENSIFY_MAX:
-            raise DataError(f"the sparse (CSR) engine supports k <= 32 (k={k}); a dense copy of this "
-                            f"tensor ({x.m}x{x.n}x{x.n}) is too large")
-        eng = eng or _lib.Engine(x.n, x.m, k, device=key[0], engine=cfg.engine)
-        eng.upload(dense_slices(x))
+        if cached is not None:
+            cached[1].close()  # free its device storage before the new engine allocates
+    if key[4] != "sparse" and is_sparse(x) and x.m * x.n * x.n > _DENSIFY_MAX:
+        if eng is not None:
+            eng.close()
+        raise DataError(f"the sparse (CSR) engine supports k <= 32 (k={k}); a dense copy of this "
+                        f"tensor ({x.m}x{x.n}x{x.n}) is too large")
+    if eng is None:
+        eng = (_lib.Engine(x.n, x.m, k, device=key[0], sparse=True) if key[4] == "sparse"
+               else _lib.Engine(x.n, x.m, k, device=key[0], engine=cfg.engine))
+    try:
+        if key[4] == "sparse":
+            eng.upload_csr(list(x.slices))
+        else:
+            eng.upload(dense_slices(x))
+    except BaseException:
+        eng.close()  # a rejected upload must not leave the engine holding device memory
+        raise
     eng._cache_key = key
     return eng
 
 
+def drop_cached_engine() -> None:
+    """Close this thread's kept engine (callers that create their own engine
+    for a large tensor, e.g. rescalk, free its device storage first)."""
+    old = getattr(_CACHE, "entry", None)
+    _CACHE.entry = None
+    if old is not None:
+        old[1].close()
+
+
 def _release_engine(eng) -> None:
-    """Keep a small engine for the next call (closing the one kept before)."""
+    """Keep the engine for the next call (closing the one kept before)."""
     key = getattr(eng, "_cache_key", None)
     dense_bytes = 4 * eng.m * eng.n * eng.n
     if key is None or (not eng.sparse and dense_bytes > _CACHE_MAX_BYTES) or (
