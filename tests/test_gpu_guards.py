@@ -8,6 +8,8 @@ pool: profiles/r02_memcheck.log).
 * Determinism: the K1 mbarrier / TMA / TMEM pipeline, the deterministic
   partial reductions and the k x k kernels must give bit-identical factors on
   repeated runs from the same start (a race shows up as run-to-run noise).
+* Concurrency: two engines on one GPU at once (strip-group K1 is launched
+  cooperatively) finish with the factors of their serial runs.
 """
 
 import numpy as np
@@ -89,3 +91,37 @@ def test_repeated_runs_are_bit_identical(n, m, k):
             assert cur == ref, f"run {rep} differs from run 0"
     finally:
         eng.close()
+
+
+def test_concurrent_engines_with_strip_groups():
+    """Two engines solving at once on one GPU (two host threads, two streams):
+    K1 with strip groups (members wait for each other's P tiles) is launched
+    cooperatively, so both solves finish and match their serial results."""
+    import threading
+
+    n, m, k, iters = 16384, 2, 32, 6
+    starts = [rk.random_init(n, k, m, 40 + i) for i in range(2)]
+
+    def solve(i, out):
+        eng = _lib.Engine(n, m, k, device=0)
+        try:
+            eng.fill_uniform(50 + i)
+            assert eng.info()["k1_group"] == 2
+            eng.set_factors(starts[i].A, starts[i].R)
+            eng.run(iters, 1e-16, track_error=False)
+            out[i] = eng.get_factors()
+        finally:
+            eng.close()
+
+    serial = {}
+    for i in range(2):
+        solve(i, serial)
+    conc = {}
+    th = [threading.Thread(target=solve, args=(i, conc)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "concurrent solves did not finish"
+    for i in range(2):
+        assert np.array_equal(conc[i][0], serial[i][0]) and np.array_equal(conc[i][1], serial[i][1])
