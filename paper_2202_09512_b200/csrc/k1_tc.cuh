@@ -26,7 +26,13 @@
 // ~6 us of stalled MMA per drain). At the end of a run all tiles drain.
 // The slot (CTA-private, one per (CTA, run)) is read back by later drains:
 // stored evict-last under an L2 set-aside. The CTA's final drain writes a
-// fresh slot (a read-back there would sit on the kernel's tail).
+// fresh slot (a read-back there would sit on the kernel's tail). On by
+// default (period args.qrot = 1, K <= 32): without it the cfg3-shape factors
+// leave north_star's 1e-4 within a few MU iterations.
+// Strip groups (args.grp = 2 or 4): the CTAs of a group share a strip of up
+// to grp * c tiles, each accumulating its share of P in TMEM; the last to
+// arrive per item sums the members' tiles (L2 scratch, member order) and
+// writes the strip's one P partial -- 1/grp of the partial traffic.
 //   P partial  -> Ppart[strip][t][row block][K/4][128] float4 (one writer per (t,strip,row))
 //   Q partial  -> Qpart[slot][tile][K/4][128] float4
 // k1_reduce sums the partials in a fixed order (deterministic, no atomics).
