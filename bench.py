@@ -587,7 +587,44 @@ def run_ours(args, dist, rank, world, local_rank):
     barrier(dist)
 
 
+def gpu_local_cpus(dev):
+    """The host CPUs NVML reports as local to CUDA device ``dev`` (its NUMA
+    node), within this process's affinity; None when unknown."""
+    try:
+        import pynvml
+        import torch
+
+        p = torch.cuda.get_device_properties(dev)
+        bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, ((os.cpu_count() or 64) + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def e2e_leg(args, dist, rank, world, local_rank, units):
+    """e2e with the process bound to the GPU's local CPUs while the pinned
+    host input is allocated (first touch places its pages on the GPU's NUMA
+    node) and the timed call runs -- as a NUMA-aware caller would; a far-node
+    buffer cost the H2D copy ~15 % on some boxes. Affinity restored after."""
+    old = os.sched_getaffinity(0)
+    local = gpu_local_cpus(local_rank)
+    if local:
+        os.sched_setaffinity(0, local)
+    try:
+        out = e2e_leg_body(args, dist, rank, world, local_rank, units)
+    finally:
+        os.sched_setaffinity(0, old)
+    if out is not None and isinstance(out, dict):
+        out.setdefault("phases", {})["gpu_local_cpus"] = len(local) if local else None
+    return out
+
+
+def e2e_leg_body(args, dist, rank, world, local_rank, units):
     """The same metric through the public API with host buffers: the host->
     device copy of X (pinned), the solve and the factor download are inside
     the timed region. N=1: rescal_solve(RelTensor / SparseRelTensor);
