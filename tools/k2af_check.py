@@ -1,8 +1,9 @@
-"""A/B of the fused K2a+K2f kernel (k2af) against the two-kernel path:
-python tools/k2af_check.py cfgX  (run once with RK_K2AF=1 and once without).
-Prints the graph-replayed ms/iteration (untracked and tracked), the trace and
-a hash of the factor bytes after 20 iterations (the two paths must agree bit
-for bit)."""
+"""Factor hash + graph-replayed timing probe for library A/Bs
+(tools/ab_hash.sh runs it against two builds via RK_LIB_PATH):
+python tools/k2af_check.py cfgX. Prints the ms/iteration (untracked and
+tracked), the trace tail and a hash of the factor bytes after 20 iterations
+(two builds that keep the arithmetic must agree bit for bit). Named after
+its first use, the fused K2a+K2f A/B of round 2."""
 import hashlib, json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -17,7 +18,7 @@ n, m, k = {"cfg1": (256, 8, 4), "cfg5": (16384, 8, 16), "cfg2": (8192, 16, 16),
 eng = _lib.Engine(n, m, k, device=0)
 eng.fill_uniform(1)
 f0 = rk.random_init(n, k, m, 0)
-out = {"cfg": cfg, "k2af": os.environ.get("RK_K2AF", "0"), "env": {a: b for a, b in os.environ.items() if a.startswith("RK_")}}
+out = {"cfg": cfg, "env": {a: b for a, b in os.environ.items() if a.startswith("RK_")}}
 for track in (False, True):
     eng.set_factors(f0.A, f0.R)
     done, tr = eng.run(20, 1e-16, track)
