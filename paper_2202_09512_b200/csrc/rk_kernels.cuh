@@ -1666,12 +1666,15 @@ RK_DEV double pcg_field(double u, double delta) {
 }
 
 // Coalesced resampling for whole-row tensors (single GPU): a warp owns a
-// 2048-element segment of one row; lane l draws elements base+64c+2l and +1.
+// kSeg-element segment of one row; lane l draws elements base+64c+2l and +1.
 // Each lane jumps once per segment (log-time), then per 64-element chunk uses
 // the fixed 62-step coefficients: ~1.5 LCG steps per draw, and every load and
 // store is a coalesced bf16x2 access. Draws are bit-identical to the per-run
 // kernel (same element -> same PCG64 output).
-constexpr int kSeg = 2048;
+// warp segment: one log-time jump (~64 128-bit multiply-adds per lane) per
+// 8192 elements, i.e. per 128 draw pairs of a lane (2048 left the jump as
+// costly as the draws: cfg5 perturbation 17 ms per member)
+constexpr int kSeg = 8192;
 
 __global__ void __launch_bounds__(256) perturb_rows(
     const __nv_bfloat16* __restrict__ Xh0, const __nv_bfloat16* __restrict__ Xl0,
